@@ -1,0 +1,349 @@
+"""Benchmark: fine-grid DOF * F-cycles / s of the B200 multigrid F-cycle.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C4|C5|C1|C3p] [--no-cpu-baseline]
+
+A step is one F-cycle (BASELINE.json metric) on workload C4 by default:
+8191^2 interior unknowns (8193^2 vertices), 13 levels, -Laplace u = f,
+f ~ U[-1,1] from std::mt19937(1), zero start, damped Jacobi 0.7 with 2+2 steps,
+adaptive correction weights, exact-order (reference-identical) reductions.
+Every vector is 537 MB, far larger than the 126 MB L2, so no L2 flush is needed.
+
+value  : device-resident — b and x already in HBM; K cycles of one solve call,
+         timed with CUDA events on the solver stream (max over ranks).
+e2e    : through the public C-ABI solve (gmg_dev_solve) with pinned host buffers:
+         every step uploads b and x, solves to the reference's tolerance and
+         downloads x; wall time of the call; DOF*cycles/s.
+roofline: the finest-level post-smoother (u + omega*P uc, 2 Jacobi steps fused)
+         timed live with CUDA events; 26 B per fine DOF of algorithmic traffic.
+cpu_baseline: the reference compiled from its own sources (oracle/_ref), one
+         F-cycle of the same workload on one host core (the reference has no
+         intra-solve parallelism).
+--impl reference: the same metric from the reference's CPU code on all usable
+         host cores (independent solves in parallel threads), rank 0 only.
+Multi-GPU (N>1 via torchrun): each rank solves its own replica of the workload
+(weak scaling of independent problems; row-slab sharding of one grid is not in
+this build), timing = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: levels, coarse, alpha, beta, smoothing steps, tol, seed_x
+    "C4": dict(levels=13, alpha=1.0, beta=1.0, pre=2, post=2, tol=1e-10, seed_x=0,
+               desc="8191^2 interior (8193^2 vertices), 13 levels, isotropic Poisson, jacobi 0.7 2+2, "
+                    "F-cycle, adaptive omega_l, exact-order reductions"),
+    "C5": dict(levels=14, alpha=1e-2, beta=1.0, pre=3, post=3, tol=1e-30, seed_x=2,
+               desc="16383^2 interior (16385^2 vertices), 14 levels, anisotropic eps=1e-2, jacobi 0.7 3+3, "
+                    "F-cycle, adaptive omega_l, exact-order reductions"),
+    "C1": dict(levels=7, alpha=1.0, beta=1.0, pre=2, post=2, tol=1e-8, seed_x=0,
+               desc="127^2 interior (129^2 vertices), 7 levels, isotropic Poisson, jacobi 0.7 2+2"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[q] for s in self.samples for q in range(4)
+                          if len(s) > 3 + q and s[3 + q].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_fcycle(wl, threads=1, cycles=1, seconds_cap=None):
+    """Times `cycles` F-cycles of the reference (oracle/_ref, else the C port) on
+    `threads` independent solves run concurrently. Returns (DOF*cycles/s, info)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    kind = "reference" if pyoracle.Reference.available() else "port"
+    B = pyoracle.Reference if kind == "reference" else pyoracle.Oracle
+    w = WORKLOADS[wl]
+    t0 = time.time()
+    prob = B(w["levels"], 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+    n = prob.n(w["levels"])
+    b = B.random_vector(n, 1)
+    setup = time.time() - t0
+    spec = pyoracle.CycleSpec(smoother="jacobi", smoother_omega=1.0, smoothing_omega=0.7, pre_steps=w["pre"],
+                              post_steps=w["post"], tolerance=1e-300, max_cycles=cycles)
+    xs = [np.zeros(n) if not w["seed_x"] else B.random_vector(n, w["seed_x"]) for _ in range(threads)]
+    res = [None] * threads
+
+    def run(q):
+        res[q] = prob.solve(spec, b, xs[q])
+
+    ts = time.time()
+    th = [threading.Thread(target=run, args=(q,)) for q in range(threads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    dt = time.time() - ts
+    return threads * n * cycles / dt, dict(kind=kind, setup_s=round(setup, 2), seconds=round(dt, 2), n=n)
+
+
+def usable_threads(n_dof):
+    cores = len(os.sched_getaffinity(0))
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 32 << 30
+    per_solve = 70 * 8 * n_dof  # measured peak transient of one reference F-cycle (~70 vectors)
+    shared = 60 * n_dof  # operators + b
+    by_mem = max(1, int((avail * 0.8 - shared) // per_solve))
+    return max(1, min(cores, by_mem))
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    wl = args.workload
+    w = WORKLOADS[wl]
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    kind = "reference" if pyoracle.Reference.available() else "port"
+    B = pyoracle.Reference if kind == "reference" else pyoracle.Oracle
+    prob = B(w["levels"], 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+    n = prob.n(w["levels"])
+    b = B.random_vector(n, 1)
+    P = usable_threads(n) if args.ref_threads <= 0 else args.ref_threads
+    spec = pyoracle.CycleSpec(smoother="jacobi", smoother_omega=1.0, smoothing_omega=0.7, pre_steps=w["pre"],
+                              post_steps=w["post"], tolerance=1e-300, max_cycles=1)
+    xs = [np.zeros(n) if not w["seed_x"] else B.random_vector(n, w["seed_x"]) for _ in range(P)]
+
+    def step():
+        th = [threading.Thread(target=prob.solve, args=(spec, b, xs[q])) for q in range(P)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.time()
+        step()
+        times.append(time.time() - t0)
+    total = sum(times)
+    value = P * n * args.steps / total
+    line = {
+        "impl": "reference", "metric": "fine-grid DOF*F-cycles/s (fp64)", "value": value,
+        "unit": "DOF*cycles/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1] rhs, std::mt19937)",
+        "config": {"workload": f"{wl}: {w['desc']}", "dof": n},
+        "cpu_baseline": {"value": value, "unit": "DOF*cycles/s", "cores": P, "kind": kind,
+                         "sample": f"each step = 1 F-cycle (gmg::solve, max_cycles=1, incl. its r0/|b| norms) "
+                                   f"of {wl} on each of {P} independent solves in parallel threads"},
+        "e2e": {"value": value, "unit": "DOF*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_0805_3041_b200 import gmg
+
+    wl = args.workload
+    w = WORKLOADS[wl]
+    L = w["levels"]
+    prob = gmg.MultilevelProblem(L, 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"], device=local)
+    n = prob.n(L)
+    b_host = gmg.random_vector(n, 1)
+    x0_host = np.zeros(n) if not w["seed_x"] else gmg.random_vector(n, w["seed_x"])
+    b_dev = torch.from_numpy(b_host).cuda()
+    x_dev = torch.from_numpy(x0_host).cuda()
+    spec_kw = dict(smoother="jacobi", smoother_omega=1.0, smoothing_omega=0.7, pre_steps=w["pre"],
+                   post_steps=w["post"], cycle="F", adaptive_correction=True, reduction=args.reduction)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up: W cycles (captures the CUDA graphs)
+    gmg.solve_device(prob, b_dev.data_ptr(), x_dev.data_ptr(),
+                     gmg.CycleSpec(tolerance=1e-300, max_cycles=max(1, args.warmup), **spec_kw))
+    x_dev.copy_(torch.from_numpy(x0_host))
+    spec = gmg.CycleSpec(tolerance=1e-300, max_cycles=args.steps, **spec_kw)
+    per_cycle = gmg.cycle_kernel_count(prob, spec)
+
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        rep = gmg.solve_device(prob, b_dev.data_ptr(), x_dev.data_ptr(), spec)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    barrier()
+    t = torch.tensor([ms], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = ws * n * args.steps / (ms_max / 1e3)
+
+    # roofline: the finest post-smoother, timed live (CUDA events on the solver stream)
+    peak, peak_src = load_peaks()
+    ms_k, bytes_k = gmg.time_smoother(prob, spec, variant=1, reps=20)
+    achieved = bytes_k / (ms_k / 1e3) / 1e9
+    ms_pre, bytes_pre = gmg.time_smoother(prob, spec, variant=0, reps=20)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(f"{wl}/post_smoother")
+        except Exception:
+            traffic = None
+
+    # e2e: public C-ABI solve with pinned host buffers, to the reference tolerance
+    pin_b = torch.from_numpy(b_host).pin_memory()
+    pin_x = torch.zeros(n, dtype=torch.float64).pin_memory()
+    e2e_spec = gmg.CycleSpec(tolerance=w["tol"] if w["tol"] > 1e-29 else 1e-300,
+                             max_cycles=args.steps if w["tol"] <= 1e-29 else 50, **spec_kw)
+    e2e_cycles, e2e_time = 0, 0.0
+    e2e_steps = max(1, min(args.e2e_steps, args.steps))
+    for _ in range(e2e_steps):
+        xnp = pin_x.numpy()
+        xnp[:] = x0_host
+        barrier()
+        t0 = time.perf_counter()
+        r = gmg.solve(prob, pin_b.numpy(), e2e_spec, xnp)
+        torch.cuda.synchronize()
+        e2e_time += time.perf_counter() - t0
+        e2e_cycles += r.iterations
+    et = torch.tensor([e2e_time], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = ws * n * e2e_cycles / float(et.item())
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, info = cpu_reference_fcycle(wl, threads=1, cycles=1)
+        cpu = {"value": v, "unit": "DOF*cycles/s", "cores": 1, "kind": info["kind"],
+               "sample": f"1 F-cycle of {wl} (gmg::solve max_cycles=1 incl. r0/|b| norms) on 1 host core; "
+                         f"{info['seconds']} s timed, setup {info['setup_s']} s excluded"}
+
+    if rank == 0:
+        hist = rep.residual_history
+        line = {
+            "metric": "fine-grid DOF*F-cycles/s (fp64)", "value": value, "unit": "DOF*cycles/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[-1,1] rhs from std::mt19937, as the reference tests)",
+            "config": {"workload": f"{wl}: {w['desc']}", "dof": n, "cycles_timed": args.steps,
+                       "l2": "inputs larger than L2 (537 MB per vector at C4 vs 126 MB L2); no flush",
+                       "reduction": args.reduction,
+                       "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "residual_first_last": [hist[0], hist[-1]]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_smooth<2,SrcCorrect> finest post-smoother (u+omega*P uc, 2 Jacobi steps)",
+                         "bytes_per_launch": bytes_k, "ms_per_launch": ms_k, "peak_source": peak_src,
+                         "pre_smoother_GBps": bytes_pre / (ms_pre / 1e3) / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "DOF*cycles/s", "h2d_bytes_per_step": 2 * n * 8,
+                    "d2h_bytes_per_step": n * 8 + 8 * 51, "cycles_per_step": e2e_cycles / e2e_steps,
+                    "note": "gmg_dev_solve on pinned host buffers to the reference tolerance"},
+            "gpu_launches": per_cycle * args.steps + 9,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C4")
+    ap.add_argument("--reduction", choices=["exact", "fast"], default="exact")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

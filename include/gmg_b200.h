@@ -1,0 +1,191 @@
+/*
+ * gmg_b200.h — C ABI of the B200-native geometric-multigrid F-cycle
+ * (libgmg_b200.so, sources in paper_0805_3041_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference gmg2d solver path
+ * (/root/reference/proj). The reference has no FFI of its own; its boundary is
+ * the free-function C++ API in namespace gmg, and each entry point below
+ * replaces one of those functions behind plain pointers and sizes:
+ *
+ *   gmg_dev_problem_create  <- gmg::MultilevelProblem ctor   include/gmg/cycle.hpp:66 (src/cycle.cpp:25-30)
+ *   gmg_dev_solve           <- gmg::solve                    include/gmg/cycle.hpp:105-106 (src/cycle.cpp:146-194)
+ *   gmg_dev_mg_cycle        <- gmg::mg_cycle                 include/gmg/cycle.hpp:92-94 (src/cycle.cpp:69-100)
+ *   gmg_dev_apply           <- gmg::apply                    include/gmg/stencil.hpp:44 (src/stencil.cpp:129-146)
+ *   gmg_dev_residual        <- gmg::residual                 include/gmg/stencil.hpp:47 (src/stencil.cpp:148-153)
+ *   gmg_dev_smooth_step     <- gmg::smooth_step (+ setup)    include/gmg/smoother.hpp:73,77-78 (src/smoother.cpp:231-276,389-399)
+ *   gmg_dev_restriction     <- gmg::restriction              include/gmg/transfer.hpp:17 (src/transfer.cpp:72-101)
+ *   gmg_dev_prolongation    <- gmg::prolongation             include/gmg/transfer.hpp:12 (src/transfer.cpp:32-70)
+ *   gmg_dev_adaptive_omega  <- gmg::adaptive_omega           include/gmg/cycle.hpp:86-87 (src/cycle.cpp:40-51)
+ *   gmg_dev_coarse_solve    <- gmg::BandedCholesky::solve    include/gmg/stencil.hpp:54 (src/stencil.cpp:190-210)
+ *   gmg_dev_norm_l2/dot/axpy<- gmg::norm_l2 / dot / axpy     include/gmg/grid_function.hpp:29-34 (src/stencil.cpp:9-31)
+ *
+ * Exceptions become status codes; the C++ shim
+ * include/gmg_b200.hpp re-throws the reference's own exception types.
+ *
+ * Layout at the boundary: every grid function is the reference's
+ * GridFunction::v — interior nodes only, row-major with x fastest,
+ * k = j*nx + i (include/gmg/grid_function.hpp:10-26). Host pointers unless a
+ * function name says _devptr. All arithmetic is IEEE fp64 in the reference's
+ * operation order; results are bit-identical to the reference.
+ */
+#ifndef GMG_B200_H
+#define GMG_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes -------------------------------------------------------- */
+#define GMG_OK 0
+#define GMG_ERR_LOGIC 1       /* std::logic_error: shape/level mismatch */
+#define GMG_ERR_INVALID 2     /* std::invalid_argument: bad omega, steps, ... */
+#define GMG_ERR_RUNTIME 3     /* std::runtime_error: nonpositive energy, not SPD */
+#define GMG_DIVERGED 4        /* gmg::DivergenceError; report is filled */
+#define GMG_ERR_CUDA 5        /* CUDA failure (no device, OOM, launch error) */
+#define GMG_ERR_UNSUPPORTED 6 /* a spec this build does not implement */
+
+/* ---- enums: same order as the reference enums ----------------------------- */
+/* gmg::SmootherKind, include/gmg/smoother.hpp:13-25 */
+enum gmg_smoother_kind {
+    GMG_SMOOTHER_RICHARDSON = 0,
+    GMG_SMOOTHER_JACOBI = 1,
+    GMG_SMOOTHER_GAUSS_SEIDEL = 2,
+    GMG_SMOOTHER_SOR = 3,
+    GMG_SMOOTHER_ILU0 = 4,
+    GMG_SMOOTHER_TRI_X = 5,
+    GMG_SMOOTHER_TRI_Y = 6,
+    GMG_SMOOTHER_ADI = 7,
+    GMG_SMOOTHER_GSTRI_X = 8,
+    GMG_SMOOTHER_GSTRI_Y = 9,
+    GMG_SMOOTHER_GSADI = 10
+};
+/* gmg::CycleType, include/gmg/cycle.hpp:17 */
+enum gmg_cycle_type { GMG_CYCLE_V = 0, GMG_CYCLE_W = 1, GMG_CYCLE_F = 2 };
+/* gmg::CoordinateSystem, include/gmg/mesh.hpp:8 */
+enum gmg_coords { GMG_CARTESIAN = 0, GMG_CYLINDRICAL = 1, GMG_SPHERICAL = 2 };
+/* how dot products / norms are summed on the device */
+enum gmg_reduction {
+    GMG_REDUCE_EXACT = 0, /* bit-identical to the reference's left-to-right sum */
+    GMG_REDUCE_FAST = 1   /* tree reduction (not bit-identical; ~1e-13 relative) */
+};
+
+/* ---- problem description --------------------------------------------------- */
+/* One level of a gmg::MultilevelProblem: LevelGrid (mesh.hpp:37-48) + StencilOperator
+ * (stencil.hpp:20-34). All arrays are host memory, copied at create time. */
+typedef struct gmg_level_desc {
+    int level;       /* 1 = coarsest */
+    int nx, ny;      /* interior points */
+    const double* x; /* nx+2 node coordinates incl. boundary */
+    const double* y; /* ny+2 */
+    const double *c, *n, *s, *e, *w; /* nx*ny each */
+} gmg_level_desc;
+
+typedef struct gmg_problem_desc {
+    int num_levels;
+    const gmg_level_desc* levels; /* levels[0] = level 1 */
+    int device;                   /* CUDA ordinal */
+} gmg_problem_desc;
+
+/* gmg::CycleSpec, include/gmg/cycle.hpp:23-39 (+ SmootherSpec) */
+typedef struct gmg_cycle_desc {
+    int cycle;               /* gmg_cycle_type */
+    int pre_steps;
+    int post_steps;
+    int adaptive_correction; /* 1: energy-norm minimiser (adaptive_omega) */
+    double correction_omega;
+    int smoother_kind;       /* gmg_smoother_kind */
+    double smoother_omega;
+    double smoothing_omega;  /* outer damping of each smooth_step */
+    double tolerance;
+    int max_cycles;
+    unsigned long long coarse_direct_max_neq; /* ULLONG_MAX = unlimited */
+    int reduction;           /* gmg_reduction */
+} gmg_cycle_desc;
+
+/* gmg::SolveReport, include/gmg/cycle.hpp:41-47. Buffers are caller-owned. */
+typedef struct gmg_solve_report {
+    int iterations;
+    int converged;
+    double wall_seconds;
+    double* residual_history;    /* capacity >= max_cycles + 1 */
+    double* convergence_factors; /* capacity >= max_cycles, may be NULL */
+    int history_len;
+    char message[256];
+} gmg_solve_report;
+
+typedef struct gmg_problem gmg_problem;
+
+/* Thread-local text of the last failure (exception message in the reference). */
+const char* gmg_last_error(void);
+/* Library build string (arch, reduction engine version). */
+const char* gmg_version(void);
+
+/* ---- problem lifecycle ----------------------------------------------------- */
+int gmg_dev_problem_create(const gmg_problem_desc* desc, gmg_problem** out);
+int gmg_dev_problem_destroy(gmg_problem* p);
+int gmg_dev_num_levels(const gmg_problem* p);
+int gmg_dev_level_shape(const gmg_problem* p, int level, int* nx, int* ny);
+/* operator storage chosen at create: 0 = constant 5-point, 1 = x-varying rows, 2 = full field */
+int gmg_dev_level_coef_kind(const gmg_problem* p, int level);
+
+/* ---- the hot path ---------------------------------------------------------- */
+/* gmg::solve: b read, x_inout carries the start vector in and the solution out.
+ * Host pointers (nx*ny doubles, reference layout). */
+int gmg_dev_solve(gmg_problem* p, const gmg_cycle_desc* spec, const double* b, double* x_inout,
+                  gmg_solve_report* report);
+/* Same, with b and x already resident on the device (reference layout, nx*ny
+ * doubles each). Used by the benchmark's device-resident leg. */
+int gmg_dev_solve_devptr(gmg_problem* p, const gmg_cycle_desc* spec, const double* b_dev,
+                         double* x_dev, gmg_solve_report* report);
+/* gmg::mg_cycle on level `level` (u0, g in, u out; host pointers). */
+int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, const double* u0,
+                     const double* g, double* u);
+
+/* ---- per-operator entry points (host arrays; unit parity) ------------------- */
+int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y);
+int gmg_dev_residual(gmg_problem* p, int level, const double* x, const double* b, double* r);
+int gmg_dev_smooth_step(gmg_problem* p, int level, int smoother_kind, double smoother_omega,
+                        double omega_damp, const double* x, const double* b, double* out);
+int gmg_dev_restriction(gmg_problem* p, int fine_level, const double* fine, double* coarse);
+int gmg_dev_prolongation(gmg_problem* p, int coarse_level, const double* coarse, double* fine);
+int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* defect,
+                           const double* correction, double* omega);
+int gmg_dev_coarse_solve(gmg_problem* p, const double* b, double* x);
+int gmg_dev_norm_l2(gmg_problem* p, long long n, const double* v, int reduction, double* out);
+int gmg_dev_dot(gmg_problem* p, long long n, const double* a, const double* b, int reduction,
+                double* out);
+int gmg_dev_axpy(gmg_problem* p, long long n, double alpha, const double* x, double* y);
+
+/* ---- measurement hooks (bench.py) ------------------------------------------ */
+/* Times `reps` back-to-back launches of the finest-level Jacobi smoother kernel
+ * exactly as the F-cycle launches it, with CUDA events on the solver stream.
+ * variant 0: pre-smoothing of the top visit (u0 = P e streamed from the coarse
+ * level; 18 B/DOF algorithmic: g in, coarse e in, u out), 1: post-smoothing
+ * (u + omega P uc; 26 B/DOF: u, g in, coarse uc in, u out), 2: plain smoother
+ * from u (24 B/DOF). Writes the average ms per launch and the algorithmic
+ * bytes per launch. */
+int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int variant, int reps,
+                          double* ms_per_launch, double* bytes_per_launch);
+/* Number of kernels one solver cycle launches (from the captured graph). */
+int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* count);
+
+/* ---- host-side setup helpers (no device work) ------------------------------ */
+/* gmg::build_hierarchy + gmg::assemble (mesh.cpp:103-138, stencil.cpp:77-127)
+ * followed by gmg_dev_problem_create. */
+int gmg_host_problem_create(int num_levels, int coarse_nx, int coarse_ny, double grading_x,
+                            double grading_y, int coords, double alpha, double beta, int device,
+                            gmg_problem** out);
+/* std::mt19937(seed) + uniform_real_distribution<double>(-1,1), the reference test
+ * recipe (tests/oracles.hpp:252-258). */
+void gmg_host_random_vector(long long n, unsigned seed, double* out);
+/* Host emulation of the device exact-order summation engine (same chunking,
+ * speculation and record chain), for CPU tests of its logic. */
+int gmg_host_seqsum_emulate(long long n, const double* terms, int threads_per_chunk,
+                            int elems_per_thread, double* out, long long* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,75 @@
+"""In-tree build of libgmg_b200.so (sm_100a) — no JIT caches, so the built
+library travels to the GPU box with the repo snapshot.
+
+    python -m paper_0805_3041_b200.build [--force]
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(ROOT, "build", "gmg_b200")
+LIB = os.path.join(PKG, "libgmg_b200.so")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -fmad=false: no FMA contraction anywhere (bit-exact with the reference's
+# unfused x86-64 arithmetic); -ffp-contract=off for the host code likewise.
+NVFLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
+           "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-Xptxas", "-v"]
+CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall"]
+
+SOURCES_CU = ["solver.cu"]
+SOURCES_CPP = ["host_setup.cpp"]
+DEPS = ["common.cuh", "march.cuh", "seqsum.cuh", "seqsum_core.h", "host_setup.h",
+        os.path.join("..", "..", "include", "gmg_b200.h")]
+
+
+def _newer(target: str, sources) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def _run(cmd, log):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    with open(log, "a") as f:
+        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr + "\n")
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ... (see {log})")
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    log = os.path.join(BUILD, "build.log")
+    deps = [os.path.join(CSRC, d) for d in DEPS]
+    objs = []
+    for src in SOURCES_CU:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _newer(o, [s, *deps]):
+            if verbose:
+                print("nvcc", src, flush=True)
+            _run([NVCC, *NVFLAGS, "-c", s, "-o", o], log)
+        objs.append(o)
+    for src in SOURCES_CPP:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src + ".o")
+        if force or _newer(o, [s, *deps]):
+            if verbose:
+                print("g++", src, flush=True)
+            _run(["g++", *CXXFLAGS, "-c", s, "-o", o], log)
+        objs.append(o)
+    if force or _newer(LIB, objs):
+        _run([NVCC, "-shared", *ARCH, "-Xcompiler", "-fPIC", *objs, "-o", LIB], log)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,164 @@
+// Shared device definitions for the B200 multigrid path.
+//
+// Data layout in HBM: every level-l grid function lives in a
+// pitched buffer, element (i,j) at base[j*pitch + i], pitch = nx rounded up to
+// 32 doubles (256 B rows), base 256-B aligned, with a zero ghost ring
+// (row -1, row ny, column -1 == previous row's padding, column nx..pitch-1).
+// Kernels never write ghosts; all neighbour reads are guarded explicitly, so
+// a ghost contributes coefficient * (+0), which is the identity on the
+// accumulator exactly as the reference's skipped term (stencil.cpp:134-144).
+//
+// All arithmetic is fp64 in the reference's association order. The library is
+// compiled with -fmad=false: no multiply-add contraction anywhere (SURVEY.md
+// Appendix A); fused ops appear only inside correctly-rounded helpers that are
+// bit-identical to the unfused IEEE result.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gmg_dev {
+
+constexpr int kWarp = 32;
+
+struct Grid {
+    int nx, ny;
+    long long pitch;
+    __host__ __device__ long long at(int i, int j) const { return (long long)j * pitch + i; }
+    __host__ __device__ bool inside(int i, int j) const { return i >= 0 && i < nx && j >= 0 && j < ny; }
+};
+
+// ---------------------------------------------------------------------------
+// Operator storage classes (classified on the host from the reference's five
+// StencilOperator arrays, stencil.hpp:20-28).
+//   CONST : c, w, e, s, n identical on every interior row/column and exactly 0
+//           toward the boundary (cartesian uniform grids, all BASELINE configs
+//           but C3): 0 B/DOF of coefficient traffic.
+//   ROWX  : coefficients depend on i only (uniform cylindrical, C3'): 1-D tables.
+//   FIELD : general graded / spherical: five pitched arrays.
+// `div_by_c` is the Jacobi preconditioner z = r / c (smoother.cpp:293-295):
+// a true IEEE division, or a multiplication by the exact reciprocal when c is a
+// power of two (identical result).
+// ---------------------------------------------------------------------------
+struct CoefConst {
+    double c, w, e, s, n;
+    double inv_c;  // exact reciprocal (valid only when c_pow2)
+    int c_pow2;
+    __device__ __forceinline__ void load(int, int, double& C, double& W, double& E, double& S,
+                                         double& N) const {
+        C = c;
+        W = w;
+        E = e;
+        S = s;
+        N = n;
+    }
+    __device__ __forceinline__ double diag(int, int) const { return c; }
+    __device__ __forceinline__ double div_by_c(double r, int, int) const {
+        return c_pow2 ? r * inv_c : r / c;
+    }
+};
+
+struct CoefRowX {
+    const double *c, *w, *e, *s, *n;  // length nx each
+    __device__ __forceinline__ void load(int i, int, double& C, double& W, double& E, double& S,
+                                         double& N) const {
+        C = __ldg(c + i);
+        W = __ldg(w + i);
+        E = __ldg(e + i);
+        S = __ldg(s + i);
+        N = __ldg(n + i);
+    }
+    __device__ __forceinline__ double diag(int i, int) const { return __ldg(c + i); }
+    __device__ __forceinline__ double div_by_c(double r, int i, int) const { return r / __ldg(c + i); }
+};
+
+struct CoefField {
+    const double *c, *w, *e, *s, *n;  // pitched like the level's grid functions
+    long long pitch;
+    __device__ __forceinline__ void load(int i, int j, double& C, double& W, double& E, double& S,
+                                         double& N) const {
+        const long long k = (long long)j * pitch + i;
+        C = __ldg(c + k);
+        W = __ldg(w + k);
+        E = __ldg(e + k);
+        S = __ldg(s + k);
+        N = __ldg(n + k);
+    }
+    __device__ __forceinline__ double diag(int i, int j) const { return __ldg(c + (long long)j * pitch + i); }
+    __device__ __forceinline__ double div_by_c(double r, int i, int j) const {
+        return r / __ldg(c + (long long)j * pitch + i);
+    }
+};
+
+// y = (A x)(i,j) in the reference's order c, w, e, s, n (stencil.cpp:133-137).
+template <class Coef>
+__device__ __forceinline__ double stencil_apply(const Coef& A, int i, int j, double xc, double xw,
+                                                double xe, double xs, double xn) {
+    double C, W, E, S, N;
+    A.load(i, j, C, W, E, S, N);
+    double acc = C * xc;
+    acc = acc + W * xw;
+    acc = acc + E * xe;
+    acc = acc + S * xs;
+    acc = acc + N * xn;
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Grid transfers (transfer.cpp). Weights are host-precomputed 1-D tables with
+// the reference's own expressions (odd_weight, transfer.cpp:26-28).
+// ---------------------------------------------------------------------------
+struct Prolong {
+    const double* uc;  // coarse grid function (pitched)
+    Grid cg;           // coarse grid
+    const double* tx;  // per fine column i: odd_weight for odd node index pi=i+1
+    const double* ty;  // per fine row j
+    __device__ __forceinline__ double cval(int ci, int cj) const {
+        return cg.inside(ci, cj) ? __ldg(uc + cg.at(ci, cj)) : 0.0;
+    }
+    // Fine interior point (i,j) — transfer.cpp:43-68 term for term.
+    __device__ __forceinline__ double at(int i, int j) const {
+        const int pi = i + 1, pj = j + 1;
+        if ((pi & 1) == 0 && (pj & 1) == 0) return cval(pi / 2 - 1, pj / 2 - 1);
+        if ((pi & 1) == 1 && (pj & 1) == 0) {
+            const int qx = (pi - 1) / 2;
+            const double t = __ldg(tx + i);
+            return (1.0 - t) * cval(qx - 1, pj / 2 - 1) + t * cval(qx, pj / 2 - 1);
+        }
+        if ((pi & 1) == 0 && (pj & 1) == 1) {
+            const int qy = (pj - 1) / 2;
+            const double t = __ldg(ty + j);
+            return (1.0 - t) * cval(pi / 2 - 1, qy - 1) + t * cval(pi / 2 - 1, qy);
+        }
+        const int qx = (pi - 1) / 2, qy = (pj - 1) / 2;
+        const double tX = __ldg(tx + i), tY = __ldg(ty + j);
+        double v = (1.0 - tX) * (1.0 - tY) * cval(qx - 1, qy - 1);
+        v = v + tX * (1.0 - tY) * cval(qx, qy - 1);
+        v = v + (1.0 - tX) * tY * cval(qx - 1, qy);
+        v = v + tX * tY * cval(qx, qy);
+        return v;
+    }
+};
+
+struct RestrictW {
+    // per coarse column P (0-based): west/east odd weights and the 1-D sum sx;
+    // per coarse row Q likewise (transfer.cpp:80-85)
+    const double *wxw, *wxe, *sx, *wys, *wyn, *sy;
+};
+
+// Full-weighting restriction of fine values f at coarse (P,Q), 9 terms in the
+// reference's dj-outer / di-inner order from acc = 0 (transfer.cpp:86-97).
+// `F(di, dj)` returns the fine value at fine interior (2P+1+di, 2Q+1+dj).
+template <class F>
+__device__ __forceinline__ double restrict_at(const RestrictW& rw, int P, int Q, F&& f) {
+    const double wx[3] = {__ldg(rw.wxw + P), 1.0, __ldg(rw.wxe + P)};
+    const double wy[3] = {__ldg(rw.wys + Q), 1.0, __ldg(rw.wyn + Q)};
+    double acc = 0.0;
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj)
+#pragma unroll
+        for (int di = -1; di <= 1; ++di) acc = acc + wx[di + 1] * wy[dj + 1] * f(di, dj);
+    return acc / (__ldg(rw.sx + P) * __ldg(rw.sy + Q));
+}
+
+}  // namespace gmg_dev

@@ -1,0 +1,349 @@
+// Host setup for the B200 multigrid path. Compiled with -ffp-contract=off so
+// every expression rounds exactly as the reference's.
+#include "host_setup.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "seqsum_core.h"
+
+namespace gmg_host {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;  // std::numbers::pi
+
+// grade_axis (mesh.cpp:48-75): n interior nodes, geometric cell widths.
+std::vector<double> graded_unit_axis(int n, double ratio) {
+    if (n < 1) throw std::invalid_argument("grade_axis: n must be >= 1");
+    if (!(ratio > 0.0)) throw std::invalid_argument("grade_axis: factor must be > 0");
+    const int cells = n + 1;
+    const double first = ratio == 1.0 ? 1.0 / cells : (ratio - 1.0) / (std::pow(ratio, cells) - 1.0);
+    std::vector<double> u(static_cast<std::size_t>(n) + 2);
+    u[0] = 0.0;
+    double h = first;
+    for (int q = 1; q <= n; ++q) {
+        u[q] = u[q - 1] + h;
+        h *= ratio;
+    }
+    u[n + 1] = 1.0;
+    for (int q = 0; q <= n; ++q)
+        if (!(u[q] < u[q + 1])) throw std::invalid_argument("grade_axis: factor too extreme for n points");
+    return u;
+}
+
+// axis_range (mesh.cpp:25-36) then physical_axis (mesh.cpp:79-93).
+std::vector<double> mapped_axis(int n, double ratio, int coords, int axis) {
+    double lo = 0.0, hi = 1.0;
+    if (coords == 1 && axis == 0) lo = 0.1;
+    if (coords == 2) {
+        lo = 0.1;
+        if (axis == 1) hi = kPi - 0.1;
+    }
+    std::vector<double> p = graded_unit_axis(n, ratio);
+    for (double& v : p) v = lo + (hi - lo) * v;
+    p.front() = lo;
+    p.back() = hi;
+    for (std::size_t q = 0; q + 1 < p.size(); ++q)
+        if (!(p[q] < p[q + 1]))
+            throw std::invalid_argument("grading: factor too extreme for this resolution and axis range");
+    return p;
+}
+
+// Flux-form coefficients (stencil.cpp:49-73).
+double face_x(int cs, double x) { return cs == 0 ? 1.0 : (cs == 1 ? x : x * x); }
+double face_y(int cs, double y) { return cs == 2 ? std::sin(y) : 1.0; }
+double measure_x(int cs, double a, double b) { return cs == 1 ? 0.5 * (b * b - a * a) : b - a; }
+double measure_y(int cs, double a, double b) { return cs == 2 ? std::cos(a) - std::cos(b) : b - a; }
+
+void assemble_level(Level& L, int cs, double alpha, double beta) {
+    const int nx = L.nx, ny = L.ny;
+    const std::size_t N = static_cast<std::size_t>(nx) * ny;
+    L.c.assign(N, 0.0);
+    L.n.assign(N, 0.0);
+    L.s.assign(N, 0.0);
+    L.e.assign(N, 0.0);
+    L.w.assign(N, 0.0);
+    for (int j = 0; j < ny; ++j) {
+        const double ys = 0.5 * (L.y[j] + L.y[j + 1]);
+        const double yn = 0.5 * (L.y[j + 1] + L.y[j + 2]);
+        const double dys = L.y[j + 1] - L.y[j];
+        const double dyn = L.y[j + 2] - L.y[j + 1];
+        const double my = measure_y(cs, ys, yn);
+        for (int i = 0; i < nx; ++i) {
+            const double xw = 0.5 * (L.x[i] + L.x[i + 1]);
+            const double xe = 0.5 * (L.x[i + 1] + L.x[i + 2]);
+            const double dxw = L.x[i + 1] - L.x[i];
+            const double dxe = L.x[i + 2] - L.x[i + 1];
+            const double mx = measure_x(cs, xw, xe);
+            const double fe = alpha * face_x(cs, xe) * my / dxe;
+            const double fw = alpha * face_x(cs, xw) * my / dxw;
+            const double fn = beta * face_y(cs, yn) * mx / dyn;
+            const double fs = beta * face_y(cs, ys) * mx / dys;
+            const std::size_t k = static_cast<std::size_t>(j) * nx + i;
+            L.c[k] = fe + fw + fn + fs;
+            if (i + 1 < nx) L.e[k] = -fe;
+            if (i > 0) L.w[k] = -fw;
+            if (j + 1 < ny) L.n[k] = -fn;
+            if (j > 0) L.s[k] = -fs;
+        }
+    }
+}
+
+bool same_bits(double a, double b) { return std::memcmp(&a, &b, sizeof(double)) == 0; }
+
+}  // namespace
+
+std::vector<Level> build_problem(int num_levels, int cnx, int cny, double gx, double gy, int coords,
+                                 double alpha, double beta) {
+    if (num_levels < 1) throw std::invalid_argument("levels: must be >= 1");
+    if (cnx < 1 || cny < 1) throw std::invalid_argument("coarse_n: interior counts must be >= 1");
+    if (!(gx > 0.0) || !(gy > 0.0)) throw std::invalid_argument("grading: factors must be > 0");
+    if (coords < 0 || coords > 2) throw std::invalid_argument("coords: unknown coordinate system");
+    if (!(alpha > 0.0) || !(beta > 0.0)) throw std::invalid_argument("alpha/beta must be > 0");
+    std::vector<Level> lv(static_cast<std::size_t>(num_levels));
+    Level& f = lv.back();
+    f.level = num_levels;
+    f.nx = ((cnx + 1) << (num_levels - 1)) - 1;
+    f.ny = ((cny + 1) << (num_levels - 1)) - 1;
+    f.x = mapped_axis(f.nx, gx, coords, 0);
+    f.y = mapped_axis(f.ny, gy, coords, 1);
+    for (int l = num_levels - 1; l >= 1; --l) {
+        const Level& fine = lv[l];
+        Level& coarse = lv[l - 1];
+        coarse.level = l;
+        coarse.nx = (fine.nx - 1) / 2;
+        coarse.ny = (fine.ny - 1) / 2;
+        coarse.x.resize(static_cast<std::size_t>(coarse.nx) + 2);
+        coarse.y.resize(static_cast<std::size_t>(coarse.ny) + 2);
+        for (std::size_t q = 0; q < coarse.x.size(); ++q) coarse.x[q] = fine.x[2 * q];
+        for (std::size_t q = 0; q < coarse.y.size(); ++q) coarse.y[q] = fine.y[2 * q];
+    }
+    for (Level& L : lv) assemble_level(L, coords, alpha, beta);
+    return lv;
+}
+
+std::vector<double> cholesky_band(const double* c, const double* w, const double* s, int nx, int ny) {
+    const int n = nx * ny, bw = nx;
+    std::vector<double> band(static_cast<std::size_t>(bw + 1) * n, 0.0);
+    auto B = [&](int d, int k) -> double& { return band[static_cast<std::size_t>(d) * n + k]; };
+    for (int k = 0; k < n; ++k) {
+        B(0, k) = c[k];
+        if (k % nx != 0) B(1, k) = w[k];
+        if (k >= nx) B(bw, k) = s[k];
+    }
+    for (int col = 0; col < n; ++col) {
+        double d = B(0, col);
+        for (int m = std::max(0, col - bw); m < col; ++m) {
+            const double l = B(col - m, col);
+            d -= l * l;
+        }
+        if (!(d > 0.0)) throw std::runtime_error("BandedCholesky: matrix not positive definite");
+        const double piv = std::sqrt(d);
+        B(0, col) = piv;
+        for (int row = col + 1; row <= std::min(n - 1, col + bw); ++row) {
+            double a = B(row - col, row);
+            for (int m = std::max(0, row - bw); m < col; ++m) a -= B(row - m, row) * B(col - m, col);
+            B(row - col, row) = a / piv;
+        }
+    }
+    return band;
+}
+
+CoefClass classify(int nx, int ny, const double* c, const double* n, const double* s, const double* e,
+                   const double* w) {
+    CoefClass cc;
+    const std::size_t N = static_cast<std::size_t>(nx) * ny;
+    // reference interior values (the row/column that has the neighbour)
+    const double C = c[0];
+    const double W = nx > 1 ? w[1] : 0.0;
+    const double E = nx > 1 ? e[0] : 0.0;
+    const double S = ny > 1 ? s[nx] : 0.0;
+    const double Nn = ny > 1 ? n[0] : 0.0;
+    bool isconst = true;
+    for (std::size_t k = 0; k < N && isconst; ++k) {
+        const int i = static_cast<int>(k % nx), j = static_cast<int>(k / nx);
+        isconst = same_bits(c[k], C) && same_bits(w[k], i > 0 ? W : 0.0) &&
+                  same_bits(e[k], i + 1 < nx ? E : 0.0) && same_bits(s[k], j > 0 ? S : 0.0) &&
+                  same_bits(n[k], j + 1 < ny ? Nn : 0.0);
+    }
+    if (isconst) {
+        cc.kind = COEF_CONST;
+        cc.c = C;
+        cc.w = W;
+        cc.e = E;
+        cc.s = S;
+        cc.n = Nn;
+        return cc;
+    }
+    // x-varying rows: every row equals row 0 except s (0 on row 0) and n (0 on the last row)
+    bool rowx = true;
+    for (int j = 0; j < ny && rowx; ++j)
+        for (int i = 0; i < nx && rowx; ++i) {
+            const std::size_t k = static_cast<std::size_t>(j) * nx + i;
+            const double Si = ny > 1 ? s[static_cast<std::size_t>(nx) + i] : 0.0;
+            rowx = same_bits(c[k], c[i]) && same_bits(w[k], w[i]) && same_bits(e[k], e[i]) &&
+                   same_bits(s[k], j > 0 ? Si : 0.0) && same_bits(n[k], j + 1 < ny ? n[i] : 0.0);
+        }
+    if (rowx) {
+        cc.kind = COEF_ROWX;
+        cc.rc.assign(c, c + nx);
+        cc.rw.assign(w, w + nx);
+        cc.re.assign(e, e + nx);
+        cc.rs.resize(nx);
+        for (int i = 0; i < nx; ++i) cc.rs[i] = ny > 1 ? s[static_cast<std::size_t>(nx) + i] : 0.0;
+        cc.rn.assign(n, n + nx);
+        return cc;
+    }
+    cc.kind = COEF_FIELD;
+    return cc;
+}
+
+static double odd_w(const std::vector<double>& xf, const std::vector<double>& xc, int q) {
+    return (xf[2 * q + 1] - xc[q]) / (xc[q + 1] - xc[q]);
+}
+
+std::vector<double> prolong_weights(const std::vector<double>& xf, const std::vector<double>& xc, int nf) {
+    std::vector<double> t(static_cast<std::size_t>(nf), 0.0);
+    for (int i = 0; i < nf; ++i)
+        if ((i + 1) % 2 == 1) t[i] = odd_w(xf, xc, i / 2);
+    return t;
+}
+
+void restrict_weights(const std::vector<double>& xf, const std::vector<double>& xc, int nc,
+                      std::vector<double>& ww, std::vector<double>& we, std::vector<double>& sw) {
+    ww.resize(nc);
+    we.resize(nc);
+    sw.resize(nc);
+    for (int P = 0; P < nc; ++P) {
+        ww[P] = odd_w(xf, xc, P);
+        we[P] = 1.0 - odd_w(xf, xc, P + 1);
+        sw[P] = ww[P] + 1.0 + we[P];
+    }
+}
+
+std::string check_nested(const Level& coarse, const Level& fine) {
+    if (fine.level != coarse.level + 1 || fine.nx != 2 * coarse.nx + 1 || fine.ny != 2 * coarse.ny + 1)
+        return "levels are not parent and child";
+    for (int q = 0; q < coarse.nx + 2; ++q)
+        if (std::abs(coarse.x[q] - fine.x[2 * q]) > 1e-14) return "grids are not nested";
+    for (int q = 0; q < coarse.ny + 2; ++q)
+        if (std::abs(coarse.y[q] - fine.y[2 * q]) > 1e-14) return "grids are not nested";
+    return "";
+}
+
+// ---------------------------------------------------------------------------
+// Host emulation of the device pipeline (seqsum.cuh) with identical chunking:
+// S1 approximate chunk sums, S2 approximate prefix, S3 per-thread speculative
+// walks + segmented merge into per-chunk records, S4 exact chain with
+// fallback. stats: [0] chunks, [1] records, [2] fallbacks, [3] breaks.
+double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* stats) {
+    using namespace gmg_ss;
+    const long long C = static_cast<long long>(T) * EPT;
+    const long long nch = (n + C - 1) / C;
+    const int RMAX = 256;
+    std::vector<double> csum(nch, 0.0), cpred(nch, 0.0);
+    for (long long c = 0; c < nch; ++c) {
+        double a = 0.0;
+        for (long long k = c * C; k < std::min(n, (c + 1) * C); ++k) a += p[k];
+        csum[c] = a;
+    }
+    double run = 0.0;
+    for (long long c = 0; c < nch; ++c) {
+        cpred[c] = run;
+        run += csum[c];
+    }
+    std::vector<std::vector<Rec>> recs(nch);
+    std::vector<int> dirty(nch, 0);
+    long long nbreaks = 0;
+    for (long long c = 0; c < nch; ++c) {
+        const long long base = c * C;
+        const int clen = static_cast<int>(std::min(C, n - base));
+        std::vector<double> pred(T);
+        double acc = cpred[c];
+        for (int t = 0; t < T; ++t) {
+            pred[t] = acc;
+            double ts = 0.0;
+            for (int m = 0; m < EPT; ++m) {
+                const int e = t * EPT + m;
+                if (e < clen) ts += p[base + e];
+            }
+            acc += ts;
+        }
+        Seg carry = seg_empty();
+        int carry_f = 0;
+        std::vector<Rec> out;
+        for (int t = 0; t < T; ++t) {
+            State st = make_state(pred[t]);
+            Seg cur = seg_empty();
+            bool first = true;
+            for (int m = 0; m < EPT; ++m) {
+                const int e = t * EPT + m;
+                if (e >= clen) break;
+                const double v = p[base + e];
+                if (!walk_try(st, cur, v)) {
+                    ++nbreaks;
+                    if (first) {
+                        out.push_back(rec_make(seg_merge(carry, cur), true, v));
+                        first = false;
+                    } else {
+                        out.push_back(rec_make(cur, true, v));
+                    }
+                    cur = seg_empty();
+                    real_add(st, v);
+                }
+            }
+            if (first) {
+                carry = seg_merge(carry, cur);
+            } else {
+                carry = cur;
+                carry_f = 1;
+            }
+        }
+        (void)carry_f;
+        out.push_back(rec_make(carry, false, 0.0));
+        if (static_cast<int>(out.size()) > RMAX) dirty[c] = 1;
+        recs[c] = std::move(out);
+    }
+    long long nrec = 0, nfb = 0;
+    State st = make_state(0.0);
+    for (long long c = 0; c < nch; ++c) {
+        const long long base = c * C;
+        const int clen = static_cast<int>(std::min(C, n - base));
+        int pos = 0;
+        bool fb = dirty[c] != 0;
+        if (!fb) {
+            for (const Rec& r : recs[c]) {
+                ++nrec;
+                const Seg g = rec_seg(r);
+                if (!seg_valid(g, st)) {
+                    fb = true;
+                    break;
+                }
+                seg_apply(g, st);
+                pos += g.len;
+                if (rec_has_break(r)) {
+                    real_add(st, r.pb);
+                    pos += 1;
+                }
+            }
+        }
+        if (fb) {
+            ++nfb;
+            double s = st.s;
+            for (int e = pos; e < clen; ++e) s = s + p[base + e];
+            st = make_state(s);
+        }
+    }
+    if (stats) {
+        stats[0] = nch;
+        stats[1] = nrec;
+        stats[2] = nfb;
+        stats[3] = nbreaks;
+    }
+    return st.s;
+}
+
+}  // namespace gmg_host

@@ -1,0 +1,50 @@
+// Host-side (CPU) setup for the device problem: hierarchy + assembly for the
+// standalone API, the level-1 banded Cholesky factor, operator classification
+// and transfer weight tables. Setup runs once per problem and stays on the host
+// (SURVEY.md §3.2); only its products are uploaded.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace gmg_host {
+
+struct Level {
+    int level = 1, nx = 0, ny = 0;
+    std::vector<double> x, y;               // nx+2 / ny+2 node coordinates
+    std::vector<double> c, n, s, e, w;      // nx*ny each, reference layout
+};
+
+// gmg::build_hierarchy + gmg::assemble (mesh.cpp:48-138, stencil.cpp:49-127).
+// Throws std::invalid_argument with the reference's messages.
+std::vector<Level> build_problem(int num_levels, int coarse_nx, int coarse_ny, double grading_x,
+                                 double grading_y, int coords, double alpha, double beta);
+
+// BandedCholesky ctor (stencil.cpp:155-188): band[d*n + k] = L(k, k-d),
+// half bandwidth nx. Throws std::runtime_error if not SPD.
+std::vector<double> cholesky_band(const double* c, const double* w, const double* s, int nx, int ny);
+
+// Operator classification (see common.cuh).
+enum CoefKind { COEF_CONST = 0, COEF_ROWX = 1, COEF_FIELD = 2 };
+struct CoefClass {
+    CoefKind kind = COEF_FIELD;
+    double c = 0, w = 0, e = 0, s = 0, n = 0;            // CONST
+    std::vector<double> rc, rw, re, rs, rn;              // ROWX tables (length nx)
+};
+CoefClass classify(int nx, int ny, const double* c, const double* n, const double* s,
+                   const double* e, const double* w);
+
+// odd_weight (transfer.cpp:26-28) tables.
+// Prolongation (fine level f from coarse cx): tx[i] for fine column i (odd node i+1).
+std::vector<double> prolong_weights(const std::vector<double>& xf, const std::vector<double>& xc, int nf);
+// Restriction onto coarse: per coarse column P: wxw, wxe, sx (transfer.cpp:80-85).
+void restrict_weights(const std::vector<double>& xf, const std::vector<double>& xc, int nc,
+                      std::vector<double>& ww, std::vector<double>& we, std::vector<double>& sw);
+// require_nested (transfer.cpp:10-22); returns an error message or "".
+std::string check_nested(const Level& coarse, const Level& fine);
+
+// CPU emulation of the device exact-order summation engine.
+double seqsum_emulate(const double* terms, long long n, int threads, int ept, long long* stats);
+
+}  // namespace gmg_host

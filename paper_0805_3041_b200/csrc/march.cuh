@@ -1,0 +1,332 @@
+// Row-streaming ("marching") stencil kernels for sm_100a.
+//
+// Each CTA owns a strip of TW columns (one thread per column) and a segment of
+// rows, and walks the rows upward. For an M-step smoother the CTA carries M
+// pipeline levels: at iteration J it loads input row J, produces level-1 row
+// J-1, level-2 row J-2, ... and writes level-M row J-M. Vertical neighbours of
+// a thread's own column live in registers (a 3-row window per level);
+// horizontal neighbours come from a double-buffered shared-memory row per
+// level, so one __syncthreads per row suffices. Each input row is read from HBM
+// once and each output row written once: M Jacobi steps cost 24 B/DOF of
+// compulsory traffic (x, g in; x' out) instead of 24*M. Strips overlap by M
+// columns on each side (recomputed halo), segments by M rows.
+//
+// Inputs are fetched PF rows ahead into registers so each SM keeps enough
+// bytes in flight to saturate HBM3e.
+//
+// Reference semantics reproduced per point (one Jacobi smooth_step,
+// smoother.cpp:389-399 with :293-295, apply from stencil.cpp:129-146):
+//     acc = c*x + w*xw + e*xe + s*xs + n*xn      (ghosts = +0)
+//     d   = acc - g
+//     z   = d / c
+//     x'  = x - omega*z
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace gmg_dev {
+
+// ---------------- level-0 sources ------------------------------------------
+// fetch() issues the loads for fine point (i,j) (returns zeros outside the
+// interior); make() finishes the value. Splitting them lets the loads run PF
+// rows ahead of the arithmetic.
+
+struct SrcZero {  // u0 = 0 (inner V-cycle visits, cycle.cpp:89)
+    struct Raw {};
+    __device__ __forceinline__ void prepare(int) {}
+    __device__ __forceinline__ Raw fetch(int, int) const { return Raw{}; }
+    __device__ __forceinline__ double make(const Raw&, int, int) const { return 0.0; }
+};
+
+struct SrcU {  // u0 = u
+    const double* u;
+    Grid g;
+    struct Raw {
+        double v;
+    };
+    __device__ __forceinline__ void prepare(int) {}
+    __device__ __forceinline__ Raw fetch(int i, int j) const {
+        return Raw{g.inside(i, j) ? __ldg(u + g.at(i, j)) : 0.0};
+    }
+    __device__ __forceinline__ double make(const Raw& r, int, int) const { return r.v; }
+};
+
+struct SrcSum {  // x + e: fcycle_pass's out = x; axpy(1.0, e, out) (cycle.cpp:139-140)
+    const double *x, *e;
+    Grid g;
+    struct Raw {
+        double a, b;
+    };
+    __device__ __forceinline__ void prepare(int) {}
+    __device__ __forceinline__ Raw fetch(int i, int j) const {
+        if (!g.inside(i, j)) return Raw{0.0, 0.0};
+        const long long k = g.at(i, j);
+        return Raw{__ldg(x + k), __ldg(e + k)};
+    }
+    __device__ __forceinline__ double make(const Raw& r, int, int) const { return r.a + 1.0 * r.b; }
+};
+
+// Coarse-to-fine bilinear prolongation evaluated while streaming the fine rows.
+struct ProlongRaw {
+    double a, b, c, d, ty;
+};
+__device__ __forceinline__ ProlongRaw prolong_fetch(const Prolong& P, int i, int j, int fnx, int fny) {
+    ProlongRaw r{0.0, 0.0, 0.0, 0.0, 0.0};
+    if (i < 0 || i >= fnx || j < 0 || j >= fny) return r;
+    const int pi = i + 1, pj = j + 1;
+    const int ci = (pi & 1) ? (pi - 1) / 2 - 1 : pi / 2 - 1;  // left/only coarse column
+    const int cj = (pj & 1) ? (pj - 1) / 2 - 1 : pj / 2 - 1;  // lower/only coarse row
+    r.a = P.cval(ci, cj);
+    if (pi & 1) r.b = P.cval(ci + 1, cj);
+    if (pj & 1) {
+        r.c = P.cval(ci, cj + 1);
+        if (pi & 1) r.d = P.cval(ci + 1, cj + 1);
+        r.ty = __ldg(P.ty + j);
+    }
+    return r;
+}
+// transfer.cpp:53,57,63-64 term order
+__device__ __forceinline__ double prolong_make(const ProlongRaw& r, int i, int j, double tX) {
+    const int pi = i + 1, pj = j + 1;
+    if (!(pi & 1) && !(pj & 1)) return r.a;
+    if ((pi & 1) && !(pj & 1)) return (1.0 - tX) * r.a + tX * r.b;
+    if (!(pi & 1) && (pj & 1)) return (1.0 - r.ty) * r.a + r.ty * r.c;
+    const double tY = r.ty;
+    double v = (1.0 - tX) * (1.0 - tY) * r.a;
+    v = v + tX * (1.0 - tY) * r.b;
+    v = v + (1.0 - tX) * tY * r.c;
+    v = v + tX * tY * r.d;
+    return v;
+}
+
+struct SrcProlong {  // u0 = P e (fcycle_pass, cycle.cpp:135)
+    Prolong P;
+    int fnx, fny;
+    double tX;
+    using Raw = ProlongRaw;
+    __device__ __forceinline__ void prepare(int i) {
+        tX = (i >= 0 && i < fnx && ((i + 1) & 1)) ? __ldg(P.tx + i) : 0.0;
+    }
+    __device__ __forceinline__ Raw fetch(int i, int j) const { return prolong_fetch(P, i, j, fnx, fny); }
+    __device__ __forceinline__ double make(const Raw& r, int i, int j) const {
+        return prolong_make(r, i, j, tX);
+    }
+};
+
+// Adaptive correction weight (cycle.cpp:40-51) finished from the device sums
+// of the exact-order engine: sums[0] = (A corr, corr), sums[1] = (d, corr),
+// *nz = 1 iff some corr_k*corr_k != 0 (i.e. the reference's nc != 0).
+struct OmegaSrc {
+    const double* sums;  // null => fixed omega
+    const int* nz;
+    double fixed;
+    int* status;  // set to 3 (runtime_error) on nonpositive energy
+    __device__ __forceinline__ double get(bool report) const {
+        if (!sums) return fixed;
+        if (!*nz) return 1.0;
+        const double den = sums[0];
+        if (!(den > 0.0)) {
+            if (report) atomicCAS(status, 0, 3);
+            return 0.0;
+        }
+        return sums[1] / den;
+    }
+};
+
+struct SrcCorrect {  // u + omega * P uc  (axpy(wl, corr, u), cycle.cpp:93-96)
+    const double* u;
+    Grid g;
+    Prolong P;
+    double omega;
+    double tX;
+    struct Raw {
+        double u;
+        ProlongRaw p;
+    };
+    __device__ __forceinline__ void prepare(int i) {
+        tX = (i >= 0 && i < g.nx && ((i + 1) & 1)) ? __ldg(P.tx + i) : 0.0;
+    }
+    __device__ __forceinline__ Raw fetch(int i, int j) const {
+        Raw r;
+        r.u = g.inside(i, j) ? __ldg(u + g.at(i, j)) : 0.0;
+        r.p = prolong_fetch(P, i, j, g.nx, g.ny);
+        return r;
+    }
+    __device__ __forceinline__ double make(const Raw& r, int i, int j) const {
+        return r.u + omega * prolong_make(r.p, i, j, tX);
+    }
+};
+
+// ---------------- M-step Jacobi smoother ----------------------------------
+template <class Coef>
+__device__ __forceinline__ double jacobi_point(const Coef& A, int i, int j, double xc, double xw,
+                                               double xe, double xs, double xn, double g,
+                                               double omega) {
+    const double acc = stencil_apply(A, i, j, xc, xw, xe, xs, xn);
+    const double d = acc - g;
+    const double z = A.div_by_c(d, i, j);
+    return xc - omega * z;
+}
+
+// Launch: grid (ceil(nx/(TW-2M)), ceil(ny/seg)), block TW.
+// For SrcCorrect the correction weight is finished in the prologue from `om`.
+template <int M, int TW, int PF, class Coef, class Src>
+__global__ void __launch_bounds__(TW) k_smooth(Grid fg, Coef A, Src src, OmegaSrc om,
+                                               const double* __restrict__ g,
+                                               double* __restrict__ out, double omega_damp, int seg) {
+    constexpr int OUTW = TW - 2 * M;
+    constexpr int ML = M > 0 ? M : 1;
+    __shared__ double sh[2][ML][TW];
+
+    const int t = threadIdx.x;
+    const int i = blockIdx.x * OUTW - M + t;
+    const int j0 = blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.ny);
+    const bool col_in = i >= 0 && i < fg.nx;
+    const bool owner = col_in && t >= M && t < TW - M;
+
+    src.prepare(i);
+    if constexpr (std::is_same<Src, SrcCorrect>::value) {
+        src.omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && t == 0);
+    }
+
+    double win[ML][3];
+    double gring[ML];
+#pragma unroll
+    for (int l = 0; l < ML; ++l) {
+        win[l][0] = win[l][1] = win[l][2] = 0.0;
+        gring[l] = 0.0;
+    }
+
+    const int Jbeg = j0 - M;
+    const int Jend = j1 - 1 + M;  // inclusive
+    typename Src::Raw q[PF];
+    double gq[PF];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+        const int Jf = Jbeg + p;
+        q[p] = src.fetch(i, Jf);
+        gq[p] = (M > 0 && col_in && Jf >= 0 && Jf < fg.ny) ? __ldg(g + fg.at(i, Jf)) : 0.0;
+    }
+
+    for (int Jb = Jbeg; Jb <= Jend; Jb += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int J = Jb + p;
+            if (J > Jend) break;  // uniform across the CTA
+            const typename Src::Raw raw = q[p];
+            const double gnew = gq[p];
+            {
+                const int Jf = J + PF;
+                q[p] = src.fetch(i, Jf);
+                gq[p] = (M > 0 && col_in && Jf >= 0 && Jf < fg.ny) ? __ldg(g + fg.at(i, Jf)) : 0.0;
+            }
+            const bool row_in = J >= 0 && J < fg.ny;
+            double nv = (col_in && row_in) ? src.make(raw, i, J) : 0.0;
+            if constexpr (M == 0) {
+                if (owner && J >= j0 && J < j1) out[fg.at(i, J)] = nv;
+            } else {
+                const int pb = (J - 1) & 1, cb = J & 1;
+#pragma unroll
+                for (int l = 0; l < M; ++l) {
+                    win[l][0] = win[l][1];
+                    win[l][1] = win[l][2];
+                    win[l][2] = nv;
+                    sh[cb][l][t] = nv;
+                    const int R = J - l - 1;
+                    const double xl = t > 0 ? sh[pb][l][t - 1] : 0.0;
+                    const double xr = t < TW - 1 ? sh[pb][l][t + 1] : 0.0;
+                    const double y = jacobi_point(A, i, R, win[l][1], xl, xr, win[l][0], win[l][2],
+                                                  gring[l], omega_damp);
+                    nv = (col_in && R >= 0 && R < fg.ny) ? y : 0.0;
+                }
+                const int RM = J - M;
+                if (owner && RM >= j0 && RM < j1) out[fg.at(i, RM)] = nv;
+#pragma unroll
+                for (int l = ML - 1; l > 0; --l) gring[l] = gring[l - 1];
+                gring[0] = gnew;
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// ---------------- residual (+ restriction) ---------------------------------
+// d = g - A x0 (stencil.cpp:148-153), optionally stored; x0 optionally stored;
+// optionally g_c = R d (transfer.cpp:72-101) for the next coarser level.
+// Strip stride TW-4, halo 2 columns; segments of `seg` rows (seg even).
+template <int TW, int PF, class Coef, class Src>
+__global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const double* __restrict__ g,
+                                              double* __restrict__ dout, double* __restrict__ x0out,
+                                              Grid cg, RestrictW rw, double* __restrict__ gc, int seg) {
+    const bool STORE_D = dout != nullptr, STORE_X0 = x0out != nullptr, RESTRICT = gc != nullptr;
+    constexpr int OUTW = TW - 4;
+    __shared__ double xs[2][TW];
+    __shared__ double dr[4][TW];
+
+    const int t = threadIdx.x;
+    const int i = blockIdx.x * OUTW - 2 + t;
+    const int j0 = blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.ny);
+    const bool col_in = i >= 0 && i < fg.nx;
+    const bool owner = col_in && t >= 2 && t < TW - 2;
+    src.prepare(i);
+
+    double a = 0.0, b = 0.0, c = 0.0;  // x0 rows J-2, J-1, J in own column
+    const int Jbeg = j0 - 1;
+    const int Jend = j1 + 1;
+    typename Src::Raw q[PF];
+    double gq[PF];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+        const int Jf = Jbeg + p;
+        q[p] = src.fetch(i, Jf);
+        gq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(g + fg.at(i, Jf - 1)) : 0.0;
+    }
+    for (int Jb = Jbeg; Jb <= Jend; Jb += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int J = Jb + p;
+            if (J > Jend) break;
+            const typename Src::Raw raw = q[p];
+            const double gR = gq[p];  // g at row J-1
+            {
+                const int Jf = J + PF;
+                q[p] = src.fetch(i, Jf);
+                gq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(g + fg.at(i, Jf - 1)) : 0.0;
+            }
+            const bool row_in = J >= 0 && J < fg.ny;
+            const double x0 = (col_in && row_in) ? src.make(raw, i, J) : 0.0;
+            if (STORE_X0 && owner && J >= j0 && J < j1) x0out[fg.at(i, J)] = x0;
+            a = b;
+            b = c;
+            c = x0;
+            const int R = J - 1;
+            const double xl = t > 0 ? xs[(J - 1) & 1][t - 1] : 0.0;
+            const double xr = t < TW - 1 ? xs[(J - 1) & 1][t + 1] : 0.0;
+            xs[J & 1][t] = x0;
+            double d = 0.0;
+            if (col_in && R >= 0 && R < fg.ny) d = gR - stencil_apply(A, i, R, b, xl, xr, a, c);
+            if (STORE_D && owner && R >= j0 && R < j1) dout[fg.at(i, R)] = d;
+            if (RESTRICT) dr[R & 3][t] = d;
+            __syncthreads();
+            if (RESTRICT) {
+                // coarse row Q whose centre fine row 2Q+1 = R-1 is owned
+                if (((R & 1) == 0) && R >= 2 && R - 1 >= j0 && R - 1 < j1 && owner && (i & 1)) {
+                    const int Q = R / 2 - 1;
+                    const int P = (i - 1) / 2;
+                    if (P < cg.nx && Q < cg.ny) {
+                        const double v = restrict_at(rw, P, Q, [&](int di, int dj) {
+                            return dr[(R - 1 + dj) & 3][t + di];
+                        });
+                        gc[cg.at(P, Q)] = v;
+                    }
+                }
+            }
+        }
+    }
+}
+
+}  // namespace gmg_dev

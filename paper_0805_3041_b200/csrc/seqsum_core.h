@@ -1,0 +1,226 @@
+// Exact emulation of the reference's left-to-right fp64 summation
+//   double s = 0.0; for (k) s += p[k];      (stencil.cpp:9-13,21-26; cycle.cpp:44)
+// split into parallel pieces. Shared by the CUDA kernels (seqsum.cuh) and the
+// host emulation used by the CPU tests (host_seqsum.cpp).
+//
+// Idea: while the running sum s stays inside one binade
+// [2^(e-1), 2^e) its representable neighbours are the multiples of
+// u = ulp(s) = 2^(e-53), so fl(s + p) = s + u*RN(p/u) — the sum is an exact
+// integer prefix sum M_k = s/u + sum q_j with q_j = RN(p_j/u). Only three
+// situations need a real IEEE add ("break"): the state is zero/subnormal/huge,
+// p/u is an exact half-integer (tie, resolved by the parity of the total), or
+// the integer state would leave the open binade (|M| outside [2^52+1, 2^53-1];
+// the +1 keeps a result that lands just below 2^(e-1), where the spacing halves,
+// out of the integer model).
+//
+// A *segment* is a run of elements summed in one binade; it is described by
+// (E, sign, Q, minP, maxP): Q is the integer total in units of u, minP/maxP the
+// extremes of its inclusive prefixes. Given the EXACT state M entering it, a
+// segment is valid iff E and sign match and M+minP, M+maxP stay in range —
+// then the exit state is exactly M+Q. Segments merge associatively when E and
+// sign agree. A *record* is a segment optionally followed by one break element
+// whose value is applied with a real add. The device walks every thread's
+// elements from a speculated start (an approximate prefix) to discover where
+// breaks happen; a short serial chain then replays the records from the exact
+// state, validating each segment and falling back to real adds if a
+// speculation was wrong. Correctness never depends on the speculation.
+#pragma once
+
+#include <stdint.h>
+#include <string.h>
+
+#ifdef __CUDACC__
+#define SS_HD __host__ __device__ __forceinline__
+#else
+#define SS_HD inline
+#endif
+
+namespace gmg_ss {
+
+constexpr int64_t kLo = (int64_t(1) << 52) + 1;  // smallest admissible |M| after a step
+constexpr int64_t kHi = (int64_t(1) << 53) - 1;  // largest admissible |M|
+constexpr double kTwo52 = 4503599627370496.0;
+constexpr int kEMin = 64;    // usable biased exponents: u = 2^(E-1075) and
+constexpr int kEMax = 2040;  // 2^(1075-E) both normal, far from overflow
+
+SS_HD uint64_t dbits(double x) {
+#ifdef __CUDA_ARCH__
+    return static_cast<uint64_t>(__double_as_longlong(x));
+#else
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    return b;
+#endif
+}
+SS_HD double bitsd(uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(b));
+#else
+    double x;
+    memcpy(&x, &b, 8);
+    return x;
+#endif
+}
+
+// Decomposed running sum: E = biased exponent (0 if not usable), M = signed
+// integer significand (s = M * 2^(E-1075)), inv_u = 2^(1075-E).
+struct State {
+    double s;
+    int E;
+    int64_t M;
+    double inv_u;
+};
+
+SS_HD State make_state(double s) {
+    State st;
+    st.s = s;
+    const uint64_t b = dbits(s);
+    const int E = static_cast<int>((b >> 52) & 0x7ff);
+    if (E < kEMin || E > kEMax) {
+        st.E = 0;
+        st.M = 0;
+        st.inv_u = 0.0;
+        return st;
+    }
+    int64_t m = static_cast<int64_t>((b & ((uint64_t(1) << 52) - 1)) | (uint64_t(1) << 52));
+    st.E = E;
+    st.M = (b >> 63) ? -m : m;
+    st.inv_u = bitsd(static_cast<uint64_t>(1075 + 1023 - E) << 52);  // 2^(1075-E)
+    return st;
+}
+
+// Value of integer state M in binade E (|M| in [2^52, 2^53)). Exact.
+SS_HD double compose(int64_t M, int E) {
+    const uint64_t neg = M < 0 ? 1u : 0u;
+    const uint64_t a = static_cast<uint64_t>(M < 0 ? -M : M);
+    return bitsd((neg << 63) | (static_cast<uint64_t>(E) << 52) | (a - (uint64_t(1) << 52)));
+}
+
+struct Seg {
+    int E;     // binade of the segment (meaningless when len == 0)
+    int neg;   // sign of the running sum inside the segment
+    int len;   // number of elements; 0 = empty (identity for merge)
+    int bad;   // 1 = produced by merging incompatible segments (forces a fallback)
+    int64_t Q, mn, mx;
+};
+
+SS_HD Seg seg_empty() {
+    Seg s;
+    s.E = 0;
+    s.neg = 0;
+    s.len = 0;
+    s.bad = 0;
+    s.Q = 0;
+    s.mn = 0;
+    s.mx = 0;
+    return s;
+}
+
+SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
+    if (a.len == 0 && !a.bad) return b;
+    if (b.len == 0 && !b.bad) return a;
+    Seg r;
+    r.E = a.E;
+    r.neg = a.neg;
+    r.len = a.len + b.len;
+    r.bad = a.bad | b.bad | (a.E != b.E) | (a.neg != b.neg);
+    r.Q = a.Q + b.Q;
+    const int64_t bmn = a.Q + b.mn, bmx = a.Q + b.mx;
+    r.mn = a.mn < bmn ? a.mn : bmn;
+    r.mx = a.mx > bmx ? a.mx : bmx;
+    return r;
+}
+
+// Is the segment valid from exact state st? (len == 0 is always valid.)
+SS_HD bool seg_valid(const Seg& g, const State& st) {
+    if (g.len == 0) return !g.bad;
+    if (g.bad || st.E == 0 || st.E != g.E || (st.M < 0) != (g.neg != 0)) return false;
+    if (!g.neg) return st.M + g.mn >= kLo && st.M + g.mx <= kHi;
+    return st.M + g.mx <= -kLo && st.M + g.mn >= -kHi;
+}
+
+// Apply a valid segment.
+SS_HD void seg_apply(const Seg& g, State& st) {
+    if (g.len == 0) return;
+    st.M += g.Q;
+    st.s = compose(st.M, st.E);
+}
+
+// Sequential walker: advances a (speculated or exact) state element by element,
+// accumulating the current segment, reporting breaks. Returns true if element p
+// was absorbed into the current segment, false if it is a break (the caller
+// closes the segment, then calls real_add).
+SS_HD bool walk_try(State& st, Seg& cur, double p) {
+    if (st.E == 0) return false;
+    const double x = p * st.inv_u;  // exact power-of-two scaling
+    if (!(x < kTwo52 && x > -kTwo52)) return false;
+#ifdef __CUDA_ARCH__
+    const double fl = floor(x);
+    const double q = rint(x);
+#else
+    const double fl = __builtin_floor(x);
+    const double q = __builtin_rint(x);
+#endif
+    if (x - fl == 0.5) return false;  // exact tie: rounding depends on the total's parity
+    const int64_t qi = static_cast<int64_t>(q);
+    const int64_t Mn = st.M + qi;
+    if (st.M >= 0) {
+        if (Mn < kLo || Mn > kHi) return false;
+    } else {
+        if (Mn > -kLo || Mn < -kHi) return false;
+    }
+    st.M = Mn;
+    if (cur.len == 0) {
+        cur.E = st.E;
+        cur.neg = st.M < 0;
+        cur.Q = qi;
+        cur.mn = qi;
+        cur.mx = qi;
+    } else {
+        cur.Q += qi;
+        cur.mn = cur.Q < cur.mn ? cur.Q : cur.mn;
+        cur.mx = cur.Q > cur.mx ? cur.Q : cur.mx;
+    }
+    cur.len += 1;
+    return true;
+}
+
+// The reference's own step s = s + p, from the exact (integer) state.
+SS_HD void real_add(State& st, double p) {
+    const double s = (st.E != 0 ? compose(st.M, st.E) : st.s) + p;
+    st = make_state(s);
+}
+
+// Record as stored for the chain: segment, then optionally one break element.
+struct Rec {
+    int64_t Q, mn, mx;
+    double pb;         // break element value
+    uint32_t meta;     // E (11b) | neg<<11 | has_break<<12 | bad<<13
+    int32_t len;       // segment length (elements); break element not counted
+};
+
+SS_HD Rec rec_make(const Seg& g, bool has_break, double pb) {
+    Rec r;
+    r.Q = g.Q;
+    r.mn = g.mn;
+    r.mx = g.mx;
+    r.pb = pb;
+    r.meta = static_cast<uint32_t>(g.E & 0x7ff) | (static_cast<uint32_t>(g.neg) << 11) |
+             (static_cast<uint32_t>(has_break) << 12) | (static_cast<uint32_t>(g.bad) << 13);
+    r.len = g.len;
+    return r;
+}
+SS_HD Seg rec_seg(const Rec& r) {
+    Seg g;
+    g.E = static_cast<int>(r.meta & 0x7ff);
+    g.neg = static_cast<int>((r.meta >> 11) & 1);
+    g.bad = static_cast<int>((r.meta >> 13) & 1);
+    g.len = r.len;
+    g.Q = r.Q;
+    g.mn = r.mn;
+    g.mx = r.mx;
+    return g;
+}
+SS_HD bool rec_has_break(const Rec& r) { return (r.meta >> 12) & 1; }
+
+}  // namespace gmg_ss

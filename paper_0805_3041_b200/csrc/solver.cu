@@ -1,0 +1,1206 @@
+// B200-native geometric multigrid: device problem, cycle driver, C ABI.
+//
+// The cycle driver mirrors gmg::solve / fcycle_pass / mg_cycle
+// (/root/reference/proj/src/cycle.cpp:69-194) but is executed as a CUDA graph:
+// one F-cycle (defect cascade, coarse solve, one V-cycle per level with the
+// adaptive correction weight computed on the device, the x+e update, the new
+// residual and its exact-order norm) is captured once per cycle spec and
+// replayed; the host only reads back the residual norm to run the reference's
+// stopping and divergence tests.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gmg_b200.h"
+#include "common.cuh"
+#include "host_setup.h"
+#include "march.cuh"
+#include "seqsum.cuh"
+
+using namespace gmg_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct GmgError {
+    int code;
+    std::string msg;
+};
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess)                                                                 \
+            throw GmgError{GMG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};     \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return GMG_OK;
+    } catch (const GmgError& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return GMG_ERR_INVALID;
+    } catch (const std::logic_error& e) {
+        g_last_error = e.what();
+        return GMG_ERR_LOGIC;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return GMG_ERR_CUDA;
+    } catch (const std::runtime_error& e) {
+        g_last_error = e.what();
+        return GMG_ERR_RUNTIME;
+    }
+}
+
+enum Buf { U0 = 0, U1 = 1, DCAS = 2, GRHS = 3, DD = 4, NBUF = 5 };
+
+struct Lev {
+    int l = 1, nx = 0, ny = 0;
+    long long pitch = 0;
+    size_t elems = 0, off0 = 0;
+    double* mem = nullptr;
+    double* buf[NBUF] = {};
+    int kind = 2;
+    CoefConst cconst{};
+    CoefRowX crow{};
+    CoefField cfield{};
+    double* coefmem = nullptr;
+    double *tx = nullptr, *ty = nullptr;  // prolongation weights (this level as fine)
+    RestrictW rw{};                       // restriction weights (this level as coarse)
+    double* wmem = nullptr;
+    std::vector<double> hx, hy;
+    Grid grid() const { return Grid{nx, ny, pitch}; }
+    long long n() const { return (long long)nx * ny; }
+};
+
+}  // namespace
+
+struct gmg_problem {
+    int L = 0, device = 0;
+    cudaStream_t st = nullptr;
+    std::mutex mu;
+    std::vector<Lev> lv;
+    double* xmem = nullptr;
+    double* X[2] = {nullptr, nullptr};
+    double* B = nullptr;
+    double* band = nullptr;
+    double* cscr = nullptr;
+    int cn = 0, cbw = 0;
+    // exact-order summation workspace
+    int nch_max = 0;
+    double *csum = nullptr, *cpred = nullptr;
+    int* counts = nullptr;
+    gmg_ss::Rec* recs = nullptr;
+    double* sums = nullptr;  // [0..1] omega sums, [2] residual norm^2, [3] misc
+    int* nz = nullptr;
+    int* status = nullptr;
+    double* hostbuf = nullptr;  // pinned: {norm^2, status}
+    std::map<std::string, std::array<cudaGraphExec_t, 2>> graphs;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    Lev& lev(int l) { return lv.at(l - 1); }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// simple (non-streaming) kernels
+// ---------------------------------------------------------------------------
+__global__ void k_restrict_simple(Grid fg, const double* __restrict__ f, Grid cg, RestrictW rw,
+                                  double* __restrict__ c) {
+    const int P = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Q = blockIdx.y * blockDim.y + threadIdx.y;
+    if (P >= cg.nx || Q >= cg.ny) return;
+    c[cg.at(P, Q)] = restrict_at(rw, P, Q, [&](int di, int dj) {
+        return __ldg(f + fg.at(2 * P + 1 + di, 2 * Q + 1 + dj));
+    });
+}
+
+__global__ void k_prolong_simple(Prolong P, Grid fg, double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= fg.nx || j >= fg.ny) return;
+    out[fg.at(i, j)] = P.at(i, j);
+}
+
+template <class Coef>
+__global__ void k_apply_simple(Grid g, Coef A, const double* __restrict__ x, double* __restrict__ y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= g.nx || j >= g.ny) return;
+    auto X = [&](int a, int b) { return g.inside(a, b) ? __ldg(x + g.at(a, b)) : 0.0; };
+    y[g.at(i, j)] = stencil_apply(A, i, j, X(i, j), X(i - 1, j), X(i + 1, j), X(i, j - 1), X(i, j + 1));
+}
+
+__global__ void k_axpy_flat(long long n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) y[k] = y[k] + a * x[k];
+}
+
+// BandedCholesky::solve (stencil.cpp:190-210): forward then backward
+// substitution in the reference's d-loop order, one thread (level 1 is tiny).
+__global__ void k_coarse_chol(const double* __restrict__ band, int n, int bw, Grid g,
+                              const double* __restrict__ b, double* __restrict__ x,
+                              double* __restrict__ xs) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int k = 0; k < n; ++k) {
+        double acc = b[g.at(k % g.nx, k / g.nx)];
+        const int dm = min(bw, k);
+        for (int d = 1; d <= dm; ++d) acc = acc - band[(long long)d * n + k] * xs[k - d];
+        xs[k] = acc / band[k];
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        double acc = xs[k];
+        const int dm = min(bw, n - 1 - k);
+        for (int d = 1; d <= dm; ++d) acc = acc - band[(long long)d * n + k + d] * xs[k + d];
+        xs[k] = acc / band[k];
+    }
+    for (int k = 0; k < n; ++k) x[g.at(k % g.nx, k / g.nx)] = xs[k];
+}
+
+// Fast (tree-order) reduction finisher: sums the chunk partials of S1.
+__global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, double* __restrict__ out) {
+    __shared__ double red[32];
+    for (int s = 0; s < ns; ++s) {
+        double a = 0.0;
+        for (int c = threadIdx.x; c < nch; c += blockDim.x) a += csum[(long long)s * nch + c];
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            out[s] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// adaptive_omega on two explicit arrays (unit op): (A corr, corr) and (d, corr).
+template <class Coef>
+struct OmegaTermsField {
+    static constexpr int NS = 2;
+    const double *d, *cr;
+    Grid g;
+    Coef A;
+    __device__ __forceinline__ double C(int i, int j) const {
+        return g.inside(i, j) ? __ldg(cr + g.at(i, j)) : 0.0;
+    }
+    __device__ __forceinline__ void get(long long k, double (&p)[2], int& nz) const {
+        const int j = (int)(k / g.nx), i = (int)(k - (long long)j * g.nx);
+        const double cc = C(i, j);
+        const double ac = stencil_apply(A, i, j, cc, C(i - 1, j), C(i + 1, j), C(i, j - 1), C(i, j + 1));
+        p[0] = ac * cc;
+        p[1] = __ldg(d + g.at(i, j)) * cc;
+        nz = (cc * cc) != 0.0;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+constexpr int kTW = 128;
+
+int seg_rows(int ny) { return ny <= 128 ? ((ny + 1) & ~1) : 128; }
+
+template <class F>
+void with_coef(const Lev& L, F&& f) {
+    if (L.kind == 0) f(L.cconst);
+    else if (L.kind == 1) f(L.crow);
+    else f(L.cfield);
+}
+
+template <class T>
+void set_smem(T* fn, size_t bytes) {
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)bytes));
+}
+
+template <class TG>
+void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int* nz, int mode) {
+    constexpr int NS = TG::NS;
+    const int nch = (int)((n + kSsC - 1) / kSsC);
+    if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
+    static bool attr_done = false;
+    if (!attr_done) {
+        set_smem(k_ss_walk<TG>, ss_walk_smem(NS));
+        set_smem(k_ss_chain<TG>, ss_chain_smem());
+        attr_done = true;
+    }
+    if (nz) CK(cudaMemsetAsync(nz, 0, sizeof(int), p->st));
+    k_ss_partial<TG><<<nch, kSsT, 0, p->st>>>(tg, n, p->csum, nch, nz);
+    if (mode == GMG_REDUCE_FAST) {
+        k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out);
+        return;
+    }
+    k_ss_scan<NS><<<1, 1024, 0, p->st>>>(p->csum, p->cpred, nch);
+    k_ss_walk<TG><<<nch, kSsT, ss_walk_smem(NS), p->st>>>(tg, n, p->cpred, nch, p->counts, p->recs);
+    k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, nch, p->counts, p->recs, out);
+}
+
+Prolong prolong_from(gmg_problem* p, int coarse_level, const double* uc) {
+    const Lev& C = p->lev(coarse_level);
+    const Lev& F = p->lev(coarse_level + 1);
+    return Prolong{uc, C.grid(), F.tx, F.ty};
+}
+
+enum Start { S_ZERO = 0, S_U = 1, S_PROLONG = 2, S_CORRECT = 3, S_SUM = 4 };
+
+struct SmoothSrc {
+    Start kind = S_ZERO;
+    const double* u = nullptr;   // S_U, S_CORRECT
+    const double* uc = nullptr;  // S_PROLONG, S_CORRECT: coarse grid function (level l-1)
+    OmegaSrc om{nullptr, nullptr, 1.0, nullptr};
+};
+
+template <int M, class Coef, class Src>
+void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, OmegaSrc om,
+                     const double* g, double* out, double wd) {
+    constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
+    const int seg = seg_rows(L.ny);
+    dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.ny + seg - 1) / seg);
+    k_smooth<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
+    CK(cudaGetLastError());
+}
+
+template <int M, class Coef>
+void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
+                       double* out, double wd) {
+    switch (s.kind) {
+        case S_ZERO:
+            launch_smooth_t<M>(p, L, A, SrcZero{}, s.om, g, out, wd);
+            break;
+        case S_U:
+            launch_smooth_t<M>(p, L, A, SrcU{s.u, L.grid()}, s.om, g, out, wd);
+            break;
+        case S_PROLONG: {
+            SrcProlong src{prolong_from(p, L.l - 1, s.uc), L.nx, L.ny, 0.0};
+            launch_smooth_t<M>(p, L, A, src, s.om, g, out, wd);
+            break;
+        }
+        case S_CORRECT: {
+            SrcCorrect src{s.u, L.grid(), prolong_from(p, L.l - 1, s.uc), 0.0, 0.0};
+            launch_smooth_t<M>(p, L, A, src, s.om, g, out, wd);
+            break;
+        }
+        default:
+            throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
+    }
+}
+
+// One launch of M <= 4 Jacobi steps.
+void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, const double* g, double* out,
+                   double wd) {
+    with_coef(L, [&](const auto& A) {
+        switch (M) {
+            case 0: launch_smooth_src<0>(p, L, A, s, g, out, wd); break;
+            case 1: launch_smooth_src<1>(p, L, A, s, g, out, wd); break;
+            case 2: launch_smooth_src<2>(p, L, A, s, g, out, wd); break;
+            case 3: launch_smooth_src<3>(p, L, A, s, g, out, wd); break;
+            case 4: launch_smooth_src<4>(p, L, A, s, g, out, wd); break;
+            default: throw GmgError{GMG_ERR_LOGIC, "smooth: M > 4"};
+        }
+    });
+}
+
+constexpr int kMaxFuse = 4;
+
+// `steps` smoothing steps from source s; writes alternate between bufA and
+// bufB (first launch -> bufA). Returns the buffer holding the result.
+double* smooth_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const double* g, double* bufA,
+                     double* bufB, double wd) {
+    double* dst = bufA;
+    int left = steps;
+    bool first = true;
+    while (first || left > 0) {
+        const int M = std::min(left, kMaxFuse);
+        launch_smooth(p, L, M, s, g, dst, wd);
+        left -= M;
+        first = false;
+        s = SmoothSrc{};
+        s.kind = S_U;
+        s.u = dst;
+        if (left > 0) dst = (dst == bufA) ? bufB : bufA;
+    }
+    return dst;
+}
+
+template <class Coef, class Src>
+void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, const double* g,
+                    double* dout, double* x0out, double* gc) {
+    const int seg = seg_rows(L.ny);
+    dim3 grid((L.nx + (kTW - 4) - 1) / (kTW - 4), (L.ny + seg - 1) / seg);
+    Grid cg{0, 0, 0};
+    RestrictW rw{};
+    if (gc) {
+        const Lev& C = p->lev(L.l - 1);
+        cg = C.grid();
+        rw = C.rw;
+    }
+    constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
+    k_resid<kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg);
+    CK(cudaGetLastError());
+}
+
+// residual of (u, or x+e when e != null) against g; optional outputs.
+void launch_resid(gmg_problem* p, const Lev& L, const double* u, const double* e, const double* g,
+                  double* dout, double* x0out, double* gc) {
+    with_coef(L, [&](const auto& A) {
+        if (e)
+            launch_resid_t(p, L, A, SrcSum{u, e, L.grid()}, g, dout, x0out, gc);
+        else
+            launch_resid_t(p, L, A, SrcU{u, L.grid()}, g, dout, x0out, gc);
+    });
+}
+
+void launch_restrict(gmg_problem* p, int fine_level, const double* f, double* c) {
+    const Lev& F = p->lev(fine_level);
+    const Lev& C = p->lev(fine_level - 1);
+    dim3 b(32, 8), gr((C.nx + 31) / 32, (C.ny + 7) / 8);
+    k_restrict_simple<<<gr, b, 0, p->st>>>(F.grid(), f, C.grid(), C.rw, c);
+    CK(cudaGetLastError());
+}
+
+void launch_coarse(gmg_problem* p, const double* g, double* x) {
+    const Lev& L = p->lev(1);
+    k_coarse_chol<<<1, 32, 0, p->st>>>(p->band, p->cn, p->cbw, L.grid(), g, x, p->cscr);
+    CK(cudaGetLastError());
+}
+
+void norm_sum(gmg_problem* p, const Lev& L, const double* v, double* out, int mode) {
+    seqsum(p, NormTerms{v, L.grid()}, L.n(), out, nullptr, mode);
+}
+
+void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc, int mode) {
+    with_coef(L, [&](const auto& A) {
+        using C = std::decay_t<decltype(A)>;
+        OmegaTerms<C> tg{d, L.grid(), A, prolong_from(p, L.l - 1, uc)};
+        seqsum(p, tg, L.n(), p->sums, p->nz, mode);
+    });
+}
+
+// ---------------------------------------------------------------------------
+// cycle driver (recorded into a CUDA graph)
+// ---------------------------------------------------------------------------
+struct Driver {
+    gmg_problem* p;
+    gmg_cycle_desc sp;
+
+    // gmg::mg_cycle (cycle.cpp:69-100) on level l from start s with rhs g.
+    const double* visit(int l, SmoothSrc s, const double* g) {
+        Lev& L = p->lev(l);
+        if (l == 1) {
+            // coarse_solve (cycle.cpp:57-65)
+            if ((unsigned long long)L.n() <= sp.coarse_direct_max_neq) {
+                launch_coarse(p, g, L.buf[U0]);
+                return L.buf[U0];
+            }
+            double* a = (s.u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
+            double* b = (a == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
+            return smooth_steps(p, L, std::max(1, sp.pre_steps + sp.post_steps), s, g, a, b,
+                                sp.smoothing_omega);
+        }
+        double* a = (s.u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
+        double* b = (a == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
+        double* u = smooth_steps(p, L, sp.pre_steps, s, g, a, b, sp.smoothing_omega);
+        double* other = (u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
+        const bool adaptive = sp.adaptive_correction != 0;
+        Lev& C = p->lev(l - 1);
+        launch_resid(p, L, u, nullptr, g, adaptive ? L.buf[DD] : nullptr, nullptr, C.buf[GRHS]);
+        SmoothSrc z;
+        z.kind = S_ZERO;
+        const double* uc = visit(l - 1, z, C.buf[GRHS]);
+        if (sp.cycle == GMG_CYCLE_W) {
+            SmoothSrc w;
+            w.kind = S_U;
+            w.u = uc;
+            uc = visit(l - 1, w, C.buf[GRHS]);
+        }
+        SmoothSrc cs;
+        cs.kind = S_CORRECT;
+        cs.u = u;
+        cs.uc = uc;
+        if (adaptive) {
+            omega_sums(p, L, L.buf[DD], uc, sp.reduction);
+            cs.om = OmegaSrc{p->sums, p->nz, 0.0, p->status};
+        } else {
+            cs.om = OmegaSrc{nullptr, nullptr, sp.correction_omega, p->status};
+        }
+        return smooth_steps(p, L, sp.post_steps, cs, g, other, u, sp.smoothing_omega);
+    }
+
+    // One outer cycle: x_out = cycle(x_in); r = b - A x_out -> DCAS[L]; norm^2 -> sums[2].
+    void cycle(const double* xin, double* xout) {
+        const int L = p->L;
+        Lev& F = p->lev(L);
+        const double* e;
+        if (sp.cycle == GMG_CYCLE_F) {
+            // fcycle_pass (cycle.cpp:119-142): DCAS[L], DCAS[L-1] are current
+            for (int l = L - 1; l >= 2; --l) launch_restrict(p, l, p->lev(l).buf[DCAS], p->lev(l - 1).buf[DCAS]);
+            SmoothSrc z;
+            z.kind = S_ZERO;
+            if (L == 1) {
+                SmoothSrc s0;
+                s0.kind = S_U;
+                s0.u = xin;
+                e = visit(1, s0, p->B);
+                launch_resid(p, F, e, nullptr, p->B, F.buf[DCAS], xout, nullptr);
+            } else {
+                e = visit(1, z, p->lev(1).buf[DCAS]);
+                for (int l = 2; l <= L; ++l) {
+                    SmoothSrc s;
+                    s.kind = S_PROLONG;
+                    s.uc = e;
+                    e = visit(l, s, p->lev(l).buf[DCAS]);
+                }
+                launch_resid(p, F, xin, e, p->B, F.buf[DCAS], xout, p->lev(L - 1).buf[DCAS]);
+            }
+        } else {
+            SmoothSrc s0;
+            s0.kind = S_U;
+            s0.u = xin;
+            e = visit(L, s0, p->B);
+            launch_resid(p, F, e, nullptr, p->B, F.buf[DCAS], xout, nullptr);
+        }
+        norm_sum(p, F, F.buf[DCAS], p->sums + 2, sp.reduction);
+    }
+};
+
+std::string spec_key(const gmg_cycle_desc& s) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%d|%d|%d|%d|%a|%d|%a|%a|%llu|%d", s.cycle, s.pre_steps, s.post_steps,
+                  s.adaptive_correction, s.correction_omega, s.smoother_kind, s.smoother_omega,
+                  s.smoothing_omega, s.coarse_direct_max_neq, s.reduction);
+    return buf;
+}
+
+std::array<cudaGraphExec_t, 2>& get_graphs(gmg_problem* p, const gmg_cycle_desc& sp) {
+    const std::string key = spec_key(sp);
+    auto it = p->graphs.find(key);
+    if (it != p->graphs.end()) return it->second;
+    std::array<cudaGraphExec_t, 2> ex{};
+    for (int par = 0; par < 2; ++par) {
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(p->st, cudaStreamCaptureModeThreadLocal));
+        try {
+            Driver d{p, sp};
+            d.cycle(p->X[par], p->X[1 - par]);
+        } catch (...) {
+            cudaStreamEndCapture(p->st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(p->st, &g));
+        CK(cudaGraphInstantiate(&ex[par], g, 0));
+        CK(cudaGraphDestroy(g));
+    }
+    return p->graphs.emplace(key, ex).first->second;
+}
+
+// smoother admissibility, smoother.cpp:51-69 (setup_smoothers runs first in solve)
+void check_smoother(const gmg_cycle_desc& sp) {
+    const double w = sp.smoother_omega;
+    switch (sp.smoother_kind) {
+        case GMG_SMOOTHER_RICHARDSON:
+        case GMG_SMOOTHER_JACOBI:
+        case GMG_SMOOTHER_ILU0:
+            if (!(w > 0.0)) throw std::invalid_argument("smoother_omega: must be > 0");
+            break;
+        case GMG_SMOOTHER_GAUSS_SEIDEL:
+        case GMG_SMOOTHER_SOR:
+            if (!(w > 0.0 && w < 2.0))
+                throw std::invalid_argument("smoother_omega: must be in (0, 2) for gauss_seidel/sor");
+            break;
+        case GMG_SMOOTHER_TRI_X:
+        case GMG_SMOOTHER_TRI_Y:
+        case GMG_SMOOTHER_ADI:
+        case GMG_SMOOTHER_GSTRI_X:
+        case GMG_SMOOTHER_GSTRI_Y:
+        case GMG_SMOOTHER_GSADI:
+            if (!(w > 0.0 && w <= 1.0))
+                throw std::invalid_argument("smoother_omega: must be in (0, 1] for line smoothers");
+            break;
+        default:
+            throw std::invalid_argument("smoother: unknown kind");
+    }
+    if (sp.smoother_kind != GMG_SMOOTHER_JACOBI)
+        throw GmgError{GMG_ERR_UNSUPPORTED, "smoother kind not implemented on the device yet"};
+}
+
+// checks the reference performs inside mg_cycle / smooth_step (cycle.cpp:75-76, smoother.cpp:391)
+void check_cycle(const gmg_problem* p, const gmg_cycle_desc& sp) {
+    if (sp.pre_steps < 0 || sp.post_steps < 0 || sp.pre_steps + sp.post_steps < 1)
+        throw std::invalid_argument("pre_steps/post_steps: at least one smoothing step per visit");
+    const bool smooths = p->L > 1 || (unsigned long long)p->lv[0].n() > sp.coarse_direct_max_neq;
+    if (smooths && !(sp.smoothing_omega > 0.0)) throw std::invalid_argument("omega: damping must be > 0");
+    if (sp.cycle < 0 || sp.cycle > 2) throw std::invalid_argument("cycle: must be one of V, W, F");
+}
+
+void upload(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
+    CK(cudaMemcpy2DAsync(dst, L.pitch * sizeof(double), src, L.nx * sizeof(double), L.nx * sizeof(double),
+                         L.ny, kind, p->st));
+}
+void download(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
+    CK(cudaMemcpy2DAsync(dst, L.nx * sizeof(double), src, L.pitch * sizeof(double), L.nx * sizeof(double),
+                         L.ny, kind, p->st));
+}
+
+double fetch_scalar(gmg_problem* p, const double* dev) {
+    CK(cudaMemcpyAsync(p->hostbuf, dev, sizeof(double), cudaMemcpyDeviceToHost, p->st));
+    CK(cudaStreamSynchronize(p->st));
+    return p->hostbuf[0];
+}
+
+int fetch_status(gmg_problem* p) {
+    int s = 0;
+    CK(cudaMemcpyAsync(&s, p->status, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+    CK(cudaStreamSynchronize(p->st));
+    return s;
+}
+
+// gmg::solve (cycle.cpp:146-194). b, x in device layout already (B, X[0]).
+void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep, int* final_par) {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    check_smoother(sp);
+    const int L = p->L;
+    Lev& F = p->lev(L);
+    CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+    // r0 = ||b - A x||, and the F-cycle's first defect cascade seed
+    launch_resid(p, F, p->X[0], nullptr, p->B, F.buf[DCAS], nullptr,
+                 (sp.cycle == GMG_CYCLE_F && L >= 2) ? p->lev(L - 1).buf[DCAS] : nullptr);
+    norm_sum(p, F, F.buf[DCAS], p->sums + 2, sp.reduction);
+    const double r0 = std::sqrt(fetch_scalar(p, p->sums + 2));
+    norm_sum(p, F, p->B, p->sums + 3, sp.reduction);
+    const double bnorm = std::sqrt(fetch_scalar(p, p->sums + 3));
+    int hl = 0;
+    rep->residual_history[hl++] = r0;
+    rep->iterations = 0;
+    rep->converged = 0;
+    *final_par = 0;
+    const double reference = bnorm > 0.0 ? bnorm : r0;
+    if (r0 <= sp.tolerance * reference) {
+        rep->converged = 1;
+        rep->history_len = hl;
+        rep->wall_seconds = elapsed();
+        return;
+    }
+    check_cycle(p, sp);
+    auto& ex = get_graphs(p, sp);
+    int par = 0;
+    for (int k = 1; k <= sp.max_cycles; ++k) {
+        CK(cudaGraphLaunch(ex[par], p->st));
+        par = 1 - par;
+        const double rk = std::sqrt(fetch_scalar(p, p->sums + 2));
+        if (sp.adaptive_correction && fetch_status(p) == 3) {
+            rep->history_len = hl;
+            throw std::runtime_error("adaptive_omega: correction has nonpositive energy");
+        }
+        *final_par = par;
+        if (rep->convergence_factors) rep->convergence_factors[k - 1] = rk / rep->residual_history[hl - 1];
+        rep->residual_history[hl++] = rk;
+        rep->iterations = k;
+        if (rk <= sp.tolerance * reference) {
+            rep->converged = 1;
+            break;
+        }
+        if (rk > 1e6 * std::max(r0, reference)) {
+            rep->history_len = hl;
+            rep->wall_seconds = elapsed();
+            throw GmgError{GMG_DIVERGED, "solve: residual grew beyond 1e6 times the initial residual"};
+        }
+    }
+    rep->history_len = hl;
+    rep->wall_seconds = elapsed();
+}
+
+void free_problem(gmg_problem* p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    for (auto& kv : p->graphs)
+        for (auto g : kv.second)
+            if (g) cudaGraphExecDestroy(g);
+    for (auto& L : p->lv) {
+        cudaFree(L.mem);
+        cudaFree(L.coefmem);
+        cudaFree(L.wmem);
+    }
+    cudaFree(p->xmem);
+    cudaFree(p->band);
+    cudaFree(p->cscr);
+    cudaFree(p->csum);
+    cudaFree(p->cpred);
+    cudaFree(p->counts);
+    cudaFree(p->recs);
+    cudaFree(p->sums);
+    cudaFree(p->nz);
+    cudaFree(p->status);
+    if (p->hostbuf) cudaFreeHost(p->hostbuf);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->st) cudaStreamDestroy(p->st);
+    delete p;
+}
+
+double* alloc_pitched(size_t n_buffers, Lev& L) {
+    double* m = nullptr;
+    CK(cudaMalloc(&m, n_buffers * L.elems * sizeof(double)));
+    return m;
+}
+
+void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
+    if (!d || d->num_levels < 1 || !d->levels) throw std::logic_error("problem: missing level data");
+    std::unique_ptr<gmg_problem, void (*)(gmg_problem*)> p(new gmg_problem, free_problem);
+    p->L = d->num_levels;
+    p->device = d->device;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw GmgError{GMG_ERR_CUDA, "no CUDA device available"};
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&p->ev0));
+    CK(cudaEventCreate(&p->ev1));
+    CK(cudaMallocHost(&p->hostbuf, 4 * sizeof(double)));
+    p->lv.resize(p->L);
+    std::vector<gmg_host::Level> hl(p->L);
+    for (int l = 1; l <= p->L; ++l) {
+        const gmg_level_desc& ld = d->levels[l - 1];
+        if (ld.level != l || ld.nx < 1 || ld.ny < 1) throw std::logic_error("problem: bad level description");
+        gmg_host::Level& h = hl[l - 1];
+        h.level = l;
+        h.nx = ld.nx;
+        h.ny = ld.ny;
+        h.x.assign(ld.x, ld.x + ld.nx + 2);
+        h.y.assign(ld.y, ld.y + ld.ny + 2);
+        if (l >= 2) {
+            const std::string err = gmg_host::check_nested(hl[l - 2], h);
+            if (!err.empty()) throw std::logic_error("problem: " + err);
+        }
+        Lev& L = p->lv[l - 1];
+        L.l = l;
+        L.nx = ld.nx;
+        L.ny = ld.ny;
+        L.pitch = ((ld.nx + 31) / 32) * 32;
+        L.off0 = (size_t)L.pitch + 32;
+        L.elems = L.off0 + (size_t)(L.ny + 1) * L.pitch + 64;
+        L.hx = h.x;
+        L.hy = h.y;
+        L.mem = alloc_pitched(NBUF, L);
+        CK(cudaMemset(L.mem, 0, NBUF * L.elems * sizeof(double)));
+        for (int b = 0; b < NBUF; ++b) L.buf[b] = L.mem + b * L.elems + L.off0;
+        // operator
+        const gmg_host::CoefClass cc = gmg_host::classify(ld.nx, ld.ny, ld.c, ld.n, ld.s, ld.e, ld.w);
+        L.kind = cc.kind;
+        if (cc.kind == gmg_host::COEF_CONST) {
+            L.cconst = CoefConst{cc.c, cc.w, cc.e, cc.s, cc.n, 0.0, 0};
+            int ex2;
+            const double fr = std::frexp(cc.c, &ex2);
+            if (fr == 0.5 && std::isnormal(cc.c)) {
+                L.cconst.c_pow2 = 1;
+                L.cconst.inv_c = std::ldexp(1.0, 1 - ex2);
+            }
+        } else if (cc.kind == gmg_host::COEF_ROWX) {
+            CK(cudaMalloc(&L.coefmem, 5 * L.nx * sizeof(double)));
+            const std::vector<double>* t[5] = {&cc.rc, &cc.rw, &cc.re, &cc.rs, &cc.rn};
+            for (int q = 0; q < 5; ++q)
+                CK(cudaMemcpy(L.coefmem + q * L.nx, t[q]->data(), L.nx * sizeof(double), cudaMemcpyHostToDevice));
+            L.crow = CoefRowX{L.coefmem, L.coefmem + L.nx, L.coefmem + 2 * L.nx, L.coefmem + 3 * L.nx,
+                              L.coefmem + 4 * L.nx};
+        } else {
+            CK(cudaMalloc(&L.coefmem, 5 * L.elems * sizeof(double)));
+            CK(cudaMemset(L.coefmem, 0, 5 * L.elems * sizeof(double)));
+            const double* src[5] = {ld.c, ld.w, ld.e, ld.s, ld.n};
+            double* dst[5];
+            for (int q = 0; q < 5; ++q) {
+                dst[q] = L.coefmem + q * L.elems + L.off0;
+                CK(cudaMemcpy2D(dst[q], L.pitch * sizeof(double), src[q], L.nx * sizeof(double),
+                                L.nx * sizeof(double), L.ny, cudaMemcpyHostToDevice));
+            }
+            L.cfield = CoefField{dst[0], dst[1], dst[2], dst[3], dst[4], L.pitch};
+        }
+    }
+    // transfer tables: tx, ty (fine side); restriction weights (coarse side)
+    for (int l = 1; l <= p->L; ++l) {
+        Lev& L = p->lv[l - 1];
+        std::vector<double> host;
+        size_t o_tx = 0, o_ty = 0, o_r = 0;
+        if (l >= 2) {
+            const Lev& C = p->lv[l - 2];
+            auto tx = gmg_host::prolong_weights(L.hx, C.hx, L.nx);
+            auto ty = gmg_host::prolong_weights(L.hy, C.hy, L.ny);
+            o_tx = host.size();
+            host.insert(host.end(), tx.begin(), tx.end());
+            o_ty = host.size();
+            host.insert(host.end(), ty.begin(), ty.end());
+        }
+        if (l < p->L) {
+            const Lev& Fn = p->lv[l];
+            std::vector<double> a, b, c, e, f, g;
+            gmg_host::restrict_weights(Fn.hx, L.hx, L.nx, a, b, c);
+            gmg_host::restrict_weights(Fn.hy, L.hy, L.ny, e, f, g);
+            o_r = host.size();
+            for (auto* v : {&a, &b, &c, &e, &f, &g}) host.insert(host.end(), v->begin(), v->end());
+        }
+        if (host.empty()) continue;
+        CK(cudaMalloc(&L.wmem, host.size() * sizeof(double)));
+        CK(cudaMemcpy(L.wmem, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
+        if (l >= 2) {
+            L.tx = L.wmem + o_tx;
+            L.ty = L.wmem + o_ty;
+        }
+        if (l < p->L) {
+            double* r = L.wmem + o_r;
+            L.rw = RestrictW{r, r + L.nx, r + 2 * L.nx, r + 3 * L.nx, r + 3 * L.nx + L.ny,
+                             r + 3 * L.nx + 2 * L.ny};
+        }
+    }
+    // level-1 factorization (MultilevelProblem ctor, cycle.cpp:29)
+    {
+        const gmg_level_desc& ld = d->levels[0];
+        std::vector<double> band = gmg_host::cholesky_band(ld.c, ld.w, ld.s, ld.nx, ld.ny);
+        p->cn = ld.nx * ld.ny;
+        p->cbw = ld.nx;
+        CK(cudaMalloc(&p->band, band.size() * sizeof(double)));
+        CK(cudaMemcpy(p->band, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&p->cscr, std::max(1, p->cn) * sizeof(double)));
+    }
+    // finest x (ping-pong) and b
+    {
+        Lev& F = p->lv.back();
+        CK(cudaMalloc(&p->xmem, 3 * F.elems * sizeof(double)));
+        CK(cudaMemset(p->xmem, 0, 3 * F.elems * sizeof(double)));
+        p->X[0] = p->xmem + F.off0;
+        p->X[1] = p->xmem + F.elems + F.off0;
+        p->B = p->xmem + 2 * F.elems + F.off0;
+        const long long n = F.n();
+        p->nch_max = (int)((n + kSsC - 1) / kSsC);
+        CK(cudaMalloc(&p->csum, 2 * p->nch_max * sizeof(double)));
+        CK(cudaMalloc(&p->cpred, 2 * p->nch_max * sizeof(double)));
+        CK(cudaMalloc(&p->counts, 2 * p->nch_max * sizeof(int)));
+        CK(cudaMalloc(&p->recs, 2 * (size_t)p->nch_max * kSsRMax * sizeof(gmg_ss::Rec)));
+        CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
+        CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
+        CK(cudaMalloc(&p->nz, sizeof(int)));
+        CK(cudaMalloc(&p->status, sizeof(int)));
+        CK(cudaMemset(p->status, 0, sizeof(int)));
+    }
+    CK(cudaDeviceSynchronize());
+    *out = p.release();
+}
+
+gmg_problem* checked(gmg_problem* p) {
+    if (!p) throw std::logic_error("null problem handle");
+    CK(cudaSetDevice(p->device));
+    return p;
+}
+
+void check_level(const gmg_problem* p, int level, const char* what) {
+    if (level < 1 || level > p->L) throw std::logic_error(std::string(what) + ": level out of range");
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* gmg_last_error(void) { return g_last_error.c_str(); }
+
+const char* gmg_version(void) { return "gmg_b200 sm_100a; exact-order seqsum v1 (chunk 8192, rmax 256)"; }
+
+int gmg_dev_problem_create(const gmg_problem_desc* desc, gmg_problem** out) {
+    return guarded([&] { create_problem(desc, out); });
+}
+
+int gmg_dev_problem_destroy(gmg_problem* p) {
+    free_problem(p);
+    return GMG_OK;
+}
+
+int gmg_dev_num_levels(const gmg_problem* p) { return p ? p->L : 0; }
+
+int gmg_dev_level_shape(const gmg_problem* p, int level, int* nx, int* ny) {
+    return guarded([&] {
+        check_level(p, level, "level_shape");
+        *nx = p->lv[level - 1].nx;
+        *ny = p->lv[level - 1].ny;
+    });
+}
+
+int gmg_dev_level_coef_kind(const gmg_problem* p, int level) {
+    if (!p || level < 1 || level > p->L) return -1;
+    return p->lv[level - 1].kind;
+}
+
+int gmg_dev_solve(gmg_problem* p, const gmg_cycle_desc* spec, const double* b, double* x,
+                  gmg_solve_report* rep) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        Lev& F = p->lev(p->L);
+        upload(p, F, p->B, b, cudaMemcpyHostToDevice);
+        upload(p, F, p->X[0], x, cudaMemcpyHostToDevice);
+        int par = 0;
+        try {
+            solve_core(p, *spec, rep, &par);
+        } catch (const GmgError& e) {
+            if (e.code == GMG_DIVERGED) {
+                download(p, F, x, p->X[par], cudaMemcpyDeviceToHost);
+                CK(cudaStreamSynchronize(p->st));
+                std::snprintf(rep->message, sizeof rep->message, "%s", e.msg.c_str());
+            }
+            throw;
+        } catch (const std::runtime_error&) {
+            // x keeps the last completed iterate, as the reference's in-place x does
+            download(p, F, x, p->X[par], cudaMemcpyDeviceToHost);
+            CK(cudaStreamSynchronize(p->st));
+            throw;
+        }
+        download(p, F, x, p->X[par], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_solve_devptr(gmg_problem* p, const gmg_cycle_desc* spec, const double* b_dev, double* x_dev,
+                         gmg_solve_report* rep) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        Lev& F = p->lev(p->L);
+        upload(p, F, p->B, b_dev, cudaMemcpyDeviceToDevice);
+        upload(p, F, p->X[0], x_dev, cudaMemcpyDeviceToDevice);
+        int par = 0;
+        solve_core(p, *spec, rep, &par);
+        download(p, F, x_dev, p->X[par], cudaMemcpyDeviceToDevice);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, const double* u0,
+                     const double* g, double* u) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_level(p, level, "mg_cycle");
+        check_smoother(*spec);
+        check_cycle(p, *spec);
+        Lev& L = p->lev(level);
+        // stage u0 in X-side scratch: use DD for g and DCAS for u0 of this level
+        upload(p, L, L.buf[DCAS], u0, cudaMemcpyHostToDevice);
+        upload(p, L, L.buf[GRHS], g, cudaMemcpyHostToDevice);
+        CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+        Driver d{p, *spec};
+        SmoothSrc s;
+        s.kind = S_U;
+        s.u = L.buf[DCAS];
+        // visit() writes level-l results into U0/U1, so g must not alias them: it lives in GRHS,
+        // which the recursion only writes on level l-1.
+        const double* r = d.visit(level, s, L.buf[GRHS]);
+        download(p, L, u, r, cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+        if (spec->adaptive_correction && fetch_status(p) == 3)
+            throw std::runtime_error("adaptive_omega: correction has nonpositive energy");
+    });
+}
+
+int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_level(p, level, "apply");
+        Lev& L = p->lev(level);
+        upload(p, L, L.buf[U0], x, cudaMemcpyHostToDevice);
+        with_coef(L, [&](const auto& A) {
+            dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
+            k_apply_simple<<<gr, b, 0, p->st>>>(L.grid(), A, L.buf[U0], L.buf[U1]);
+        });
+        CK(cudaGetLastError());
+        download(p, L, y, L.buf[U1], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_residual(gmg_problem* p, int level, const double* x, const double* b, double* r) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_level(p, level, "residual");
+        Lev& L = p->lev(level);
+        upload(p, L, L.buf[U0], x, cudaMemcpyHostToDevice);
+        upload(p, L, L.buf[GRHS], b, cudaMemcpyHostToDevice);
+        launch_resid(p, L, L.buf[U0], nullptr, L.buf[GRHS], L.buf[DD], nullptr, nullptr);
+        download(p, L, r, L.buf[DD], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_smooth_step(gmg_problem* p, int level, int kind, double somega, double omega_damp,
+                        const double* x, const double* b, double* out) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_level(p, level, "smooth_step");
+        gmg_cycle_desc sp{};
+        sp.smoother_kind = kind;
+        sp.smoother_omega = somega;
+        check_smoother(sp);
+        if (!(omega_damp > 0.0)) throw std::invalid_argument("omega: damping must be > 0");
+        Lev& L = p->lev(level);
+        upload(p, L, L.buf[U0], x, cudaMemcpyHostToDevice);
+        upload(p, L, L.buf[GRHS], b, cudaMemcpyHostToDevice);
+        SmoothSrc s;
+        s.kind = S_U;
+        s.u = L.buf[U0];
+        launch_smooth(p, L, 1, s, L.buf[GRHS], L.buf[U1], omega_damp);
+        download(p, L, out, L.buf[U1], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_restriction(gmg_problem* p, int fine_level, const double* fine, double* coarse) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (fine_level < 2 || fine_level > p->L) throw std::logic_error("restriction: levels are not parent and child");
+        Lev& F = p->lev(fine_level);
+        Lev& C = p->lev(fine_level - 1);
+        upload(p, F, F.buf[U0], fine, cudaMemcpyHostToDevice);
+        launch_restrict(p, fine_level, F.buf[U0], C.buf[U1]);
+        download(p, C, coarse, C.buf[U1], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_prolongation(gmg_problem* p, int coarse_level, const double* coarse, double* fine) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (coarse_level < 1 || coarse_level >= p->L)
+            throw std::logic_error("prolongation: levels are not parent and child");
+        Lev& C = p->lev(coarse_level);
+        Lev& F = p->lev(coarse_level + 1);
+        upload(p, C, C.buf[U0], coarse, cudaMemcpyHostToDevice);
+        dim3 b(32, 8), gr((F.nx + 31) / 32, (F.ny + 7) / 8);
+        k_prolong_simple<<<gr, b, 0, p->st>>>(prolong_from(p, coarse_level, C.buf[U0]), F.grid(), F.buf[U1]);
+        CK(cudaGetLastError());
+        download(p, F, fine, F.buf[U1], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* d, const double* corr, double* omega) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_level(p, level, "adaptive_omega");
+        Lev& L = p->lev(level);
+        upload(p, L, L.buf[DD], d, cudaMemcpyHostToDevice);
+        upload(p, L, L.buf[U0], corr, cudaMemcpyHostToDevice);
+        with_coef(L, [&](const auto& A) {
+            using C = std::decay_t<decltype(A)>;
+            OmegaTermsField<C> tg{L.buf[DD], L.buf[U0], L.grid(), A};
+            seqsum(p, tg, L.n(), p->sums, p->nz, GMG_REDUCE_EXACT);
+        });
+        double h[2];
+        int nz = 0;
+        CK(cudaMemcpyAsync(h, p->sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->st));
+        CK(cudaMemcpyAsync(&nz, p->nz, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+        CK(cudaStreamSynchronize(p->st));
+        if (!nz) {
+            *omega = 1.0;
+            return;
+        }
+        if (!(h[0] > 0.0)) throw std::runtime_error("adaptive_omega: correction has nonpositive energy");
+        *omega = h[1] / h[0];
+    });
+}
+
+int gmg_dev_coarse_solve(gmg_problem* p, const double* b, double* x) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        Lev& L = p->lev(1);
+        upload(p, L, L.buf[GRHS], b, cudaMemcpyHostToDevice);
+        launch_coarse(p, L.buf[GRHS], L.buf[U0]);
+        download(p, L, x, L.buf[U0], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
+static void flat_sum(gmg_problem* p, long long n, const double* a, const double* b, int mode, double* out) {
+    if (n <= 0) {
+        *out = 0.0;
+        return;
+    }
+    double *da = nullptr, *db = nullptr;
+    CK(cudaMalloc(&da, n * sizeof(double)));
+    if (b) CK(cudaMalloc(&db, n * sizeof(double)));
+    CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+    if (b) CK(cudaMemcpyAsync(db, b, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+    // a flat vector viewed as one row; chunks never exceed the workspace (checked)
+    if ((n + kSsC - 1) / kSsC > p->nch_max) {
+        cudaFree(da);
+        cudaFree(db);
+        throw std::logic_error("norm/dot: vector longer than the finest level");
+    }
+    Grid g{(int)std::min<long long>(n, INT_MAX), 1, n};
+    if (n > INT_MAX) throw std::logic_error("norm/dot: vector too long");
+    if (b)
+        seqsum(p, DotTerms{da, db, g}, n, p->sums + 4, nullptr, mode);
+    else
+        seqsum(p, NormTerms{da, g}, n, p->sums + 4, nullptr, mode);
+    *out = fetch_scalar(p, p->sums + 4);
+    cudaFree(da);
+    cudaFree(db);
+}
+
+int gmg_dev_norm_l2(gmg_problem* p, long long n, const double* v, int mode, double* out) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        double s = 0.0;
+        flat_sum(p, n, v, nullptr, mode, &s);
+        *out = std::sqrt(s);
+    });
+}
+
+int gmg_dev_dot(gmg_problem* p, long long n, const double* a, const double* b, int mode, double* out) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        flat_sum(p, n, a, b, mode, out);
+    });
+}
+
+int gmg_dev_axpy(gmg_problem* p, long long n, double alpha, const double* x, double* y) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (n <= 0) return;
+        double *dx = nullptr, *dy = nullptr;
+        CK(cudaMalloc(&dx, n * sizeof(double)));
+        CK(cudaMalloc(&dy, n * sizeof(double)));
+        CK(cudaMemcpyAsync(dx, x, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+        CK(cudaMemcpyAsync(dy, y, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+        k_axpy_flat<<<(unsigned)((n + 255) / 256), 256, 0, p->st>>>(n, alpha, dx, dy);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, p->st));
+        CK(cudaStreamSynchronize(p->st));
+        cudaFree(dx);
+        cudaFree(dy);
+    });
+}
+
+int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int variant, int reps, double* ms,
+                          double* bytes) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (p->L < 2) throw std::logic_error("time_smoother: needs >= 2 levels");
+        const int L = p->L;
+        Lev& F = p->lev(L);
+        Lev& C = p->lev(L - 1);
+        const int M = std::min(std::max(variant == 1 ? spec->post_steps : spec->pre_steps, 1), kMaxFuse);
+        SmoothSrc s;
+        double per_dof = 24.0;
+        if (variant == 0) {
+            s.kind = S_PROLONG;
+            s.uc = C.buf[U0];
+            per_dof = 18.0;
+        } else if (variant == 1) {
+            s.kind = S_CORRECT;
+            s.u = F.buf[U0];
+            s.uc = C.buf[U0];
+            s.om = OmegaSrc{nullptr, nullptr, 1.0, p->status};
+            per_dof = 26.0;
+        } else {
+            s.kind = S_U;
+            s.u = F.buf[U0];
+        }
+        launch_smooth(p, F, M, s, F.buf[DCAS], F.buf[U1], spec->smoothing_omega);  // warm
+        CK(cudaEventRecord(p->ev0, p->st));
+        for (int r = 0; r < reps; ++r) launch_smooth(p, F, M, s, F.buf[DCAS], F.buf[U1], spec->smoothing_omega);
+        CK(cudaEventRecord(p->ev1, p->st));
+        CK(cudaEventSynchronize(p->ev1));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, p->ev0, p->ev1));
+        *ms = (double)t / reps;
+        *bytes = per_dof * (double)F.n();
+    });
+}
+
+int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* count) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_smoother(*spec);
+        check_cycle(p, *spec);
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(p->st, cudaStreamCaptureModeThreadLocal));
+        Driver d{p, *spec};
+        d.cycle(p->X[0], p->X[1]);
+        CK(cudaStreamEndCapture(p->st, &g));
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        int k = 0;
+        for (auto n : nodes) {
+            cudaGraphNodeType t;
+            CK(cudaGraphNodeGetType(n, &t));
+            if (t == cudaGraphNodeTypeKernel) ++k;
+        }
+        cudaGraphDestroy(g);
+        *count = k;
+    });
+}
+
+int gmg_host_problem_create(int num_levels, int cnx, int cny, double gx, double gy, int coords, double alpha,
+                            double beta, int device, gmg_problem** out) {
+    return guarded([&] {
+        std::vector<gmg_host::Level> lv = gmg_host::build_problem(num_levels, cnx, cny, gx, gy, coords, alpha, beta);
+        std::vector<gmg_level_desc> d(lv.size());
+        for (size_t q = 0; q < lv.size(); ++q) {
+            d[q] = gmg_level_desc{lv[q].level, lv[q].nx, lv[q].ny, lv[q].x.data(), lv[q].y.data(),
+                                  lv[q].c.data(), lv[q].n.data(), lv[q].s.data(), lv[q].e.data(),
+                                  lv[q].w.data()};
+        }
+        gmg_problem_desc pd{num_levels, d.data(), device};
+        create_problem(&pd, out);
+    });
+}
+
+void gmg_host_random_vector(long long n, unsigned seed, double* out) {
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    for (long long k = 0; k < n; ++k) out[k] = dist(rng);
+}
+
+int gmg_host_seqsum_emulate(long long n, const double* terms, int threads, int ept, double* out,
+                            long long* stats) {
+    return guarded([&] {
+        if (threads < 1 || ept < 1) throw std::invalid_argument("seqsum_emulate: bad chunking");
+        *out = gmg_host::seqsum_emulate(terms, n, threads, ept, stats);
+    });
+}
+
+}  // extern "C"

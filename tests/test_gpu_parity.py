@@ -1,0 +1,218 @@
+"""Parity of the CUDA path (through the C ABI, libgmg_b200.so) with the CPU
+oracle and the reference's golden fixtures. The bar is bit-for-bit identity of
+every grid function, every residual history and every iteration count (the
+arithmetic is fp64 in the reference's operation order);
+the only tolerance used anywhere is for the opt-in "fast" reduction mode.
+"""
+import numpy as np
+import pytest
+
+from conftest import bits_equal, first_mismatch, load_golden, unhex
+from pyoracle import CycleSpec as OSpec
+from pyoracle import Oracle
+
+gmg = pytest.importorskip("paper_0805_3041_b200.gmg")
+
+pytestmark = pytest.mark.gpu
+
+GEOMS = [
+    dict(levels=5, coarse=(1, 1), coords="cartesian", alpha=1.0, beta=1.0, grading=(1.0, 1.0)),
+    dict(levels=4, coarse=(2, 3), coords="cartesian", alpha=1e-2, beta=1.0, grading=(1.0, 1.0)),
+    dict(levels=5, coarse=(1, 1), coords="cylindrical", alpha=1.0, beta=1.0, grading=(1.0, 1.0)),
+    dict(levels=4, coarse=(3, 2), coords="spherical", alpha=1.3, beta=0.7, grading=(1.1, 0.93)),
+    dict(levels=3, coarse=(60, 1), coords="cartesian", alpha=0.5, beta=2.0, grading=(1.0, 1.02)),
+]
+GIDS = ["cart_uniform", "cart_aniso_rect", "cylindrical", "spherical_graded", "wide_graded"]
+
+
+def pair(geom):
+    args = (geom["levels"], geom["coarse"][0], geom["coarse"][1], geom["grading"], geom["coords"],
+            geom["alpha"], geom["beta"])
+    return gmg.MultilevelProblem(*args), Oracle(*args)
+
+
+@pytest.fixture(scope="module")
+def problems(gpu):
+    return [pair(g) for g in GEOMS]
+
+
+def test_operator_classes(problems):
+    kinds = [p.coef_kind(p.num_levels) for p, _ in problems]
+    assert kinds[0] == "const" and kinds[1] == "const"
+    assert kinds[2] == "rowx"
+    assert kinds[3] == "field"
+
+
+@pytest.mark.parametrize("gi", range(len(GEOMS)), ids=GIDS)
+def test_per_level_operators_bitexact(problems, gi):
+    d, o = problems[gi]
+    for l in range(1, d.num_levels + 1):
+        n = d.n(l)
+        x = Oracle.random_vector(n, 10 + l)
+        b = Oracle.random_vector(n, 20 + l)
+        assert bits_equal(gmg.apply(d, l, x), o.apply(l, x)), ("apply", l)
+        assert bits_equal(gmg.residual(d, l, x, b), o.residual(l, x, b)), ("residual", l)
+        for damp in (0.7, 1.0, 0.35):
+            got = gmg.smooth_step(d, l, "jacobi", 1.0, x, b, damp)
+            want = o.smooth_step(l, "jacobi", 1.0, damp, x, b)
+            assert bits_equal(got, want), ("smooth_step", l, damp, first_mismatch(got, want))
+        if l >= 2:
+            assert bits_equal(gmg.restriction(d, l, x), o.restriction(l, x)), ("restriction", l)
+            c = Oracle.random_vector(d.n(l - 1), 30 + l)
+            assert bits_equal(gmg.prolongation(d, l - 1, c), o.prolongation(l - 1, c)), ("prolongation", l)
+            # defect/correction pairs as the cycle produces them, and random ones
+            corr = o.prolongation(l - 1, c)
+            assert gmg.adaptive_omega(d, l, b, corr) == o.adaptive_omega(l, b, corr)
+            assert gmg.adaptive_omega(d, l, b, x * x) == o.adaptive_omega(l, b, x * x)
+        assert gmg.norm_l2(d, x) == o.norm_l2(x)
+        assert gmg.dot(d, x, b) == o.dot(x, b)
+    b1 = Oracle.random_vector(d.n(1), 5)
+    assert bits_equal(gmg.coarse_solve(d, b1), o.coarse_solve(b1))
+
+
+def test_adaptive_omega_zero_correction_is_one(problems):
+    d, _ = problems[0]
+    l = d.num_levels
+    assert gmg.adaptive_omega(d, l, np.ones(d.n(l)), np.zeros(d.n(l))) == 1.0
+
+
+def test_adaptive_omega_nonpositive_energy_raises(problems):
+    d, _ = problems[0]
+    l = d.num_levels
+    # a correction whose products all underflow is "zero" only if corr*corr == 0 everywhere;
+    # here corr is tiny but nonzero: energy underflows to 0 -> runtime_error like the reference
+    corr = np.full(d.n(l), 1e-170)
+    with pytest.raises(gmg.GmgRuntimeError, match="nonpositive energy"):
+        gmg.adaptive_omega(d, l, np.ones(d.n(l)), corr)
+
+
+@pytest.mark.parametrize("n", [1, 31, 8192, 8193, 100003, 1 << 20])
+def test_exact_dot_and_norm_on_device(problems, n):
+    d, o = problems[0]
+    if n > d.n(d.num_levels) * 1:
+        d = gmg.MultilevelProblem(11)
+    rng = np.random.default_rng(n)
+    for a, b in [(rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)),
+                 (np.ldexp(np.round(rng.uniform(-8, 8, n)), -rng.integers(0, 4, n)), np.ones(n)),
+                 (rng.uniform(-1, 1, n) * 10.0 ** rng.integers(-12, 12, n), rng.uniform(0, 1, n))]:
+        assert gmg.dot(d, a, b) == o.dot(a, b)
+        assert gmg.norm_l2(d, a) == o.norm_l2(a)
+        assert abs(gmg.dot(d, a, b, reduction="fast") - o.dot(a, b)) <= 1e-10 * (np.abs(a * b).sum() + 1e-300)
+
+
+def test_axpy(problems):
+    d, _ = problems[0]
+    x = Oracle.random_vector(1000, 1)
+    y = Oracle.random_vector(1000, 2)
+    want = y + 0.3 * x
+    gmg.axpy(d, 0.3, x, y)
+    assert bits_equal(y, want)
+
+
+@pytest.mark.parametrize("cycle", ["V", "W"])
+@pytest.mark.parametrize("gi", [0, 2, 3], ids=["cart", "cyl", "sph"])
+def test_mg_cycle_bitexact(problems, cycle, gi):
+    d, o = problems[gi]
+    L = d.num_levels
+    for adaptive in (True, False):
+        spec = dict(cycle=cycle, smoother="jacobi", pre_steps=2, post_steps=1, adaptive_correction=adaptive,
+                    correction_omega=3.0)
+        for l in range(1, L + 1):
+            u0 = Oracle.random_vector(d.n(l), 40 + l)
+            g = Oracle.random_vector(d.n(l), 50 + l)
+            got = gmg.mg_cycle(d, l, u0, g, gmg.CycleSpec(**spec))
+            want = o.mg_cycle(OSpec(**spec), l, u0, g)
+            assert bits_equal(got, want), (cycle, l, adaptive, first_mismatch(got, want))
+
+
+SOLVE_FIXTURES = ["c1_adaptive", "c1_fixed4", "small_V_jacobi", "small_W_jacobi", "small_F_rect_coarse",
+                  "small_F_graded_sph", "small_F_m0", "small_F_n0", "small_F_coarse_cap", "single_level",
+                  "c3p_cylindrical", "c4_small_2047"]
+
+
+def run_fixture(name, spec_over=None):
+    g = load_golden(name)
+    pb = g["problem"]
+    d = gmg.MultilevelProblem(pb["levels"], pb["coarse_nx"], pb["coarse_ny"], tuple(pb["grading"]),
+                              pb["coords"], pb["alpha"], pb["beta"])
+    L = pb["levels"]
+    n = d.n(L)
+    b = gmg.random_vector(n, pb["seed_f"])
+    x = gmg.random_vector(n, pb["seed_x"]) if pb["seed_x"] else np.zeros(n)
+    spec = dict(g["spec"])
+    spec.update(spec_over or {})
+    return g, d, b, x, gmg.CycleSpec(**spec)
+
+
+@pytest.mark.parametrize("name", SOLVE_FIXTURES)
+def test_solve_matches_reference_golden(gpu, name):
+    g, d, b, x, spec = run_fixture(name)
+    rep = gmg.solve(d, b, spec, x)
+    want = unhex(g["history"])
+    assert rep.iterations == g["iterations"]
+    assert rep.converged == g["converged"]
+    assert bits_equal(rep.residual_history, want), first_mismatch(rep.residual_history, want)
+    assert bits_equal(x[:8], unhex(g["x_head"])) and bits_equal(x[-8:], unhex(g["x_tail"]))
+    if "x" in g:
+        assert bits_equal(x, unhex(g["x"]))
+    # SolveReport invariants (test_cycle.cpp:214-231)
+    h = rep.residual_history
+    assert len(h) == rep.iterations + 1 and len(rep.convergence_factors) == rep.iterations
+    for k, f in enumerate(rep.convergence_factors):
+        assert f == h[k + 1] / h[k]
+
+
+def test_solve_divergence_error_carries_report(gpu):
+    g, d, b, x, spec = run_fixture("diverge_omega")
+    with pytest.raises(gmg.DivergenceError) as ei:
+        gmg.solve(d, b, spec, x)
+    rep = ei.value.report
+    assert rep.iterations == g["iterations"] and not rep.converged
+    assert bits_equal(rep.residual_history, unhex(g["history"]))
+    assert "grew beyond 1e6" in str(ei.value)
+    assert bits_equal(x[:8], unhex(g["x_head"]))
+
+
+def test_solve_errors_match_reference(gpu):
+    d = gmg.MultilevelProblem(3)
+    b = gmg.random_vector(d.n(3), 1)
+    with pytest.raises(gmg.InvalidArgument, match="smoother_omega"):
+        gmg.solve(d, b, gmg.CycleSpec(smoother="jacobi", smoother_omega=0.0), np.zeros(d.n(3)))
+    with pytest.raises(gmg.InvalidArgument, match="pre_steps/post_steps"):
+        gmg.solve(d, b, gmg.CycleSpec(smoother="jacobi", pre_steps=0, post_steps=0), np.zeros(d.n(3)))
+    with pytest.raises(gmg.InvalidArgument, match="omega: damping"):
+        gmg.solve(d, b, gmg.CycleSpec(smoother="jacobi", smoothing_omega=0.0), np.zeros(d.n(3)))
+    with pytest.raises(gmg.LogicError):
+        gmg.solve(d, b[:-1], gmg.CycleSpec(smoother="jacobi"), np.zeros(d.n(3)))
+    # zero right-hand side and zero start: converged at cycle 0 (cycle.cpp:164-170)
+    rep = gmg.solve(d, np.zeros(d.n(3)), gmg.CycleSpec(smoother="jacobi"), np.zeros(d.n(3)))
+    assert rep.converged and rep.iterations == 0 and rep.residual_history == [0.0]
+
+
+def test_fast_reduction_mode_close(gpu):
+    g, d, b, x, spec = run_fixture("c1_adaptive", {"reduction": "fast"})
+    rep = gmg.solve(d, b, spec, x)
+    want = unhex(g["history"])
+    assert rep.iterations == g["iterations"]
+    np.testing.assert_allclose(rep.residual_history, want, rtol=1e-6)
+
+
+def test_repeated_solves_are_deterministic(gpu):
+    g, d, b, x0, spec = run_fixture("c3p_cylindrical")
+    hs = []
+    for _ in range(2):
+        x = x0.copy()
+        hs.append(gmg.solve(d, b, spec, x).residual_history)
+    assert bits_equal(hs[0], hs[1])
+
+
+@pytest.mark.slow
+def test_c4_full_size_history(gpu):
+    """BASELINE configs[3] at full size (8191^2 interior, 13 levels): the
+    reference's 12-cycle history, bit for bit."""
+    g, d, b, x, spec = run_fixture("c4_adaptive")
+    rep = gmg.solve(d, b, spec, x)
+    assert rep.iterations == g["iterations"] == 12
+    assert bits_equal(rep.residual_history, unhex(g["history"])), \
+        first_mismatch(rep.residual_history, unhex(g["history"]))
+    assert bits_equal(x[:8], unhex(g["x_head"])) and bits_equal(x[-8:], unhex(g["x_tail"]))
