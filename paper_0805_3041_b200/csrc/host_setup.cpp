@@ -286,10 +286,10 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
                 if (!walk_try(st, cur, v)) {
                     ++nbreaks;
                     if (first) {
-                        out.push_back(rec_make(seg_merge(carry, cur), true, v));
+                        out.push_back(rec_make(seg_merge(carry, cur), true, v, (uint32_t)c));
                         first = false;
                     } else {
-                        out.push_back(rec_make(cur, true, v));
+                        out.push_back(rec_make(cur, true, v, (uint32_t)c));
                     }
                     cur = seg_empty();
                     real_add(st, v);
@@ -303,7 +303,7 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
             }
         }
         (void)carry_f;
-        out.push_back(rec_make(carry, false, 0.0));
+        out.push_back(rec_make(carry, false, 0.0, (uint32_t)c));
         if (static_cast<int>(out.size()) > RMAX) dirty[c] = 1;
         recs[c] = std::move(out);
     }

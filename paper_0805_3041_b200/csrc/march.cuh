@@ -329,4 +329,70 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
     }
 }
 
+// ---------------- adaptive-omega terms ---------------------------------------
+// adaptive_omega (cycle.cpp:40-51) needs, for corr = P uc on the fine level,
+// the products (A corr)_k * corr_k and d_k * corr_k in the reference's k order,
+// and whether any corr_k * corr_k != 0 (nc != 0). This kernel streams the rows
+// once — one prolongation per point, A corr from the register window plus the
+// shared-memory row — and writes both product arrays densely (k = j*nx + i) for
+// the exact-order summation engine. Strip stride TW-2 (1-column halo).
+template <int TW, int PF, class Coef>
+__global__ void __launch_bounds__(TW) k_omega_terms(Grid fg, Coef A, SrcProlong src,
+                                                    const double* __restrict__ d, double* __restrict__ T0,
+                                                    double* __restrict__ T1, int* __restrict__ nz, int seg) {
+    constexpr int OUTW = TW - 2;
+    __shared__ double xs[2][TW];
+    const int t = threadIdx.x;
+    const int i = blockIdx.x * OUTW - 1 + t;
+    const int j0 = blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.ny);
+    const bool col_in = i >= 0 && i < fg.nx;
+    const bool owner = col_in && t >= 1 && t < TW - 1;
+    src.prepare(i);
+
+    double a = 0.0, b = 0.0, c = 0.0;  // corr rows J-2, J-1, J in own column
+    int any = 0;
+    const int Jbeg = j0 - 1;
+    const int Jend = j1;
+    ProlongRaw q[PF];
+    double dq[PF];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+        const int Jf = Jbeg + p;
+        q[p] = src.fetch(i, Jf);
+        dq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(d + fg.at(i, Jf - 1)) : 0.0;
+    }
+    for (int Jb = Jbeg; Jb <= Jend; Jb += PF) {
+#pragma unroll
+        for (int p = 0; p < PF; ++p) {
+            const int J = Jb + p;
+            if (J > Jend) break;
+            const ProlongRaw raw = q[p];
+            const double dR = dq[p];
+            {
+                const int Jf = J + PF;
+                q[p] = src.fetch(i, Jf);
+                dq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(d + fg.at(i, Jf - 1)) : 0.0;
+            }
+            const double cj = (col_in && J >= 0 && J < fg.ny) ? src.make(raw, i, J) : 0.0;
+            a = b;
+            b = c;
+            c = cj;
+            const int R = J - 1;
+            const double xl = t > 0 ? xs[(J - 1) & 1][t - 1] : 0.0;
+            const double xr = t < TW - 1 ? xs[(J - 1) & 1][t + 1] : 0.0;
+            xs[J & 1][t] = cj;
+            if (owner && R >= j0 && R < j1) {
+                const double ac = stencil_apply(A, i, R, b, xl, xr, a, c);
+                const long long k = (long long)R * fg.nx + i;
+                T0[k] = ac * b;
+                T1[k] = dR * b;
+                any |= (b * b) != 0.0;
+            }
+            __syncthreads();
+        }
+    }
+    if (__syncthreads_or(any) && t == 0) atomicOr(nz, 1);
+}
+
 }  // namespace gmg_dev

@@ -1,25 +1,26 @@
 // Exact-order (bit-identical to a left-to-right loop) fp64 summation on the GPU.
-// Algorithm and invariants: seqsum_core.h. Four launches per call:
+// Algorithm and invariants: seqsum_core.h. Two launches per sum (+1 memset):
 //
-//   S1 k_ss_partial : per chunk of C = 8192 terms, an approximate (tree) sum.
-//   S2 k_ss_scan    : one CTA, approximate exclusive prefix over the chunks
-//                     -> a speculated running sum at every chunk start.
-//   S3 k_ss_walk    : per chunk, each thread walks its 32 consecutive terms from
-//                     the speculated state (chunk prefix + in-chunk thread
-//                     prefix), splitting them into in-binade integer segments
-//                     and break elements; a block-wide segmented scan merges
-//                     segments across threads, so a chunk yields
-//                     (#breaks + 1) records.
-//   S4 k_ss_chain   : one CTA per sum replays all records in order from the
-//                     exact state 0.0: validate+apply each segment (integer
-//                     add), real IEEE add for each break element. A segment
-//                     that fails validation (speculation wrong) or a chunk
-//                     with too many records falls back to literal sequential
-//                     adds over that chunk's terms.
+//   k_ss_walk  : one CTA per chunk of C = 8192 terms (chunks taken from an
+//                atomic ticket, so every predecessor is already running).
+//                (1) loads its terms, (2) publishes its approximate sum and
+//                obtains the approximate prefix of all earlier chunks by
+//                decoupled look-back — the speculated running sum at its start,
+//                (3) each thread walks its 32 consecutive terms from the
+//                speculated state, splitting them into in-binade integer
+//                segments and break elements, (4) a block-wide segmented scan
+//                merges segments across threads -> (#breaks + 1) records,
+//                (5) a second look-back over record counts gives the chunk's
+//                offset in one compact, chunk-ordered record array.
+//   k_ss_chain : one CTA per sum replays the records in order from the exact
+//                state 0.0 — validate+apply each segment (integer add), real
+//                IEEE add for each break element — while the other warps
+//                stream the next batch of records into shared memory. A
+//                segment that fails validation (a wrong speculation) makes the
+//                chain re-sum the rest of that chunk with literal adds.
 //
-// Terms are produced by a generator TG (element k in the reference's k order)
-// in S1, S3 and (rarely) S4, so the inputs are streamed from HBM twice; no
-// term array is materialised.
+// Term generators: `double term(int s, long long k)` returns term k (in the
+// reference's k = j*nx + i order) of sum s.
 #pragma once
 
 #include "common.cuh"
@@ -30,31 +31,77 @@ namespace gmg_dev {
 constexpr int kSsT = 256;             // threads per chunk
 constexpr int kSsEPT = 32;            // terms per thread
 constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk
-constexpr int kSsRMax = 256;          // records stored per chunk
-constexpr int kSsCap = 2048;          // records staged per chain batch
-constexpr int kSsFT = 2048;           // fallback tile
+constexpr int kSsBatch = 1024;        // records staged per chain batch
+constexpr int kSsMaxSums = 2;
+constexpr int kSsRMax = 512;         // records a chunk may store; more -> literal re-sum
 
-// ---- block reductions / scans (256 threads) --------------------------------
-template <int NS>
-__device__ __forceinline__ void block_sum(double (&v)[NS], double* red /* [NS][8] */) {
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        double x = v[s];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) == 0) red[s * 8 + (threadIdx.x >> 5)] = x;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        double x = 0.0;
-        for (int w = 0; w < 8; ++w) x += red[s * 8 + w];
-        v[s] = x;
-    }
-    __syncthreads();
+// Per-sum look-back state (zeroed before each k_ss_walk: flags, counters).
+struct SsState {
+    int* flag;       // [nch] 0 none, 1 aggregate published, 2 inclusive published
+    int* cflag;      // [nch] record-count look-back flags
+    int* ticket;     // [1]
+    int* total;      // [1] total records stored
+    double* agg;     // [nch]
+    double* incl;    // [nch]
+    int* cagg;       // [nch]
+    int* cincl;      // [nch]
+    gmg_ss::Rec* recs;
+    int cap;         // record capacity
+};
+struct SsPair {
+    SsState s[kSsMaxSums];
+};
+
+__device__ __forceinline__ int ld_flag(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_flag(int* p, int v) {
+    __threadfence();
+    *reinterpret_cast<volatile int*>(p) = v;
 }
 
-// exclusive prefix sum of a double over the block (approximate order)
+// Exclusive prefix for chunk c by decoupled look-back (one warp). T is double
+// (approximate running sums) or int (record counts).
+template <class T>
+__device__ T lookback(int c, const int* flag, const T* agg, const T* incl) {
+    const int lane = threadIdx.x & 31;
+    T acc = T(0);
+    int p = c - 1;
+    while (p >= 0) {
+        const int idx = p - lane;
+        int f = 2;
+        if (idx >= 0) {
+            do {
+                f = ld_flag(flag + idx);
+            } while (f == 0);
+        }
+        __threadfence();
+        const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = m2 ? __ffs(m2) - 1 : 32;  // nearest predecessor with an inclusive prefix
+        T v = T(0);
+        if (idx >= 0) {
+            if (lane < stop) v = __ldcg(agg + idx);
+            else if (lane == stop) v = __ldcg(incl + idx);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc += v;
+        if (stop < 32) break;
+        p -= 32;
+    }
+    return acc;
+}
+
+// ---- block helpers (256 threads) -------------------------------------------
+__device__ __forceinline__ double block_sum_d(double x, double* sw /* [8] */) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = x;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sw[w];
+    __syncthreads();
+    return t;
+}
+
 __device__ __forceinline__ double block_excl_sum_d(double x, double* sw /* [8] */) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double inc = x;
@@ -82,7 +129,7 @@ __device__ __forceinline__ int block_excl_sum_i(int x, int* sw /* [8] */, int* t
     if (lane == 31) sw[w] = inc;
     __syncthreads();
     int base = 0, tot = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+    for (int q = 0; q < 8; ++q) {
         if (q < w) base += sw[q];
         tot += sw[q];
     }
@@ -91,7 +138,7 @@ __device__ __forceinline__ int block_excl_sum_i(int x, int* sw /* [8] */, int* t
     return base + inc - x;
 }
 
-// segmented scan element: flag = "a break closed the run before this thread"
+// segmented scan element: f = "a break closed the run inside this thread"
 struct SegF {
     gmg_ss::Seg g;
     int f;
@@ -105,16 +152,20 @@ __device__ __forceinline__ SegF segf_combine(const SegF& a, const SegF& b) {
 __device__ __forceinline__ SegF segf_shfl_up(const SegF& x, int o) {
     SegF r;
     const uint32_t meta = static_cast<uint32_t>(x.g.E) | (static_cast<uint32_t>(x.g.neg) << 11) |
-                          (static_cast<uint32_t>(x.g.bad) << 12) | (static_cast<uint32_t>(x.f) << 13);
+                          (static_cast<uint32_t>(x.g.bad) << 12) | (static_cast<uint32_t>(x.f) << 13) |
+                          (static_cast<uint32_t>(x.g.len) << 14);
     const uint32_t m2 = __shfl_up_sync(0xffffffffu, meta, o);
-    r.g.len = __shfl_up_sync(0xffffffffu, x.g.len, o);
-    r.g.Q = __shfl_up_sync(0xffffffffu, x.g.Q, o);
-    r.g.mn = __shfl_up_sync(0xffffffffu, x.g.mn, o);
-    r.g.mx = __shfl_up_sync(0xffffffffu, x.g.mx, o);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        r.g.Q[p] = __shfl_up_sync(0xffffffffu, x.g.Q[p], o);
+        r.g.mn[p] = __shfl_up_sync(0xffffffffu, x.g.mn[p], o);
+        r.g.mx[p] = __shfl_up_sync(0xffffffffu, x.g.mx[p], o);
+    }
     r.g.E = m2 & 0x7ff;
     r.g.neg = (m2 >> 11) & 1;
     r.g.bad = (m2 >> 12) & 1;
     r.f = (m2 >> 13) & 1;
+    r.g.len = static_cast<int>(m2 >> 14);
     return r;
 }
 
@@ -127,7 +178,7 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [8
         const SegF y = segf_shfl_up(inc, o);
         if (lane >= o) inc = segf_combine(y, inc);
     }
-    SegF ex = segf_shfl_up(inc, 1);
+    const SegF ex = segf_shfl_up(inc, 1);
     if (lane == 31) sw[w] = inc;
     __syncthreads();
     SegF base;
@@ -144,332 +195,325 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [8
     return segf_combine(base, ex);
 }
 
-// ---- S1 --------------------------------------------------------------------
-template <class TG>
-__global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double* __restrict__ csum,
-                                                     int nch, int* __restrict__ nzflag) {
-    constexpr int NS = TG::NS;
-    __shared__ double red[NS * 8];
-    const long long base = (long long)blockIdx.x * kSsC;
-    double acc[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    int nz = 0;
-#pragma unroll 4
-    for (int m = 0; m < kSsEPT; ++m) {
-        const long long k = base + m * kSsT + threadIdx.x;
-        if (k < n) {
-            double p[NS];
-            int z = 0;
-            tg.get(k, p, z);
-#pragma unroll
-            for (int s = 0; s < NS; ++s) acc[s] += p[s];
-            nz |= z;
-        }
-    }
-    const int anynz = __syncthreads_or(nz);
-    block_sum<NS>(acc, red);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) csum[(long long)s * nch + blockIdx.x] = acc[s];
-        if (nzflag && anynz) atomicOr(nzflag, 1);
-    }
-}
-
-// ---- S2 --------------------------------------------------------------------
-template <int NS>
-__global__ void __launch_bounds__(1024) k_ss_scan(const double* __restrict__ csum,
-                                                  double* __restrict__ cpred, int nch) {
-    __shared__ double sw[32];
-    const int T = blockDim.x;
-    const int per = (nch + T - 1) / T;
-    const int c0 = threadIdx.x * per;
-    const int c1 = min(c0 + per, nch);
-    for (int s = 0; s < NS; ++s) {
-        const double* cs = csum + (long long)s * nch;
-        double loc = 0.0;
-        for (int c = c0; c < c1; ++c) loc += cs[c];
-        // block exclusive scan over 1024 threads
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        double inc = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        if (lane == 31) sw[w] = inc;
-        __syncthreads();
-        double base = 0.0;
-        for (int q = 0; q < w; ++q) base += sw[q];
-        __syncthreads();
-        double run = base + inc - loc;
-        for (int c = c0; c < c1; ++c) {
-            cpred[(long long)s * nch + c] = run;
-            run += cs[c];
-        }
-    }
-}
-
-// ---- S3 --------------------------------------------------------------------
 __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 
+// ---- walk ---------------------------------------------------------------------
+// grid (nch, NS); block kSsT; dynamic smem (kSsC + kSsC/32) doubles.
 template <class TG>
-__global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, const double* __restrict__ cpred,
-                                                  int nch, int* __restrict__ counts,
-                                                  gmg_ss::Rec* __restrict__ recs) {
-    constexpr int NS = TG::NS;
-    extern __shared__ double tm[];  // [NS][kSsC + kSsC/32]
+__global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
+    extern __shared__ double tm[];
     __shared__ double swd[8];
     __shared__ int swi[8];
     __shared__ SegF sws[8];
-    constexpr int STRIDE = kSsC + kSsC / 32;
+    __shared__ int s_chunk;
+    __shared__ double s_pre;
+    __shared__ int s_off;
 
-    const int c = blockIdx.x;
+    const int s = blockIdx.y;
+    const SsState& S = sts.s[s];
+    const int t = threadIdx.x;
+    if (t == 0) s_chunk = atomicAdd(S.ticket, 1);
+    __syncthreads();
+    const int c = s_chunk;
     const long long base = (long long)c * kSsC;
     const int clen = (int)min((long long)kSsC, n - base);
-    const int t = threadIdx.x;
 
-#pragma unroll 4
+    // (1) terms: striped (coalesced) loads into shared memory
+#pragma unroll 8
     for (int m = 0; m < kSsEPT; ++m) {
         const int kl = m * kSsT + t;
-        double p[NS];
-        int z = 0;
-        if (kl < clen) {
-            tg.get(base + kl, p, z);
-        } else {
-#pragma unroll
-            for (int s = 0; s < NS; ++s) p[s] = 0.0;
-        }
-#pragma unroll
-        for (int s = 0; s < NS; ++s) tm[s * STRIDE + ss_pad(kl)] = p[s];
+        tm[ss_pad(kl)] = kl < clen ? tg.term(s, base + kl) : 0.0;
     }
     __syncthreads();
-
     const int e0 = t * kSsEPT;
     const int ne = max(0, min(kSsEPT, clen - e0));
+    double ts = 0.0;
+    for (int m = 0; m < ne; ++m) ts += tm[ss_pad(e0 + m)];
 
-    for (int s = 0; s < NS; ++s) {
-        const double* P = tm + s * STRIDE;
-        double ts = 0.0;
-        for (int m = 0; m < ne; ++m) ts += P[ss_pad(e0 + m)];
-        const double pred = cpred[(long long)s * nch + c] + block_excl_sum_d(ts, swd);
+    // (2) approximate prefix by look-back
+    const double tot_approx = block_sum_d(ts, swd);
+    if (t == 0) {
+        if (c == 0) {
+            S.incl[0] = tot_approx;
+            st_flag(S.flag, 2);
+        } else {
+            S.agg[c] = tot_approx;
+            st_flag(S.flag + c, 1);
+        }
+    }
+    if (t < 32) {
+        const double pre = c == 0 ? 0.0 : lookback<double>(c, S.flag, S.agg, S.incl);
+        if (t == 0) {
+            s_pre = pre;
+            if (c > 0) {
+                S.incl[c] = pre + tot_approx;
+                st_flag(S.flag + c, 2);
+            }
+        }
+    }
+    __syncthreads();
+    const double pred = s_pre + block_excl_sum_d(ts, swd);
 
-        // pass 1: leading segment, trailing segment, break count
-        gmg_ss::State st = gmg_ss::make_state(pred);
-        gmg_ss::Seg cur = gmg_ss::seg_empty(), lead = gmg_ss::seg_empty();
-        int r = 0;
-        double pb0 = 0.0;
+    // (3) thread walk, pass 1: leading segment, trailing segment, break count
+    gmg_ss::State st = gmg_ss::make_state(pred);
+    gmg_ss::Seg cur = gmg_ss::seg_empty(), lead = gmg_ss::seg_empty();
+    int r = 0;
+    double pb0 = 0.0;
+    for (int m = 0; m < ne; ++m) {
+        const double p = tm[ss_pad(e0 + m)];
+        if (!gmg_ss::walk_try(st, cur, p)) {
+            if (r == 0) {
+                lead = cur;
+                pb0 = p;
+            }
+            ++r;
+            cur = gmg_ss::seg_empty();
+            gmg_ss::real_add(st, p);
+        }
+    }
+    if (r == 0) lead = cur;
+
+    // (4) merge runs across threads
+    SegF x;
+    x.f = r > 0;
+    x.g = r > 0 ? cur : lead;
+    SegF tot;
+    const SegF carry = block_excl_segscan(x, sws, &tot);
+    int R;
+    const int pos = block_excl_sum_i(r, swi, &R);
+    R += 1;
+
+    // (5) record offset by look-back over stored counts (aggregate published
+    //     before looking back, so chunks never wait on a predecessor's look-back)
+    const int stored = R <= kSsRMax ? R : 1;
+    if (t == 0) {
+        if (c == 0) {
+            S.cincl[0] = stored;
+            st_flag(S.cflag, 2);
+        } else {
+            S.cagg[c] = stored;
+            st_flag(S.cflag + c, 1);
+        }
+    }
+    if (t < 32) {
+        const int o = c == 0 ? 0 : lookback<int>(c, S.cflag, S.cagg, S.cincl);
+        if (t == 0) {
+            if (c > 0) {
+                S.cincl[c] = o + stored;
+                st_flag(S.cflag + c, 2);
+            }
+            if (c == nch - 1) *S.total = o + stored;
+            s_off = o;
+        }
+    }
+    __syncthreads();
+    const int off = s_off;
+    if (stored != R) {  // too many breaks: the chain sums this chunk literally
+        if (t == 0) S.recs[off] = gmg_ss::rec_literal(c);
+        return;
+    }
+    gmg_ss::Rec* out = S.recs + off;
+    if (r > 0) {
+        // pass 2: emit records; the first one absorbs the run carried in
+        out[pos] = gmg_ss::rec_make(gmg_ss::seg_merge(carry.g, lead), true, pb0, c);
+        st = gmg_ss::make_state(pred);
+        cur = gmg_ss::seg_empty();
+        int k = 0;
         for (int m = 0; m < ne; ++m) {
-            const double p = P[ss_pad(e0 + m)];
+            const double p = tm[ss_pad(e0 + m)];
             if (!gmg_ss::walk_try(st, cur, p)) {
-                if (r == 0) {
-                    lead = cur;
-                    pb0 = p;
-                }
-                ++r;
+                if (k > 0) out[pos + k] = gmg_ss::rec_make(cur, true, p, c);
+                ++k;
                 cur = gmg_ss::seg_empty();
                 gmg_ss::real_add(st, p);
             }
         }
-        if (r == 0) lead = cur;
-        SegF x;
-        x.f = r > 0;
-        x.g = r > 0 ? cur : lead;
-        SegF tot;
-        const SegF carry = block_excl_segscan(x, sws, &tot);
-        int R;
-        const int pos = block_excl_sum_i(r, swi, &R);
-        R += 1;
-        int* cnt = counts + (long long)s * nch + c;
-        gmg_ss::Rec* out = recs + ((long long)s * nch + c) * kSsRMax;
-        if (R > kSsRMax) {
-            if (t == 0) *cnt = -1;
-            continue;
-        }
-        if (r > 0) {
-            // pass 2: emit records; first one absorbs the run carried in
-            out[pos] = gmg_ss::rec_make(gmg_ss::seg_merge(carry.g, lead), true, pb0);
-            st = gmg_ss::make_state(pred);
-            cur = gmg_ss::seg_empty();
-            int k = 0;
-            for (int m = 0; m < ne; ++m) {
-                const double p = P[ss_pad(e0 + m)];
-                if (!gmg_ss::walk_try(st, cur, p)) {
-                    if (k > 0) out[pos + k] = gmg_ss::rec_make(cur, true, p);
-                    ++k;
-                    cur = gmg_ss::seg_empty();
-                    gmg_ss::real_add(st, p);
-                }
-            }
-        }
-        if (t == kSsT - 1) {
-            out[R - 1] = gmg_ss::rec_make(tot.g, false, 0.0);
-            *cnt = R;
-        }
     }
+    if (t == kSsT - 1) out[R - 1] = gmg_ss::rec_make(tot.g, false, 0.0, c);
 }
 
-// ---- S4 --------------------------------------------------------------------
+// ---- chain --------------------------------------------------------------------
+__device__ __forceinline__ gmg_ss::Seg seg_shfl(const gmg_ss::Seg& x, int src) {
+    gmg_ss::Seg r;
+    const uint32_t meta = static_cast<uint32_t>(x.E) | (static_cast<uint32_t>(x.neg) << 11) |
+                          (static_cast<uint32_t>(x.bad) << 12) | (static_cast<uint32_t>(x.len) << 13);
+    const uint32_t m2 = __shfl_sync(0xffffffffu, meta, src);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        r.Q[p] = __shfl_sync(0xffffffffu, x.Q[p], src);
+        r.mn[p] = __shfl_sync(0xffffffffu, x.mn[p], src);
+        r.mx[p] = __shfl_sync(0xffffffffu, x.mx[p], src);
+    }
+    r.E = m2 & 0x7ff;
+    r.neg = (m2 >> 11) & 1;
+    r.bad = (m2 >> 12) & 1;
+    r.len = static_cast<int>(m2 >> 13);
+    return r;
+}
+
+// Literal left-to-right adds over terms [k0, k1) of sum s.
 template <class TG>
-__global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, int nch,
-                                                   const int* __restrict__ counts,
-                                                   const gmg_ss::Rec* __restrict__ recs,
-                                                   double* __restrict__ out) {
-    constexpr int NS = TG::NS;
+__device__ double literal_sum(const TG& tg, int s, double a, long long k0, long long k1) {
+    for (long long k = k0; k < k1; ++k) a = a + tg.term(s, k);
+    return a;
+}
+
+// grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays the
+// records: in each window of 32 it merges the pure segments up to the first
+// break record with a parity-aware merge-scan, validates the merged run once
+// against the exact state and applies it, then performs that record's break
+// add. Warps 1.. stream the next batch into shared memory meanwhile.
+template <class TG>
+__global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out) {
     extern __shared__ unsigned char smraw[];
-    gmg_ss::Rec* rb = reinterpret_cast<gmg_ss::Rec*>(smraw);                     // [kSsCap]
-    double* ft = reinterpret_cast<double*>(smraw + sizeof(gmg_ss::Rec) * kSsCap);  // [kSsFT]
-    __shared__ int off[kSsT + 1];
-    __shared__ int cn[kSsT];
-    __shared__ int swi[8];
-    __shared__ int s_be, s_fb_chunk, s_fb_pos;
-    __shared__ double s_state;
-
+    gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
     const int s = blockIdx.x;
-    const int t = threadIdx.x;
-    const int* cnts = counts + (long long)s * nch;
-    gmg_ss::State st = gmg_ss::make_state(0.0);  // thread 0's running state
+    const SsState& S = sts.s[s];
+    const int t = threadIdx.x, lane = t & 31;
+    const int total = *S.total;
+    const int nb = (total + kSsBatch - 1) / kSsBatch;
 
-    int c0 = 0;
-    while (c0 < nch) {
-        const int cc = c0 + t;
-        const int craw = cc < nch ? cnts[cc] : 0;
-        const int nrec = craw > 0 ? craw : 0;
-        int total;
-        const int o = block_excl_sum_i(nrec, swi, &total);
-        off[t] = o;
-        cn[t] = craw;
-        if (t == 0) off[kSsT] = total;
-        __syncthreads();
-        // batch = longest prefix of chunks whose records fit the staging buffer
-        if (t == 0) {
-            int be = 0;
-            while (be < kSsT && c0 + be < nch && off[be + 1] <= kSsCap) ++be;
-            if (be == 0) be = 1;  // a single chunk always fits (kSsRMax <= kSsCap)
-            s_be = be;
-        }
-        __syncthreads();
-        const int be = s_be;
-        const int nstage = off[be];
-        for (int q = t; q < nstage; q += kSsT) {
-            int lo = 0, hi = be - 1;  // find chunk owning staged record q
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (off[mid] <= q) lo = mid; else hi = mid - 1;
-            }
-            rb[q] = recs[((long long)s * nch + c0 + lo) * kSsRMax + (q - off[lo])];
-        }
-        __syncthreads();
-        if (t == 0) {
-            int fb_chunk = -1, fb_pos = 0;
-            for (int b = 0; b < be && fb_chunk < 0; ++b) {
-                if (cn[b] < 0) {
-                    fb_chunk = b;
-                    fb_pos = 0;
-                    break;
-                }
-                int pos = 0;
-                for (int r = 0; r < cn[b]; ++r) {
-                    const gmg_ss::Rec& rec = rb[off[b] + r];
-                    const gmg_ss::Seg g = gmg_ss::rec_seg(rec);
-                    if (!gmg_ss::seg_valid(g, st)) {
-                        fb_chunk = b;
-                        fb_pos = pos;
-                        break;
+    for (int q = t; q < min(total, kSsBatch); q += kSsT) buf[q] = S.recs[q];
+    __syncthreads();
+
+    gmg_ss::State st = gmg_ss::make_state(0.0);  // identical in every lane of warp 0
+    long long cur_chunk = -1, skip = -1;
+    int pos = 0;
+    for (int b = 0; b < nb; ++b) {
+        const gmg_ss::Rec* A = buf + (b & 1) * kSsBatch;
+        const int cnt = min(kSsBatch, total - b * kSsBatch);
+        if (t < 32) {
+            int q = 0;
+            while (q < cnt) {
+                const int idx = q + lane;
+                const bool have = idx < cnt;
+                gmg_ss::Rec rec{};
+                if (have) rec = A[idx];
+                const long long c = have ? (long long)rec.chunk : -2;
+                const bool lit = have && gmg_ss::rec_literal_flag(rec);
+                const bool skipme = have && c == skip;
+                const bool brk = have && !lit && !skipme && gmg_ss::rec_has_break(rec);
+                const unsigned stopm = __ballot_sync(0xffffffffu, !have || brk || lit || skipme);
+                const int f = stopm ? __ffs(stopm) - 1 : 32;  // lanes < f: pure segments
+                // Runs of >= 3 pure segments are merged with a warp merge-scan; break
+                // records (and short runs) take the cheap serial path below.
+                if (f >= 3) {
+                    const int run_end = f - 1;
+                    gmg_ss::Seg g = (lane <= run_end) ? gmg_ss::rec_seg(rec) : gmg_ss::seg_empty();
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const gmg_ss::Seg y = seg_shfl(g, lane >= o ? lane - o : lane);
+                        if (lane >= o) g = gmg_ss::seg_merge(y, g);
                     }
-                    gmg_ss::seg_apply(g, st);
-                    pos += g.len;
-                    if (gmg_ss::rec_has_break(rec)) {
-                        gmg_ss::real_add(st, rec.pb);
-                        pos += 1;
+                    const gmg_ss::Seg run = seg_shfl(g, run_end);
+                    if (gmg_ss::seg_valid(run, st)) {
+                        const long long c_end = __shfl_sync(0xffffffffu, c, run_end);
+                        int my = (lane <= run_end && c == c_end) ? (int)(rec.meta >> 15) : 0;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+                        pos = (c_end == cur_chunk ? pos : 0) + my;
+                        cur_chunk = c_end;
+                        gmg_ss::seg_apply(run, st);
+                        q += run_end + 1;
+                        continue;
                     }
                 }
+                // serial handling of the window's first record
+                const gmg_ss::Rec r0 = A[q];
+                const long long c0 = r0.chunk;
+                ++q;
+                if (c0 == skip) continue;
+                if (c0 != cur_chunk) {
+                    cur_chunk = c0;
+                    pos = 0;
+                }
+                const gmg_ss::Seg g0 = gmg_ss::rec_seg(r0);
+                if (gmg_ss::rec_literal_flag(r0) || !gmg_ss::seg_valid(g0, st)) {
+                    double a = 0.0;
+                    if (lane == 0) a = literal_sum(tg, s, st.s, c0 * kSsC + pos, min(n, (c0 + 1) * kSsC));
+                    a = __shfl_sync(0xffffffffu, a, 0);
+                    st = gmg_ss::make_state(a);
+                    skip = c0;
+                    continue;
+                }
+                gmg_ss::seg_apply(g0, st);
+                pos += g0.len;
+                if (gmg_ss::rec_has_break(r0)) {
+                    gmg_ss::real_add(st, r0.pb);
+                    pos += 1;
+                }
             }
-            s_fb_chunk = fb_chunk;
-            s_fb_pos = fb_pos;
-            s_state = st.s;
+        } else if (b + 1 < nb) {
+            gmg_ss::Rec* B = buf + ((b + 1) & 1) * kSsBatch;
+            const int cn = min(kSsBatch, total - (b + 1) * kSsBatch);
+            const gmg_ss::Rec* src = S.recs + (long long)(b + 1) * kSsBatch;
+            for (int q = t - 32; q < cn; q += kSsT - 32) B[q] = src[q];
         }
-        __syncthreads();
-        const int fbc = s_fb_chunk;
-        if (fbc < 0) {
-            c0 += be;
-            continue;
-        }
-        // literal sequential adds over the rest of chunk c0+fbc
-        const long long cbase = (long long)(c0 + fbc) * kSsC;
-        const int clen = (int)min((long long)kSsC, n - cbase);
-        for (int e = s_fb_pos; e < clen; e += kSsFT) {
-            const int len = min(kSsFT, clen - e);
-            for (int q = t; q < len; q += kSsT) {
-                double p[NS];
-                int z = 0;
-                tg.get(cbase + e + q, p, z);
-                ft[q] = p[s];
-            }
-            __syncthreads();
-            if (t == 0) {
-                double a = s_state;
-                for (int q = 0; q < len; ++q) a = a + ft[q];
-                s_state = a;
-            }
-            __syncthreads();
-        }
-        if (t == 0) st = gmg_ss::make_state(s_state);
-        c0 += fbc + 1;
         __syncthreads();
     }
     if (t == 0) out[s] = st.s;
 }
 
-constexpr size_t ss_walk_smem(int ns) { return sizeof(double) * ns * (kSsC + kSsC / 32); }
-constexpr size_t ss_chain_smem() { return sizeof(gmg_ss::Rec) * kSsCap + sizeof(double) * kSsFT; }
+// Fast mode: tree-order partial sums per chunk, then one CTA finishes.
+template <class TG>
+__global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double* __restrict__ csum, int nch) {
+    __shared__ double swd[8];
+    const int s = blockIdx.y;
+    const long long base = (long long)blockIdx.x * kSsC;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int m = 0; m < kSsEPT; ++m) {
+        const long long k = base + m * kSsT + threadIdx.x;
+        if (k < n) acc += tg.term(s, k);
+    }
+    acc = block_sum_d(acc, swd);
+    if (threadIdx.x == 0) csum[(long long)s * nch + blockIdx.x] = acc;
+}
 
-// ---- term generators -------------------------------------------------------
-struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13)
+constexpr size_t ss_walk_smem() { return sizeof(double) * (kSsC + kSsC / 32); }
+constexpr size_t ss_chain_smem() { return sizeof(gmg_ss::Rec) * 2 * kSsBatch; }
+
+// ---- term generators ----------------------------------------------------------
+// row index j = k / nx without an integer division: fp64 estimate + exact fix-up
+__device__ __forceinline__ int row_of(long long k, int nx, double inv_nx) {
+    int j = (int)((double)k * inv_nx);
+    const long long r = k - (long long)j * nx;
+    j += (r >= nx) - (r < 0);
+    return j;
+}
+
+struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid function
     static constexpr int NS = 1;
     const double* r;
     Grid g;
-    __device__ __forceinline__ void get(long long k, double (&p)[1], int& nz) const {
-        const int j = (int)(k / g.nx), i = (int)(k - (long long)j * g.nx);
+    double inv_nx;
+    __device__ __forceinline__ double term(int, long long k) const {
+        const int j = row_of(k, g.nx, inv_nx), i = (int)(k - (long long)j * g.nx);
         const double v = __ldg(r + g.at(i, j));
-        p[0] = v * v;
-        nz = 0;
+        return v * v;
     }
 };
 
-struct DotTerms {  // a_k * b_k (dot, stencil.cpp:21-26)
+struct DotTerms {  // a_k * b_k (dot, stencil.cpp:21-26) on flat arrays
     static constexpr int NS = 1;
     const double *a, *b;
-    Grid g;
-    __device__ __forceinline__ void get(long long k, double (&p)[1], int& nz) const {
-        const int j = (int)(k / g.nx), i = (int)(k - (long long)j * g.nx);
-        const long long o = g.at(i, j);
-        p[0] = __ldg(a + o) * __ldg(b + o);
-        nz = 0;
+    __device__ __forceinline__ double term(int, long long k) const { return __ldg(a + k) * __ldg(b + k); }
+};
+
+struct FlatNormTerms {  // v_k * v_k on a flat array
+    static constexpr int NS = 1;
+    const double* a;
+    __device__ __forceinline__ double term(int, long long k) const {
+        const double v = __ldg(a + k);
+        return v * v;
     }
 };
 
-// adaptive_omega (cycle.cpp:40-51) on corr = P uc computed on the fly:
-// p[0] = (A corr)_k * corr_k, p[1] = d_k * corr_k, nz |= corr_k*corr_k != 0.
-template <class Coef>
-struct OmegaTerms {
+struct ArrTerms {  // materialised terms: sum s reads t[s][k]
     static constexpr int NS = 2;
-    const double* d;
-    Grid g;
-    Coef A;
-    Prolong P;
-    __device__ __forceinline__ double corr(int i, int j) const {
-        return g.inside(i, j) ? P.at(i, j) : 0.0;
-    }
-    __device__ __forceinline__ void get(long long k, double (&p)[2], int& nz) const {
-        const int j = (int)(k / g.nx), i = (int)(k - (long long)j * g.nx);
-        const double cc = corr(i, j);
-        const double ac = stencil_apply(A, i, j, cc, corr(i - 1, j), corr(i + 1, j), corr(i, j - 1),
-                                        corr(i, j + 1));
-        p[0] = ac * cc;
-        p[1] = __ldg(d + g.at(i, j)) * cc;
-        nz = (cc * cc) != 0.0;
-    }
+    const double* t0;
+    const double* t1;
+    __device__ __forceinline__ double term(int s, long long k) const { return __ldg((s ? t1 : t0) + k); }
 };
 
 }  // namespace gmg_dev

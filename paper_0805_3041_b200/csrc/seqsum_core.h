@@ -1,21 +1,21 @@
 // Exact emulation of the reference's left-to-right fp64 summation
 //   double s = 0.0; for (k) s += p[k];      (stencil.cpp:9-13,21-26; cycle.cpp:44)
 // split into parallel pieces. Shared by the CUDA kernels (seqsum.cuh) and the
-// host emulation used by the CPU tests (host_seqsum.cpp).
+// host emulation used by the CPU tests (host_setup.cpp).
 //
 // Idea: while the running sum s stays inside one binade
 // [2^(e-1), 2^e) its representable neighbours are the multiples of
 // u = ulp(s) = 2^(e-53), so fl(s + p) = s + u*RN(p/u) — the sum is an exact
-// integer prefix sum M_k = s/u + sum q_j with q_j = RN(p_j/u). Only three
-// situations need a real IEEE add ("break"): the state is zero/subnormal/huge,
-// p/u is an exact half-integer (tie, resolved by the parity of the total), or
-// the integer state would leave the open binade (|M| outside [2^52+1, 2^53-1];
-// the +1 keeps a result that lands just below 2^(e-1), where the spacing halves,
-// out of the integer model).
+// integer prefix sum M_k = s/u + sum q_j with q_j = RN(p_j/u) (an exact
+// half-integer p/u rounds to the even total; see Seg). Only two situations need
+// a real IEEE add ("break"): the state is zero/subnormal/huge or |p/u| >= 2^52,
+// or the integer state would leave the open binade (|M| outside
+// [2^52+1, 2^53-1]; the +1 keeps a result that lands just below 2^(e-1), where
+// the spacing halves, out of the integer model).
 //
 // A *segment* is a run of elements summed in one binade; it is described by
-// (E, sign, Q, minP, maxP): Q is the integer total in units of u, minP/maxP the
-// extremes of its inclusive prefixes. Given the EXACT state M entering it, a
+// (E, sign, Q, minP, maxP) (two variants, see Seg): Q is the integer total in
+// units of u, minP/maxP the extremes of its inclusive prefixes. Given the EXACT state M entering it, a
 // segment is valid iff E and sign match and M+minP, M+maxP stay in range —
 // then the exit state is exactly M+Q. Segments merge associatively when E and
 // sign agree. A *record* is a segment optionally followed by one break element
@@ -96,12 +96,17 @@ SS_HD double compose(int64_t M, int E) {
     return bitsd((neg << 63) | (static_cast<uint64_t>(E) << 52) | (a - (uint64_t(1) << 52)));
 }
 
+// A segment carries two variants, indexed by the parity of the exact integer
+// state entering it: an exact tie (p/u = n + 1/2) rounds to the even total, so
+// q = n + ((M + n) & 1) depends only on M's parity — and after the first tie
+// the running state is even in both variants. Ties therefore stay inside the
+// integer model instead of forcing a real add.
 struct Seg {
     int E;     // binade of the segment (meaningless when len == 0)
     int neg;   // sign of the running sum inside the segment
     int len;   // number of elements; 0 = empty (identity for merge)
     int bad;   // 1 = produced by merging incompatible segments (forces a fallback)
-    int64_t Q, mn, mx;
+    int64_t Q[2], mn[2], mx[2];
 };
 
 SS_HD Seg seg_empty() {
@@ -110,9 +115,7 @@ SS_HD Seg seg_empty() {
     s.neg = 0;
     s.len = 0;
     s.bad = 0;
-    s.Q = 0;
-    s.mn = 0;
-    s.mx = 0;
+    for (int p = 0; p < 2; ++p) s.Q[p] = s.mn[p] = s.mx[p] = 0;
     return s;
 }
 
@@ -124,10 +127,14 @@ SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
     r.neg = a.neg;
     r.len = a.len + b.len;
     r.bad = a.bad | b.bad | (a.E != b.E) | (a.neg != b.neg);
-    r.Q = a.Q + b.Q;
-    const int64_t bmn = a.Q + b.mn, bmx = a.Q + b.mx;
-    r.mn = a.mn < bmn ? a.mn : bmn;
-    r.mx = a.mx > bmx ? a.mx : bmx;
+    for (int p = 0; p < 2; ++p) {
+        const int64_t qa = a.Q[p];
+        const int pb = static_cast<int>((p + qa) & 1);
+        r.Q[p] = qa + b.Q[pb];
+        const int64_t bmn = qa + b.mn[pb], bmx = qa + b.mx[pb];
+        r.mn[p] = a.mn[p] < bmn ? a.mn[p] : bmn;
+        r.mx[p] = a.mx[p] > bmx ? a.mx[p] : bmx;
+    }
     return r;
 }
 
@@ -135,52 +142,60 @@ SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
 SS_HD bool seg_valid(const Seg& g, const State& st) {
     if (g.len == 0) return !g.bad;
     if (g.bad || st.E == 0 || st.E != g.E || (st.M < 0) != (g.neg != 0)) return false;
-    if (!g.neg) return st.M + g.mn >= kLo && st.M + g.mx <= kHi;
-    return st.M + g.mx <= -kLo && st.M + g.mn >= -kHi;
+    const int p = static_cast<int>(st.M & 1);
+    if (!g.neg) return st.M + g.mn[p] >= kLo && st.M + g.mx[p] <= kHi;
+    return st.M + g.mx[p] <= -kLo && st.M + g.mn[p] >= -kHi;
 }
 
 // Apply a valid segment.
 SS_HD void seg_apply(const Seg& g, State& st) {
     if (g.len == 0) return;
-    st.M += g.Q;
+    st.M += g.Q[st.M & 1];
     st.s = compose(st.M, st.E);
 }
 
 // Sequential walker: advances a (speculated or exact) state element by element,
-// accumulating the current segment, reporting breaks. Returns true if element p
-// was absorbed into the current segment, false if it is a break (the caller
-// closes the segment, then calls real_add).
+// accumulating the current segment. Returns true if element p was absorbed,
+// false if it is a break (the caller closes the segment, then calls real_add).
 SS_HD bool walk_try(State& st, Seg& cur, double p) {
     if (st.E == 0) return false;
     const double x = p * st.inv_u;  // exact power-of-two scaling
     if (!(x < kTwo52 && x > -kTwo52)) return false;
 #ifdef __CUDA_ARCH__
     const double fl = floor(x);
-    const double q = rint(x);
 #else
     const double fl = __builtin_floor(x);
-    const double q = __builtin_rint(x);
 #endif
-    if (x - fl == 0.5) return false;  // exact tie: rounding depends on the total's parity
-    const int64_t qi = static_cast<int64_t>(q);
-    const int64_t Mn = st.M + qi;
+    const double fr = x - fl;  // exact
+    const int64_t n = static_cast<int64_t>(fl);
+    const bool tie = fr == 0.5;
+    const int64_t qr = n + (fr > 0.5 ? 1 : 0);  // non-tie rounding
+    const int64_t qs = tie ? n + ((st.M + n) & 1) : qr;
+    const int64_t Mn = st.M + qs;
     if (st.M >= 0) {
         if (Mn < kLo || Mn > kHi) return false;
     } else {
         if (Mn > -kLo || Mn < -kHi) return false;
     }
-    st.M = Mn;
     if (cur.len == 0) {
         cur.E = st.E;
         cur.neg = st.M < 0;
-        cur.Q = qi;
-        cur.mn = qi;
-        cur.mx = qi;
-    } else {
-        cur.Q += qi;
-        cur.mn = cur.Q < cur.mn ? cur.Q : cur.mn;
-        cur.mx = cur.Q > cur.mx ? cur.Q : cur.mx;
+        for (int v = 0; v < 2; ++v) cur.Q[v] = cur.mn[v] = cur.mx[v] = 0;
     }
+    for (int v = 0; v < 2; ++v) {
+        // variant v: segment entered with parity v; current parity (v + Q[v]) & 1
+        const int64_t q = tie ? n + ((v + cur.Q[v] + n) & 1) : qr;
+        const int64_t P = cur.Q[v] + q;
+        if (cur.len == 0) {
+            cur.mn[v] = P;
+            cur.mx[v] = P;
+        } else {
+            cur.mn[v] = P < cur.mn[v] ? P : cur.mn[v];
+            cur.mx[v] = P > cur.mx[v] ? P : cur.mx[v];
+        }
+        cur.Q[v] = P;
+    }
+    st.M = Mn;
     cur.len += 1;
     return true;
 }
@@ -191,23 +206,35 @@ SS_HD void real_add(State& st, double p) {
     st = make_state(s);
 }
 
-// Record as stored for the chain: segment, then optionally one break element.
+// Record as stored for the chain: a segment, then optionally one break element
+// (applied with a real add). 64 bytes.
+//   meta: E (11b) | neg<<11 | has_break<<12 | bad<<13 | literal<<14 | len<<15 (16b)
+// `literal` marks a chunk whose records did not fit: the chain re-sums it
+// with literal adds.
 struct Rec {
-    int64_t Q, mn, mx;
-    double pb;         // break element value
-    uint32_t meta;     // E (11b) | neg<<11 | has_break<<12 | bad<<13
-    int32_t len;       // segment length (elements); break element not counted
+    int64_t Q[2], mn[2], mx[2];
+    double pb;
+    uint32_t meta;
+    uint32_t chunk;
 };
 
-SS_HD Rec rec_make(const Seg& g, bool has_break, double pb) {
+SS_HD Rec rec_make(const Seg& g, bool has_break, double pb, uint32_t chunk) {
     Rec r;
-    r.Q = g.Q;
-    r.mn = g.mn;
-    r.mx = g.mx;
+    for (int p = 0; p < 2; ++p) {
+        r.Q[p] = g.Q[p];
+        r.mn[p] = g.mn[p];
+        r.mx[p] = g.mx[p];
+    }
     r.pb = pb;
     r.meta = static_cast<uint32_t>(g.E & 0x7ff) | (static_cast<uint32_t>(g.neg) << 11) |
-             (static_cast<uint32_t>(has_break) << 12) | (static_cast<uint32_t>(g.bad) << 13);
-    r.len = g.len;
+             (static_cast<uint32_t>(has_break) << 12) | (static_cast<uint32_t>(g.bad) << 13) |
+             (static_cast<uint32_t>(g.len) << 15);
+    r.chunk = chunk;
+    return r;
+}
+SS_HD Rec rec_literal(uint32_t chunk) {
+    Rec r = rec_make(seg_empty(), false, 0.0, chunk);
+    r.meta |= 1u << 14;
     return r;
 }
 SS_HD Seg rec_seg(const Rec& r) {
@@ -215,12 +242,15 @@ SS_HD Seg rec_seg(const Rec& r) {
     g.E = static_cast<int>(r.meta & 0x7ff);
     g.neg = static_cast<int>((r.meta >> 11) & 1);
     g.bad = static_cast<int>((r.meta >> 13) & 1);
-    g.len = r.len;
-    g.Q = r.Q;
-    g.mn = r.mn;
-    g.mx = r.mx;
+    g.len = static_cast<int>(r.meta >> 15);
+    for (int p = 0; p < 2; ++p) {
+        g.Q[p] = r.Q[p];
+        g.mn[p] = r.mn[p];
+        g.mx[p] = r.mx[p];
+    }
     return g;
 }
 SS_HD bool rec_has_break(const Rec& r) { return (r.meta >> 12) & 1; }
+SS_HD bool rec_literal_flag(const Rec& r) { return (r.meta >> 14) & 1; }
 
 }  // namespace gmg_ss

@@ -107,9 +107,13 @@ struct gmg_problem {
     int cn = 0, cbw = 0;
     // exact-order summation workspace
     int nch_max = 0;
-    double *csum = nullptr, *cpred = nullptr;
-    int* counts = nullptr;
-    gmg_ss::Rec* recs = nullptr;
+    double* csum = nullptr;          // fast-mode partials [2][nch]
+    double* T = nullptr;             // materialised omega terms, 2 x N_L dense
+    double* lb = nullptr;            // look-back values: per sum agg, incl [nch] each
+    int* lbi = nullptr;              // per sum: cagg, cincl [nch] each
+    int* flags = nullptr;            // per sum: ticket, total, flag[nch], cflag[nch]
+    gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records
+    int rec_cap = 0;
     double* sums = nullptr;  // [0..1] omega sums, [2] residual norm^2, [3] misc
     int* nz = nullptr;
     int* status = nullptr;
@@ -194,32 +198,37 @@ __global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, d
     }
 }
 
-// adaptive_omega on two explicit arrays (unit op): (A corr, corr) and (d, corr).
+// adaptive_omega on two explicit arrays (unit op): writes (A corr)_k corr_k and
+// d_k corr_k densely, and whether some corr_k^2 != 0.
 template <class Coef>
-struct OmegaTermsField {
-    static constexpr int NS = 2;
-    const double *d, *cr;
-    Grid g;
-    Coef A;
-    __device__ __forceinline__ double C(int i, int j) const {
-        return g.inside(i, j) ? __ldg(cr + g.at(i, j)) : 0.0;
-    }
-    __device__ __forceinline__ void get(long long k, double (&p)[2], int& nz) const {
-        const int j = (int)(k / g.nx), i = (int)(k - (long long)j * g.nx);
-        const double cc = C(i, j);
-        const double ac = stencil_apply(A, i, j, cc, C(i - 1, j), C(i + 1, j), C(i, j - 1), C(i, j + 1));
-        p[0] = ac * cc;
-        p[1] = __ldg(d + g.at(i, j)) * cc;
-        nz = (cc * cc) != 0.0;
-    }
-};
+__global__ void k_omega_terms_field(Grid g, Coef A, const double* __restrict__ d, const double* __restrict__ cr,
+                                    double* __restrict__ T0, double* __restrict__ T1, int* __restrict__ nz) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= g.nx || j >= g.ny) return;
+    auto C = [&](int a, int b) { return g.inside(a, b) ? __ldg(cr + g.at(a, b)) : 0.0; };
+    const double cc = C(i, j);
+    const double ac = stencil_apply(A, i, j, cc, C(i - 1, j), C(i + 1, j), C(i, j - 1), C(i, j + 1));
+    const long long k = (long long)j * g.nx + i;
+    T0[k] = ac * cc;
+    T1[k] = __ldg(d + g.at(i, j)) * cc;
+    if ((cc * cc) != 0.0) atomicOr(nz, 1);
+}
 
 // ---------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------
 constexpr int kTW = 128;
 
-int seg_rows(int ny) { return ny <= 128 ? ((ny + 1) & ~1) : 128; }
+// Rows per CTA segment: 128 on large levels; on small levels short segments so
+// the grid has enough CTAs and each marches few rows (the march is latency-bound
+// per row). Always even (the restriction pairs fine rows).
+int seg_rows(int nx, int ny) {
+    const int strips = (nx + 123) / 124;
+    int seg = 128;
+    while (seg > 8 && (long long)strips * ((ny + seg - 1) / seg) < 2 * 148) seg /= 2;
+    return seg;
+}
 
 template <class F>
 void with_coef(const Lev& L, F&& f) {
@@ -234,26 +243,50 @@ void set_smem(T* fn, size_t bytes) {
                             (int)bytes));
 }
 
+SsPair ss_state(gmg_problem* p, int nch) {
+    SsPair sp{};
+    for (int s = 0; s < kSsMaxSums; ++s) {
+        SsState& S = sp.s[s];
+        int* f = p->flags + (size_t)s * (2 + 2 * (size_t)p->nch_max);
+        S.ticket = f;
+        S.total = f + 1;
+        S.flag = f + 2;
+        S.cflag = f + 2 + nch;
+        S.agg = p->lb + (size_t)s * 2 * p->nch_max;
+        S.incl = S.agg + p->nch_max;
+        S.cagg = p->lbi + (size_t)s * 2 * p->nch_max;
+        S.cincl = S.cagg + p->nch_max;
+        S.recs = p->recs + (size_t)s * p->rec_cap;
+        S.cap = p->rec_cap;
+    }
+    return sp;
+}
+
+// Sums of TG's NS term sequences, each bit-identical to the reference's
+// left-to-right loop (mode EXACT) or in tree order (mode FAST); out[s].
 template <class TG>
-void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int* nz, int mode) {
+void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int mode) {
     constexpr int NS = TG::NS;
     const int nch = (int)((n + kSsC - 1) / kSsC);
     if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
     static bool attr_done = false;
     if (!attr_done) {
-        set_smem(k_ss_walk<TG>, ss_walk_smem(NS));
+        set_smem(k_ss_walk<TG>, ss_walk_smem());
         set_smem(k_ss_chain<TG>, ss_chain_smem());
         attr_done = true;
     }
-    if (nz) CK(cudaMemsetAsync(nz, 0, sizeof(int), p->st));
-    k_ss_partial<TG><<<nch, kSsT, 0, p->st>>>(tg, n, p->csum, nch, nz);
     if (mode == GMG_REDUCE_FAST) {
+        k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
         k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out);
+        CK(cudaGetLastError());
         return;
     }
-    k_ss_scan<NS><<<1, 1024, 0, p->st>>>(p->csum, p->cpred, nch);
-    k_ss_walk<TG><<<nch, kSsT, ss_walk_smem(NS), p->st>>>(tg, n, p->cpred, nch, p->counts, p->recs);
-    k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, nch, p->counts, p->recs, out);
+    const SsPair sp = ss_state(p, nch);
+    for (int s = 0; s < NS; ++s)
+        CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
+    k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp);
+    k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, sp, out);
+    CK(cudaGetLastError());
 }
 
 Prolong prolong_from(gmg_problem* p, int coarse_level, const double* uc) {
@@ -275,7 +308,7 @@ template <int M, class Coef, class Src>
 void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, OmegaSrc om,
                      const double* g, double* out, double wd) {
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
-    const int seg = seg_rows(L.ny);
+    const int seg = seg_rows(L.nx, L.ny);
     dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.ny + seg - 1) / seg);
     k_smooth<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
     CK(cudaGetLastError());
@@ -346,7 +379,7 @@ double* smooth_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const
 template <class Coef, class Src>
 void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, const double* g,
                     double* dout, double* x0out, double* gc) {
-    const int seg = seg_rows(L.ny);
+    const int seg = seg_rows(L.nx, L.ny);
     dim3 grid((L.nx + (kTW - 4) - 1) / (kTW - 4), (L.ny + seg - 1) / seg);
     Grid cg{0, 0, 0};
     RestrictW rw{};
@@ -386,15 +419,23 @@ void launch_coarse(gmg_problem* p, const double* g, double* x) {
 }
 
 void norm_sum(gmg_problem* p, const Lev& L, const double* v, double* out, int mode) {
-    seqsum(p, NormTerms{v, L.grid()}, L.n(), out, nullptr, mode);
+    seqsum(p, NormTerms{v, L.grid(), 1.0 / L.nx}, L.n(), out, mode);
 }
 
+// adaptive_omega sums for corr = P uc: terms materialised by k_omega_terms.
 void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc, int mode) {
+    CK(cudaMemsetAsync(p->nz, 0, sizeof(int), p->st));
+    const int seg = seg_rows(L.nx, L.ny);
+    dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.ny + seg - 1) / seg);
+    SrcProlong src{prolong_from(p, L.l - 1, uc), L.nx, L.ny, 0.0};
+    double* T0 = p->T;
+    double* T1 = p->T + p->lev(p->L).n();
     with_coef(L, [&](const auto& A) {
         using C = std::decay_t<decltype(A)>;
-        OmegaTerms<C> tg{d, L.grid(), A, prolong_from(p, L.l - 1, uc)};
-        seqsum(p, tg, L.n(), p->sums, p->nz, mode);
+        k_omega_terms<kTW, 2, C><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, d, T0, T1, p->nz, seg);
     });
+    CK(cudaGetLastError());
+    seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, mode);
 }
 
 // ---------------------------------------------------------------------------
@@ -647,8 +688,10 @@ void free_problem(gmg_problem* p) {
     cudaFree(p->band);
     cudaFree(p->cscr);
     cudaFree(p->csum);
-    cudaFree(p->cpred);
-    cudaFree(p->counts);
+    cudaFree(p->T);
+    cudaFree(p->lb);
+    cudaFree(p->lbi);
+    cudaFree(p->flags);
     cudaFree(p->recs);
     cudaFree(p->sums);
     cudaFree(p->nz);
@@ -792,10 +835,15 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         p->B = p->xmem + 2 * F.elems + F.off0;
         const long long n = F.n();
         p->nch_max = (int)((n + kSsC - 1) / kSsC);
-        CK(cudaMalloc(&p->csum, 2 * p->nch_max * sizeof(double)));
-        CK(cudaMalloc(&p->cpred, 2 * p->nch_max * sizeof(double)));
-        CK(cudaMalloc(&p->counts, 2 * p->nch_max * sizeof(int)));
-        CK(cudaMalloc(&p->recs, 2 * (size_t)p->nch_max * kSsRMax * sizeof(gmg_ss::Rec)));
+        const size_t nm = p->nch_max;
+        CK(cudaMalloc(&p->csum, 2 * nm * sizeof(double)));
+        CK(cudaMalloc(&p->T, 2 * (size_t)n * sizeof(double)));
+        CK(cudaMalloc(&p->lb, 2 * 2 * nm * sizeof(double)));
+        CK(cudaMalloc(&p->lbi, 2 * 2 * nm * sizeof(int)));
+        CK(cudaMalloc(&p->flags, 2 * (2 + 2 * nm) * sizeof(int)));
+        // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
+        p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
+        CK(cudaMalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
         CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
         CK(cudaMalloc(&p->nz, sizeof(int)));
@@ -825,7 +873,7 @@ extern "C" {
 
 const char* gmg_last_error(void) { return g_last_error.c_str(); }
 
-const char* gmg_version(void) { return "gmg_b200 sm_100a; exact-order seqsum v1 (chunk 8192, rmax 256)"; }
+const char* gmg_version(void) { return "gmg_b200 sm_100a; exact-order seqsum v2 (chunk 8192, look-back, tie-parity segments)"; }
 
 int gmg_dev_problem_create(const gmg_problem_desc* desc, gmg_problem** out) {
     return guarded([&] { create_problem(desc, out); });
@@ -1015,11 +1063,15 @@ int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* d, const dou
         Lev& L = p->lev(level);
         upload(p, L, L.buf[DD], d, cudaMemcpyHostToDevice);
         upload(p, L, L.buf[U0], corr, cudaMemcpyHostToDevice);
+        CK(cudaMemsetAsync(p->nz, 0, sizeof(int), p->st));
+        double* T0 = p->T;
+        double* T1 = p->T + p->lev(p->L).n();
         with_coef(L, [&](const auto& A) {
-            using C = std::decay_t<decltype(A)>;
-            OmegaTermsField<C> tg{L.buf[DD], L.buf[U0], L.grid(), A};
-            seqsum(p, tg, L.n(), p->sums, p->nz, GMG_REDUCE_EXACT);
+            dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
+            k_omega_terms_field<<<gr, b, 0, p->st>>>(L.grid(), A, L.buf[DD], L.buf[U0], T0, T1, p->nz);
         });
+        CK(cudaGetLastError());
+        seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, GMG_REDUCE_EXACT);
         double h[2];
         int nz = 0;
         CK(cudaMemcpyAsync(h, p->sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->st));
@@ -1062,12 +1114,10 @@ static void flat_sum(gmg_problem* p, long long n, const double* a, const double*
         cudaFree(db);
         throw std::logic_error("norm/dot: vector longer than the finest level");
     }
-    Grid g{(int)std::min<long long>(n, INT_MAX), 1, n};
-    if (n > INT_MAX) throw std::logic_error("norm/dot: vector too long");
     if (b)
-        seqsum(p, DotTerms{da, db, g}, n, p->sums + 4, nullptr, mode);
+        seqsum(p, DotTerms{da, db}, n, p->sums + 4, mode);
     else
-        seqsum(p, NormTerms{da, g}, n, p->sums + 4, nullptr, mode);
+        seqsum(p, FlatNormTerms{da}, n, p->sums + 4, mode);
     *out = fetch_scalar(p, p->sums + 4);
     cudaFree(da);
     cudaFree(db);
