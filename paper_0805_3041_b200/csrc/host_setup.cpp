@@ -236,111 +236,73 @@ std::string check_nested(const Level& coarse, const Level& fine) {
 
 // ---------------------------------------------------------------------------
 // Host emulation of the device pipeline (seqsum.cuh) with identical chunking:
-// S1 approximate chunk sums, S2 approximate prefix, S3 per-thread speculative
-// walks + segmented merge into per-chunk records, S4 exact chain with
-// fallback. stats: [0] chunks, [1] records, [2] fallbacks, [3] breaks.
+// approximate prefixes as speculation, per-thread walks, runs merged across
+// threads and chunks, one record per break (+ the final record), replayed from
+// the exact state with literal re-sums of any record that fails validation.
+// stats: [0] chunks, [1] records, [2] literal re-sums, [3] breaks.
 double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* stats) {
     using namespace gmg_ss;
     const long long C = static_cast<long long>(T) * EPT;
     const long long nch = (n + C - 1) / C;
-    const int RMAX = 256;
-    std::vector<double> csum(nch, 0.0), cpred(nch, 0.0);
-    for (long long c = 0; c < nch; ++c) {
-        double a = 0.0;
-        for (long long k = c * C; k < std::min(n, (c + 1) * C); ++k) a += p[k];
-        csum[c] = a;
-    }
-    double run = 0.0;
-    for (long long c = 0; c < nch; ++c) {
-        cpred[c] = run;
-        run += csum[c];
-    }
-    std::vector<std::vector<Rec>> recs(nch);
-    std::vector<int> dirty(nch, 0);
+    std::vector<Rec> recs;
+    Seg carry = seg_empty();  // run since the last break, across chunks
+    double approx = 0.0;
     long long nbreaks = 0;
     for (long long c = 0; c < nch; ++c) {
         const long long base = c * C;
         const int clen = static_cast<int>(std::min(C, n - base));
-        std::vector<double> pred(T);
-        double acc = cpred[c];
+        double acc = approx;
         for (int t = 0; t < T; ++t) {
-            pred[t] = acc;
+            const double pred = acc;
             double ts = 0.0;
             for (int m = 0; m < EPT; ++m) {
                 const int e = t * EPT + m;
                 if (e < clen) ts += p[base + e];
             }
             acc += ts;
-        }
-        Seg carry = seg_empty();
-        int carry_f = 0;
-        std::vector<Rec> out;
-        for (int t = 0; t < T; ++t) {
-            State st = make_state(pred[t]);
+            State st = make_state(pred);
             Seg cur = seg_empty();
-            bool first = true;
             for (int m = 0; m < EPT; ++m) {
                 const int e = t * EPT + m;
                 if (e >= clen) break;
                 const double v = p[base + e];
                 if (!walk_try(st, cur, v)) {
                     ++nbreaks;
-                    if (first) {
-                        out.push_back(rec_make(seg_merge(carry, cur), true, v, (uint32_t)c));
-                        first = false;
-                    } else {
-                        out.push_back(rec_make(cur, true, v, (uint32_t)c));
-                    }
+                    recs.push_back(rec_make(seg_merge(carry, cur), true, v, static_cast<uint32_t>(base + e)));
+                    carry = seg_empty();
                     cur = seg_empty();
                     real_add(st, v);
                 }
             }
-            if (first) {
-                carry = seg_merge(carry, cur);
-            } else {
-                carry = cur;
-                carry_f = 1;
-            }
+            carry = seg_merge(carry, cur);
         }
-        (void)carry_f;
-        out.push_back(rec_make(carry, false, 0.0, (uint32_t)c));
-        if (static_cast<int>(out.size()) > RMAX) dirty[c] = 1;
-        recs[c] = std::move(out);
+        approx = acc;
     }
-    long long nrec = 0, nfb = 0;
+    recs.push_back(rec_make(carry, false, 0.0, static_cast<uint32_t>(n)));
+    long long nlit = 0, prev = -1;
     State st = make_state(0.0);
-    for (long long c = 0; c < nch; ++c) {
-        const long long base = c * C;
-        const int clen = static_cast<int>(std::min(C, n - base));
-        int pos = 0;
-        bool fb = dirty[c] != 0;
-        if (!fb) {
-            for (const Rec& r : recs[c]) {
-                ++nrec;
-                const Seg g = rec_seg(r);
-                if (!seg_valid(g, st)) {
-                    fb = true;
-                    break;
-                }
-                seg_apply(g, st);
-                pos += g.len;
-                if (rec_has_break(r)) {
-                    real_add(st, r.pb);
-                    pos += 1;
-                }
-            }
-        }
-        if (fb) {
-            ++nfb;
+    for (const Rec& r : recs) {
+        const Seg g = rec_seg(r);
+        const bool brk = rec_has_break(r);
+        const long long kb = r.kb;
+        if (!seg_valid(g, st)) {
+            ++nlit;
             double s = st.s;
-            for (int e = pos; e < clen; ++e) s = s + p[base + e];
+            for (long long k = prev + 1; k < std::min(kb, n); ++k) s = s + p[k];
             st = make_state(s);
+            if (brk) st = make_state(st.s + r.pb);
+        } else if (brk) {
+            const double sb = g.len ? compose(st.M + g.Q[st.M & 1], st.E) : st.s;
+            st = make_state(sb + r.pb);
+        } else {
+            seg_apply(g, st);
         }
+        prev = brk ? kb : n - 1;
     }
     if (stats) {
         stats[0] = nch;
-        stats[1] = nrec;
-        stats[2] = nfb;
+        stats[1] = static_cast<long long>(recs.size());
+        stats[2] = nlit;
         stats[3] = nbreaks;
     }
     return st.s;

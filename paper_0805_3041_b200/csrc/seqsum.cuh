@@ -1,23 +1,24 @@
 // Exact-order (bit-identical to a left-to-right loop) fp64 summation on the GPU.
-// Algorithm and invariants: seqsum_core.h. Two launches per sum (+1 memset):
+// Algorithm and invariants: seqsum_core.h. Two launches per call (+1 memset):
 //
-//   k_ss_walk  : one CTA per chunk of C = 8192 terms (chunks taken from an
-//                atomic ticket, so every predecessor is already running).
-//                (1) loads its terms, (2) publishes its approximate sum and
-//                obtains the approximate prefix of all earlier chunks by
-//                decoupled look-back — the speculated running sum at its start,
-//                (3) each thread walks its 32 consecutive terms from the
+//   k_ss_walk  : one CTA per chunk of C = 8192 terms, chunks taken from an
+//                atomic ticket so every predecessor is already running.
+//                (1) load the chunk's terms; (2) publish its approximate sum and
+//                get the approximate prefix of all earlier chunks by decoupled
+//                look-back: the speculated running sum at the chunk start;
+//                (3) each thread walks its 32 consecutive terms from its
 //                speculated state, splitting them into in-binade integer
-//                segments and break elements, (4) a block-wide segmented scan
-//                merges segments across threads -> (#breaks + 1) records,
-//                (5) a second look-back over record counts gives the chunk's
-//                offset in one compact, chunk-ordered record array.
-//   k_ss_chain : one CTA per sum replays the records in order from the exact
-//                state 0.0 — validate+apply each segment (integer add), real
-//                IEEE add for each break element — while the other warps
-//                stream the next batch of records into shared memory. A
-//                segment that fails validation (a wrong speculation) makes the
-//                chain re-sum the rest of that chunk with literal adds.
+//                segments and break elements; (4) a block segmented scan merges
+//                segments across threads; (5) a second decoupled look-back — a
+//                segmented scan over chunks — carries the run since the last
+//                break into the chunk and gives its record offset. Chunks without
+//                a break emit nothing; each break emits one record (the merged
+//                run before it + the break value), stored compactly in order.
+//   k_ss_chain : one CTA per sum replays the records from the exact state 0.0
+//                (warps 1.. stage batches into shared memory): validate the run
+//                and apply it as one integer add, then one real IEEE add for the
+//                break. A run that fails validation (wrong speculation) is
+//                re-summed literally over its own element range.
 //
 // Term generators: `double term(int s, long long k)` returns term k (in the
 // reference's k = j*nx + i order) of sum s.
@@ -33,20 +34,20 @@ constexpr int kSsEPT = 32;            // terms per thread
 constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
-constexpr int kSsRMax = 512;         // records a chunk may store; more -> literal re-sum
+constexpr int kSsRMax = 256;          // records a chunk may store; more -> literal re-sum
 
-// Per-sum look-back state (zeroed before each k_ss_walk: flags, counters).
+// Per-sum look-back state (flags, ticket and total zeroed before each walk).
 struct SsState {
-    int* flag;       // [nch] 0 none, 1 aggregate published, 2 inclusive published
-    int* cflag;      // [nch] record-count look-back flags
+    int* flag;       // [nch] approximate-sum look-back: 0 none, 1 aggregate, 2 inclusive
+    int* cflag;      // [nch] run/count look-back flags
     int* ticket;     // [1]
-    int* total;      // [1] total records stored
+    int* total;      // [1] records stored
     double* agg;     // [nch]
     double* incl;    // [nch]
-    int* cagg;       // [nch]
-    int* cincl;      // [nch]
+    unsigned char* cagg;   // [nch] ChunkAgg
+    unsigned char* cincl;  // [nch] ChunkAgg
     gmg_ss::Rec* recs;
-    int cap;         // record capacity
+    unsigned long long* stats;  // [8] calls, records, -, -, break adds, literal ranges, literal terms, chunks
 };
 struct SsPair {
     SsState s[kSsMaxSums];
@@ -58,12 +59,105 @@ __device__ __forceinline__ void st_flag(int* p, int v) {
     *reinterpret_cast<volatile int*>(p) = v;
 }
 
-// Exclusive prefix for chunk c by decoupled look-back (one warp). T is double
-// (approximate running sums) or int (record counts).
-template <class T>
-__device__ T lookback(int c, const int* flag, const T* agg, const T* incl) {
+// ---- segmented run values --------------------------------------------------
+// f = "a break happened inside", g = run since the last break (or the whole
+// span if none), cnt = records stored.
+struct SegF {
+    gmg_ss::Seg g;
+    int f;
+    int cnt;
+};
+__device__ __forceinline__ SegF segf_id() {
+    SegF r;
+    r.g = gmg_ss::seg_empty();
+    r.f = 0;
+    r.cnt = 0;
+    return r;
+}
+// a then b (a older)
+__device__ __forceinline__ SegF segf_combine(const SegF& a, const SegF& b) {
+    SegF r;
+    r.f = a.f | b.f;
+    r.g = b.f ? b.g : gmg_ss::seg_merge(a.g, b.g);
+    r.cnt = a.cnt + b.cnt;
+    return r;
+}
+__device__ __forceinline__ SegF segf_shfl(const SegF& x, int src, bool up, int o) {
+    SegF r;
+    const uint32_t meta = static_cast<uint32_t>(x.g.E) | (static_cast<uint32_t>(x.g.neg) << 11) |
+                          (static_cast<uint32_t>(x.g.bad) << 12) | (static_cast<uint32_t>(x.f) << 13);
+    uint32_t m2;
+    if (up) {
+        m2 = __shfl_up_sync(0xffffffffu, meta, o);
+        r.g.len = __shfl_up_sync(0xffffffffu, x.g.len, o);
+        r.cnt = __shfl_up_sync(0xffffffffu, x.cnt, o);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            r.g.Q[p] = __shfl_up_sync(0xffffffffu, x.g.Q[p], o);
+            r.g.mn[p] = __shfl_up_sync(0xffffffffu, x.g.mn[p], o);
+            r.g.mx[p] = __shfl_up_sync(0xffffffffu, x.g.mx[p], o);
+        }
+    } else {
+        m2 = __shfl_sync(0xffffffffu, meta, src);
+        r.g.len = __shfl_sync(0xffffffffu, x.g.len, src);
+        r.cnt = __shfl_sync(0xffffffffu, x.cnt, src);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            r.g.Q[p] = __shfl_sync(0xffffffffu, x.g.Q[p], src);
+            r.g.mn[p] = __shfl_sync(0xffffffffu, x.g.mn[p], src);
+            r.g.mx[p] = __shfl_sync(0xffffffffu, x.g.mx[p], src);
+        }
+    }
+    r.g.E = m2 & 0x7ff;
+    r.g.neg = (m2 >> 11) & 1;
+    r.g.bad = (m2 >> 12) & 1;
+    r.f = (m2 >> 13) & 1;
+    return r;
+}
+
+// ChunkAgg: SegF as published between chunks (plain struct, read with __ldcg)
+struct ChunkAgg {
+    long long Q[2], mn[2], mx[2];
+    int meta;  // E | neg<<11 | bad<<12 | f<<13
+    int len;
+    int cnt;
+    int pad;
+};
+__device__ __forceinline__ void agg_store(unsigned char* base, int c, const SegF& v) {
+    ChunkAgg a;
+    for (int p = 0; p < 2; ++p) {
+        a.Q[p] = v.g.Q[p];
+        a.mn[p] = v.g.mn[p];
+        a.mx[p] = v.g.mx[p];
+    }
+    a.meta = v.g.E | (v.g.neg << 11) | (v.g.bad << 12) | (v.f << 13);
+    a.len = v.g.len;
+    a.cnt = v.cnt;
+    a.pad = 0;
+    reinterpret_cast<ChunkAgg*>(base)[c] = a;
+}
+__device__ __forceinline__ SegF agg_load(const unsigned char* base, int c) {
+    const ChunkAgg* p = reinterpret_cast<const ChunkAgg*>(base) + c;
+    SegF v;
+    for (int q = 0; q < 2; ++q) {
+        v.g.Q[q] = __ldcg(&p->Q[q]);
+        v.g.mn[q] = __ldcg(&p->mn[q]);
+        v.g.mx[q] = __ldcg(&p->mx[q]);
+    }
+    const int meta = __ldcg(&p->meta);
+    v.g.E = meta & 0x7ff;
+    v.g.neg = (meta >> 11) & 1;
+    v.g.bad = (meta >> 12) & 1;
+    v.f = (meta >> 13) & 1;
+    v.g.len = __ldcg(&p->len);
+    v.cnt = __ldcg(&p->cnt);
+    return v;
+}
+
+// Decoupled look-back (one warp) for chunk c: approximate double prefix.
+__device__ double lookback_d(int c, const int* flag, const double* agg, const double* incl) {
     const int lane = threadIdx.x & 31;
-    T acc = T(0);
+    double acc = 0.0;
     int p = c - 1;
     while (p >= 0) {
         const int idx = p - lane;
@@ -75,8 +169,8 @@ __device__ T lookback(int c, const int* flag, const T* agg, const T* incl) {
         }
         __threadfence();
         const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
-        const int stop = m2 ? __ffs(m2) - 1 : 32;  // nearest predecessor with an inclusive prefix
-        T v = T(0);
+        const int stop = m2 ? __ffs(m2) - 1 : 32;
+        double v = 0.0;
         if (idx >= 0) {
             if (lane < stop) v = __ldcg(agg + idx);
             else if (lane == stop) v = __ldcg(incl + idx);
@@ -84,6 +178,43 @@ __device__ T lookback(int c, const int* flag, const T* agg, const T* incl) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         acc += v;
+        if (stop < 32) break;
+        p -= 32;
+    }
+    return acc;
+}
+
+// Decoupled look-back (one warp) for chunk c: exclusive ordered segmented
+// combine of the chunk aggregates (lane l holds predecessor p - l; older
+// chunks combine on the left).
+__device__ SegF lookback_seg(int c, const int* flag, const unsigned char* agg, const unsigned char* incl) {
+    const int lane = threadIdx.x & 31;
+    SegF acc = segf_id();
+    int p = c - 1;
+    while (p >= 0) {
+        const int idx = p - lane;
+        int f = 2;
+        if (idx >= 0) {
+            do {
+                f = ld_flag(flag + idx);
+            } while (f == 0);
+        }
+        __threadfence();
+        const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
+        const int stop = m2 ? __ffs(m2) - 1 : 32;
+        SegF v = segf_id();
+        if (idx >= 0) {
+            if (lane < stop) v = agg_load(agg, idx);
+            else if (lane == stop) v = agg_load(incl, idx);
+        }
+        // ordered reduction: result in lane 0 = v_31 o ... o v_0
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const SegF y = segf_shfl(v, (lane + o) & 31, false, 0);
+            if ((lane & (2 * o - 1)) == 0) v = segf_combine(y, v);
+        }
+        v = segf_shfl(v, 0, false, 0);
+        acc = segf_combine(v, acc);
         if (stop < 32) break;
         p -= 32;
     }
@@ -118,73 +249,19 @@ __device__ __forceinline__ double block_excl_sum_d(double x, double* sw /* [8] *
     return base + inc - x;
 }
 
-__device__ __forceinline__ int block_excl_sum_i(int x, int* sw /* [8] */, int* total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int inc = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) sw[w] = inc;
-    __syncthreads();
-    int base = 0, tot = 0;
-    for (int q = 0; q < 8; ++q) {
-        if (q < w) base += sw[q];
-        tot += sw[q];
-    }
-    __syncthreads();
-    *total = tot;
-    return base + inc - x;
-}
-
-// segmented scan element: f = "a break closed the run inside this thread"
-struct SegF {
-    gmg_ss::Seg g;
-    int f;
-};
-__device__ __forceinline__ SegF segf_combine(const SegF& a, const SegF& b) {
-    SegF r;
-    r.f = a.f | b.f;
-    r.g = b.f ? b.g : gmg_ss::seg_merge(a.g, b.g);
-    return r;
-}
-__device__ __forceinline__ SegF segf_shfl_up(const SegF& x, int o) {
-    SegF r;
-    const uint32_t meta = static_cast<uint32_t>(x.g.E) | (static_cast<uint32_t>(x.g.neg) << 11) |
-                          (static_cast<uint32_t>(x.g.bad) << 12) | (static_cast<uint32_t>(x.f) << 13) |
-                          (static_cast<uint32_t>(x.g.len) << 14);
-    const uint32_t m2 = __shfl_up_sync(0xffffffffu, meta, o);
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        r.g.Q[p] = __shfl_up_sync(0xffffffffu, x.g.Q[p], o);
-        r.g.mn[p] = __shfl_up_sync(0xffffffffu, x.g.mn[p], o);
-        r.g.mx[p] = __shfl_up_sync(0xffffffffu, x.g.mx[p], o);
-    }
-    r.g.E = m2 & 0x7ff;
-    r.g.neg = (m2 >> 11) & 1;
-    r.g.bad = (m2 >> 12) & 1;
-    r.f = (m2 >> 13) & 1;
-    r.g.len = static_cast<int>(m2 >> 14);
-    return r;
-}
-
-// Block exclusive segmented scan; also returns the block inclusive total.
+// Block exclusive segmented scan (256 threads); returns the block inclusive total too.
 __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [8] */, SegF* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     SegF inc = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const SegF y = segf_shfl_up(inc, o);
+        const SegF y = segf_shfl(inc, 0, true, o);
         if (lane >= o) inc = segf_combine(y, inc);
     }
-    const SegF ex = segf_shfl_up(inc, 1);
+    const SegF ex = segf_shfl(inc, 0, true, 1);
     if (lane == 31) sw[w] = inc;
     __syncthreads();
-    SegF base;
-    base.g = gmg_ss::seg_empty();
-    base.f = 0;
-    SegF tot = base;
+    SegF base = segf_id(), tot = segf_id();
     for (int q = 0; q < 8; ++q) {
         if (q < w) base = segf_combine(base, sw[q]);
         tot = segf_combine(tot, sw[q]);
@@ -203,11 +280,10 @@ template <class TG>
 __global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
     extern __shared__ double tm[];
     __shared__ double swd[8];
-    __shared__ int swi[8];
     __shared__ SegF sws[8];
     __shared__ int s_chunk;
     __shared__ double s_pre;
-    __shared__ int s_off;
+    __shared__ SegF s_carry;
 
     const int s = blockIdx.y;
     const SsState& S = sts.s[s];
@@ -242,7 +318,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, int nch, S
         }
     }
     if (t < 32) {
-        const double pre = c == 0 ? 0.0 : lookback<double>(c, S.flag, S.agg, S.incl);
+        const double pre = c == 0 ? 0.0 : lookback_d(c, S.flag, S.agg, S.incl);
         if (t == 0) {
             s_pre = pre;
             if (c > 0) {
@@ -258,14 +334,10 @@ __global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, int nch, S
     gmg_ss::State st = gmg_ss::make_state(pred);
     gmg_ss::Seg cur = gmg_ss::seg_empty(), lead = gmg_ss::seg_empty();
     int r = 0;
-    double pb0 = 0.0;
     for (int m = 0; m < ne; ++m) {
         const double p = tm[ss_pad(e0 + m)];
         if (!gmg_ss::walk_try(st, cur, p)) {
-            if (r == 0) {
-                lead = cur;
-                pb0 = p;
-            }
+            if (r == 0) lead = cur;
             ++r;
             cur = gmg_ss::seg_empty();
             gmg_ss::real_add(st, p);
@@ -273,175 +345,164 @@ __global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, int nch, S
     }
     if (r == 0) lead = cur;
 
-    // (4) merge runs across threads
-    SegF x;
+    // (4) merge runs across threads; records = breaks (+ the final record)
+    SegF x = segf_id();
     x.f = r > 0;
     x.g = r > 0 ? cur : lead;
+    x.cnt = r;
     SegF tot;
     const SegF carry = block_excl_segscan(x, sws, &tot);
-    int R;
-    const int pos = block_excl_sum_i(r, swi, &R);
-    R += 1;
+    const bool last = c == nch - 1;
+    const int R = tot.cnt + (last ? 1 : 0);
+    const bool literal = R > kSsRMax;
 
-    // (5) record offset by look-back over stored counts (aggregate published
-    //     before looking back, so chunks never wait on a predecessor's look-back)
-    const int stored = R <= kSsRMax ? R : 1;
+    // (5) run carry + record offset by look-back over chunks (aggregate
+    //     published first, so no chunk waits on a predecessor's look-back)
+    SegF mine = tot;
+    mine.cnt = literal ? 1 : R;
+    if (literal) {
+        mine.f = 1;
+        mine.g = gmg_ss::seg_empty();
+    }
     if (t == 0) {
         if (c == 0) {
-            S.cincl[0] = stored;
+            agg_store(S.cincl, 0, mine);
             st_flag(S.cflag, 2);
         } else {
-            S.cagg[c] = stored;
+            agg_store(S.cagg, c, mine);
             st_flag(S.cflag + c, 1);
         }
     }
     if (t < 32) {
-        const int o = c == 0 ? 0 : lookback<int>(c, S.cflag, S.cagg, S.cincl);
+        const SegF ex = c == 0 ? segf_id() : lookback_seg(c, S.cflag, S.cagg, S.cincl);
         if (t == 0) {
             if (c > 0) {
-                S.cincl[c] = o + stored;
+                agg_store(S.cincl, c, segf_combine(ex, mine));
                 st_flag(S.cflag + c, 2);
             }
-            if (c == nch - 1) *S.total = o + stored;
-            s_off = o;
+            if (last) *S.total = ex.cnt + mine.cnt;
+            s_carry = ex;
         }
     }
     __syncthreads();
-    const int off = s_off;
-    if (stored != R) {  // too many breaks: the chain sums this chunk literally
-        if (t == 0) S.recs[off] = gmg_ss::rec_literal(c);
+    const SegF cin = s_carry;  // run since the last break before this chunk; cnt = offset
+    gmg_ss::Rec* out = S.recs + cin.cnt;
+    if (literal) {
+        if (t == 0) out[0] = gmg_ss::rec_literal((uint32_t)(base + clen - 1));
         return;
     }
-    gmg_ss::Rec* out = S.recs + off;
     if (r > 0) {
-        // pass 2: emit records; the first one absorbs the run carried in
-        out[pos] = gmg_ss::rec_make(gmg_ss::seg_merge(carry.g, lead), true, pb0, c);
+        // pass 2: emit this thread's records; the first absorbs the run carried in
+        const int pos = carry.cnt;
+        gmg_ss::Seg first = carry.g;
+        if (!carry.f) first = gmg_ss::seg_merge(cin.g, first);
         st = gmg_ss::make_state(pred);
         cur = gmg_ss::seg_empty();
         int k = 0;
         for (int m = 0; m < ne; ++m) {
             const double p = tm[ss_pad(e0 + m)];
             if (!gmg_ss::walk_try(st, cur, p)) {
-                if (k > 0) out[pos + k] = gmg_ss::rec_make(cur, true, p, c);
+                const gmg_ss::Seg g = k == 0 ? gmg_ss::seg_merge(first, cur) : cur;
+                out[pos + k] = gmg_ss::rec_make(g, true, p, (uint32_t)(base + e0 + m));
                 ++k;
                 cur = gmg_ss::seg_empty();
                 gmg_ss::real_add(st, p);
             }
         }
     }
-    if (t == kSsT - 1) out[R - 1] = gmg_ss::rec_make(tot.g, false, 0.0, c);
+    if (last && t == kSsT - 1) {
+        const gmg_ss::Seg g = tot.f ? tot.g : gmg_ss::seg_merge(cin.g, tot.g);
+        out[R - 1] = gmg_ss::rec_make(g, false, 0.0, (uint32_t)n);
+    }
 }
 
 // ---- chain --------------------------------------------------------------------
-__device__ __forceinline__ gmg_ss::Seg seg_shfl(const gmg_ss::Seg& x, int src) {
-    gmg_ss::Seg r;
-    const uint32_t meta = static_cast<uint32_t>(x.E) | (static_cast<uint32_t>(x.neg) << 11) |
-                          (static_cast<uint32_t>(x.bad) << 12) | (static_cast<uint32_t>(x.len) << 13);
-    const uint32_t m2 = __shfl_sync(0xffffffffu, meta, src);
-#pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        r.Q[p] = __shfl_sync(0xffffffffu, x.Q[p], src);
-        r.mn[p] = __shfl_sync(0xffffffffu, x.mn[p], src);
-        r.mx[p] = __shfl_sync(0xffffffffu, x.mx[p], src);
-    }
-    r.E = m2 & 0x7ff;
-    r.neg = (m2 >> 11) & 1;
-    r.bad = (m2 >> 12) & 1;
-    r.len = static_cast<int>(m2 >> 13);
-    return r;
-}
-
-// Literal left-to-right adds over terms [k0, k1) of sum s.
+// Literal left-to-right adds over terms [k0, k1) of sum s, by one warp: lanes
+// load 32 consecutive terms (next batch prefetched), lane 0's order of adds.
 template <class TG>
 __device__ double literal_sum(const TG& tg, int s, double a, long long k0, long long k1) {
-    for (long long k = k0; k < k1; ++k) a = a + tg.term(s, k);
-    return a;
+    const int lane = threadIdx.x & 31;
+    double nxt = (k0 + lane < k1) ? tg.term(s, k0 + lane) : 0.0;
+    long long k = k0;
+    for (; k + 32 <= k1; k += 32) {
+        const double cur = nxt;
+        nxt = (k + 32 + lane < k1) ? tg.term(s, k + 32 + lane) : 0.0;
+        double v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __shfl_sync(0xffffffffu, cur, j);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a = a + v[j];
+    }
+    const int m = (int)(k1 - k);
+    for (int j = 0; j < m; ++j) a = a + __shfl_sync(0xffffffffu, nxt, j);
+    return __shfl_sync(0xffffffffu, a, 0);
 }
 
-// grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays the
-// records: in each window of 32 it merges the pure segments up to the first
-// break record with a parity-aware merge-scan, validates the merged run once
-// against the exact state and applies it, then performs that record's break
-// add. Warps 1.. stream the next batch into shared memory meanwhile.
+// grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays,
+// warps 1.. stage the next batch.
 template <class TG>
 __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out) {
     extern __shared__ unsigned char smraw[];
     gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
     const int s = blockIdx.x;
     const SsState& S = sts.s[s];
-    const int t = threadIdx.x, lane = t & 31;
+    const int t = threadIdx.x;
     const int total = *S.total;
     const int nb = (total + kSsBatch - 1) / kSsBatch;
 
     for (int q = t; q < min(total, kSsBatch); q += kSsT) buf[q] = S.recs[q];
     __syncthreads();
 
-    gmg_ss::State st = gmg_ss::make_state(0.0);  // identical in every lane of warp 0
-    long long cur_chunk = -1, skip = -1;
-    int pos = 0;
+    // Exact running sum kept as a double. While a record's run validates, the
+    // sum stays inside one binade whose spacing is u = 2^(E-1075), so
+    // s + Q*u is exact (Q*u: power-of-two scaling; the result is representable)
+    // and the integer state is M = s * 2^(1075-E), also exact.
+    double sv = 0.0;
+    long long prev = -1;  // global index of the last element consumed
+    unsigned long long n_brk = 0, n_lit = 0, n_litterms = 0, cyc_lit = 0;
+    const long long cyc0 = clock64();
     for (int b = 0; b < nb; ++b) {
         const gmg_ss::Rec* A = buf + (b & 1) * kSsBatch;
         const int cnt = min(kSsBatch, total - b * kSsBatch);
         if (t < 32) {
-            int q = 0;
-            while (q < cnt) {
-                const int idx = q + lane;
-                const bool have = idx < cnt;
-                gmg_ss::Rec rec{};
-                if (have) rec = A[idx];
-                const long long c = have ? (long long)rec.chunk : -2;
-                const bool lit = have && gmg_ss::rec_literal_flag(rec);
-                const bool skipme = have && c == skip;
-                const bool brk = have && !lit && !skipme && gmg_ss::rec_has_break(rec);
-                const unsigned stopm = __ballot_sync(0xffffffffu, !have || brk || lit || skipme);
-                const int f = stopm ? __ffs(stopm) - 1 : 32;  // lanes < f: pure segments
-                // Runs of >= 3 pure segments are merged with a warp merge-scan; break
-                // records (and short runs) take the cheap serial path below.
-                if (f >= 3) {
-                    const int run_end = f - 1;
-                    gmg_ss::Seg g = (lane <= run_end) ? gmg_ss::rec_seg(rec) : gmg_ss::seg_empty();
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const gmg_ss::Seg y = seg_shfl(g, lane >= o ? lane - o : lane);
-                        if (lane >= o) g = gmg_ss::seg_merge(y, g);
-                    }
-                    const gmg_ss::Seg run = seg_shfl(g, run_end);
-                    if (gmg_ss::seg_valid(run, st)) {
-                        const long long c_end = __shfl_sync(0xffffffffu, c, run_end);
-                        int my = (lane <= run_end && c == c_end) ? (int)(rec.meta >> 15) : 0;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
-                        pos = (c_end == cur_chunk ? pos : 0) + my;
-                        cur_chunk = c_end;
-                        gmg_ss::seg_apply(run, st);
-                        q += run_end + 1;
-                        continue;
-                    }
+#pragma unroll 2
+            for (int q = 0; q < cnt; ++q) {
+                const gmg_ss::Rec& r = A[q];
+                const uint32_t meta = r.meta;
+                const long long kb = r.kb;
+                const bool brk = (meta >> 12) & 1u, lit = (meta >> 14) & 1u, ne = (meta >> 15) & 1u;
+                const uint64_t Er = meta & 0x7ffu;
+                const bool negr = (meta >> 11) & 1u, badr = (meta >> 13) & 1u;
+                const bool ties = r.Q[0] != r.Q[1] || r.mn[0] != r.mn[1] || r.mx[0] != r.mx[1];
+                const double pb = r.pb;
+                // critical path: the bits of the exact sum give E, the integer
+                // significand and its parity directly
+                const uint64_t bits = gmg_ss::dbits(sv);
+                const uint64_t E = (bits >> 52) & 0x7ffu;
+                const int v = (ties && (bits & 1u)) ? 1 : 0;
+                const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
+                const long long Qi = r.Q[v], mni = r.mn[v], mxi = r.mx[v];
+                const bool neg = bits >> 63;
+                // |M| = mant; for a negative sum M + x ranges over -(mant - x)
+                const long long lo_v = neg ? mant - mxi : mant + mni;
+                const long long hi_v = neg ? mant - mni : mant + mxi;
+                const bool ok_run = E >= (uint64_t)gmg_ss::kEMin && E <= (uint64_t)gmg_ss::kEMax && E == Er &&
+                                    neg == negr && lo_v >= gmg_ss::kLo && hi_v <= gmg_ss::kHi;
+                const bool ok = !lit && !badr && (!ne || ok_run);
+                const double u = gmg_ss::bitsd((E - 52) << 52);
+                double s1 = ne ? sv + (double)Qi * u : sv;
+                if (!ok) {
+                    // re-sum this record's range literally (through kb for literal chunks)
+                    const long long k1 = min(lit ? kb + 1 : kb, n);
+                    const long long c0 = clock64();
+                    s1 = literal_sum(tg, s, sv, prev + 1, k1);
+                    cyc_lit += clock64() - c0;
+                    ++n_lit;
+                    n_litterms += k1 - (prev + 1);
                 }
-                // serial handling of the window's first record
-                const gmg_ss::Rec r0 = A[q];
-                const long long c0 = r0.chunk;
-                ++q;
-                if (c0 == skip) continue;
-                if (c0 != cur_chunk) {
-                    cur_chunk = c0;
-                    pos = 0;
-                }
-                const gmg_ss::Seg g0 = gmg_ss::rec_seg(r0);
-                if (gmg_ss::rec_literal_flag(r0) || !gmg_ss::seg_valid(g0, st)) {
-                    double a = 0.0;
-                    if (lane == 0) a = literal_sum(tg, s, st.s, c0 * kSsC + pos, min(n, (c0 + 1) * kSsC));
-                    a = __shfl_sync(0xffffffffu, a, 0);
-                    st = gmg_ss::make_state(a);
-                    skip = c0;
-                    continue;
-                }
-                gmg_ss::seg_apply(g0, st);
-                pos += g0.len;
-                if (gmg_ss::rec_has_break(r0)) {
-                    gmg_ss::real_add(st, r0.pb);
-                    pos += 1;
-                }
+                sv = brk ? s1 + pb : s1;
+                n_brk += brk;
+                prev = (lit || brk) ? kb : n - 1;
             }
         } else if (b + 1 < nb) {
             gmg_ss::Rec* B = buf + ((b + 1) & 1) * kSsBatch;
@@ -451,7 +512,19 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
         }
         __syncthreads();
     }
-    if (t == 0) out[s] = st.s;
+    if (t == 0) {
+        out[s] = sv;
+        if (S.stats) {
+            atomicAdd(S.stats + 0, 1ull);
+            atomicAdd(S.stats + 1, (unsigned long long)total);
+            atomicAdd(S.stats + 2, (unsigned long long)(clock64() - cyc0));
+            atomicAdd(S.stats + 3, cyc_lit);
+            atomicAdd(S.stats + 4, n_brk);
+            atomicAdd(S.stats + 5, n_lit);
+            atomicAdd(S.stats + 6, n_litterms);
+            atomicAdd(S.stats + 7, (unsigned long long)((n + kSsC - 1) / kSsC));
+        }
+    }
 }
 
 // Fast mode: tree-order partial sums per chunk, then one CTA finishes.

@@ -206,19 +206,21 @@ SS_HD void real_add(State& st, double p) {
     st = make_state(s);
 }
 
-// Record as stored for the chain: a segment, then optionally one break element
-// (applied with a real add). 64 bytes.
-//   meta: E (11b) | neg<<11 | has_break<<12 | bad<<13 | literal<<14 | len<<15 (16b)
-// `literal` marks a chunk whose records did not fit: the chain re-sums it
-// with literal adds.
+// Record as stored for the chain: the merged run of elements since the previous
+// record's break element, then optionally one break element at global index kb
+// (applied with a real add). The run's elements are exactly (prev.kb, kb), so a
+// record that fails validation is re-summed literally over that range. 64 bytes.
+//   meta: E (11b) | neg<<11 | has_break<<12 | bad<<13 | literal<<14 | nonempty<<15
+// `literal` marks a chunk with too many breaks to store: the chain re-sums
+// (prev.kb, kb] literally (kb = the chunk's last element).
 struct Rec {
     int64_t Q[2], mn[2], mx[2];
     double pb;
     uint32_t meta;
-    uint32_t chunk;
+    uint32_t kb;
 };
 
-SS_HD Rec rec_make(const Seg& g, bool has_break, double pb, uint32_t chunk) {
+SS_HD Rec rec_make(const Seg& g, bool has_break, double pb, uint32_t kb) {
     Rec r;
     for (int p = 0; p < 2; ++p) {
         r.Q[p] = g.Q[p];
@@ -228,12 +230,12 @@ SS_HD Rec rec_make(const Seg& g, bool has_break, double pb, uint32_t chunk) {
     r.pb = pb;
     r.meta = static_cast<uint32_t>(g.E & 0x7ff) | (static_cast<uint32_t>(g.neg) << 11) |
              (static_cast<uint32_t>(has_break) << 12) | (static_cast<uint32_t>(g.bad) << 13) |
-             (static_cast<uint32_t>(g.len) << 15);
-    r.chunk = chunk;
+             (static_cast<uint32_t>(g.len > 0) << 15);
+    r.kb = kb;
     return r;
 }
-SS_HD Rec rec_literal(uint32_t chunk) {
-    Rec r = rec_make(seg_empty(), false, 0.0, chunk);
+SS_HD Rec rec_literal(uint32_t kb) {
+    Rec r = rec_make(seg_empty(), false, 0.0, kb);
     r.meta |= 1u << 14;
     return r;
 }
@@ -242,7 +244,7 @@ SS_HD Seg rec_seg(const Rec& r) {
     g.E = static_cast<int>(r.meta & 0x7ff);
     g.neg = static_cast<int>((r.meta >> 11) & 1);
     g.bad = static_cast<int>((r.meta >> 13) & 1);
-    g.len = static_cast<int>(r.meta >> 15);
+    g.len = static_cast<int>((r.meta >> 15) & 1);  // emptiness only
     for (int p = 0; p < 2; ++p) {
         g.Q[p] = r.Q[p];
         g.mn[p] = r.mn[p];

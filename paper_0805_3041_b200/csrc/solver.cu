@@ -110,10 +110,11 @@ struct gmg_problem {
     double* csum = nullptr;          // fast-mode partials [2][nch]
     double* T = nullptr;             // materialised omega terms, 2 x N_L dense
     double* lb = nullptr;            // look-back values: per sum agg, incl [nch] each
-    int* lbi = nullptr;              // per sum: cagg, cincl [nch] each
+    unsigned char* lbs = nullptr;    // per sum: cagg, cincl [nch] ChunkAgg each
     int* flags = nullptr;            // per sum: ticket, total, flag[nch], cflag[nch]
     gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records
     int rec_cap = 0;
+    unsigned long long* ss_stats = nullptr;  // [8] exact-sum engine counters (seqsum.cuh)
     double* sums = nullptr;  // [0..1] omega sums, [2] residual norm^2, [3] misc
     int* nz = nullptr;
     int* status = nullptr;
@@ -254,10 +255,10 @@ SsPair ss_state(gmg_problem* p, int nch) {
         S.cflag = f + 2 + nch;
         S.agg = p->lb + (size_t)s * 2 * p->nch_max;
         S.incl = S.agg + p->nch_max;
-        S.cagg = p->lbi + (size_t)s * 2 * p->nch_max;
-        S.cincl = S.cagg + p->nch_max;
+        S.cagg = p->lbs + (size_t)s * 2 * p->nch_max * sizeof(ChunkAgg);
+        S.cincl = S.cagg + (size_t)p->nch_max * sizeof(ChunkAgg);
         S.recs = p->recs + (size_t)s * p->rec_cap;
-        S.cap = p->rec_cap;
+        S.stats = p->ss_stats;
     }
     return sp;
 }
@@ -274,6 +275,10 @@ void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int mode) {
         set_smem(k_ss_walk<TG>, ss_walk_smem());
         set_smem(k_ss_chain<TG>, ss_chain_smem());
         attr_done = true;
+    }
+    if (n == 0) {  // the reference's loop leaves s = 0.0
+        CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
+        return;
     }
     if (mode == GMG_REDUCE_FAST) {
         k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
@@ -690,9 +695,10 @@ void free_problem(gmg_problem* p) {
     cudaFree(p->csum);
     cudaFree(p->T);
     cudaFree(p->lb);
-    cudaFree(p->lbi);
+    cudaFree(p->lbs);
     cudaFree(p->flags);
     cudaFree(p->recs);
+    cudaFree(p->ss_stats);
     cudaFree(p->sums);
     cudaFree(p->nz);
     cudaFree(p->status);
@@ -839,11 +845,13 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         CK(cudaMalloc(&p->csum, 2 * nm * sizeof(double)));
         CK(cudaMalloc(&p->T, 2 * (size_t)n * sizeof(double)));
         CK(cudaMalloc(&p->lb, 2 * 2 * nm * sizeof(double)));
-        CK(cudaMalloc(&p->lbi, 2 * 2 * nm * sizeof(int)));
+        CK(cudaMalloc(&p->lbs, 2 * 2 * nm * sizeof(ChunkAgg)));
         CK(cudaMalloc(&p->flags, 2 * (2 + 2 * nm) * sizeof(int)));
         // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
         p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
         CK(cudaMalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
+        CK(cudaMalloc(&p->ss_stats, 8 * sizeof(unsigned long long)));
+        CK(cudaMemset(p->ss_stats, 0, 8 * sizeof(unsigned long long)));
         CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
         CK(cudaMalloc(&p->nz, sizeof(int)));
@@ -873,7 +881,7 @@ extern "C" {
 
 const char* gmg_last_error(void) { return g_last_error.c_str(); }
 
-const char* gmg_version(void) { return "gmg_b200 sm_100a; exact-order seqsum v2 (chunk 8192, look-back, tie-parity segments)"; }
+const char* gmg_version(void) { return "gmg_b200 sm_100a; exact-order seqsum v3 (chunk 8192, look-back run carry, tie-parity segments)"; }
 
 int gmg_dev_problem_create(const gmg_problem_desc* desc, gmg_problem** out) {
     return guarded([&] { create_problem(desc, out); });
@@ -1195,6 +1203,16 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
         CK(cudaEventElapsedTime(&t, p->ev0, p->ev1));
         *ms = (double)t / reps;
         *bytes = per_dof * (double)F.n();
+    });
+}
+
+int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out8) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        CK(cudaStreamSynchronize(p->st));
+        CK(cudaMemcpy(out8, p->ss_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        if (reset) CK(cudaMemset(p->ss_stats, 0, 8 * sizeof(unsigned long long)));
     });
 }
 

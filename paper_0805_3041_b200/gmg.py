@@ -50,7 +50,7 @@ EXPORTS = [
     "gmg_dev_solve_devptr", "gmg_dev_mg_cycle", "gmg_dev_apply", "gmg_dev_residual",
     "gmg_dev_smooth_step", "gmg_dev_restriction", "gmg_dev_prolongation", "gmg_dev_adaptive_omega",
     "gmg_dev_coarse_solve", "gmg_dev_norm_l2", "gmg_dev_dot", "gmg_dev_axpy",
-    "gmg_dev_time_smoother", "gmg_dev_cycle_kernel_count", "gmg_host_problem_create",
+    "gmg_dev_time_smoother", "gmg_dev_cycle_kernel_count", "gmg_dev_seqsum_stats", "gmg_host_problem_create",
     "gmg_host_random_vector", "gmg_host_seqsum_emulate",
 ]
 
@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
         L.gmg_dev_dot.argtypes = [C.c_void_p, C.c_longlong, _dp, _dp, C.c_int, _dp]
         L.gmg_dev_axpy.argtypes = [C.c_void_p, C.c_longlong, C.c_double, _dp, _dp]
         L.gmg_dev_time_smoother.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, C.c_int, _dp, _dp]
+        L.gmg_dev_seqsum_stats.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_ulonglong)]
         L.gmg_dev_cycle_kernel_count.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.POINTER(C.c_int)]
         L.gmg_host_problem_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                               C.c_int, C.c_double, C.c_double, C.c_int,
@@ -423,3 +424,12 @@ def cycle_kernel_count(prob: MultilevelProblem, spec: CycleSpec) -> int:
     n = C.c_int()
     _check(lib().gmg_dev_cycle_kernel_count(prob._h, C.byref(spec._c()), C.byref(n)))
     return n.value
+
+
+def seqsum_stats(prob: MultilevelProblem, reset: bool = True) -> dict:
+    """Exact-order summation engine counters since the last reset."""
+    a = (C.c_ulonglong * 8)()
+    _check(lib().gmg_dev_seqsum_stats(prob._h, int(reset), a))
+    keys = ["sums", "records", "chain_cycles", "literal_cycles", "break_adds", "literal_ranges",
+            "literal_terms", "chunks"]
+    return dict(zip(keys, list(a)))

@@ -20,6 +20,8 @@ for red in ["exact", "fast"]:
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         print(f"L={L} {red:5s} cycles={cyc}: {1e3*dt:8.2f} ms total, wall in report {1e3*r.wall_seconds:8.2f}")
+        if red == "exact":
+            print("   engine stats (warm+timed calls):", gmg.seqsum_stats(p))
 for variant in (0, 1, 2):
     ms, by = gmg.time_smoother(p, gmg.CycleSpec(smoother="jacobi"), variant=variant, reps=10)
     print(f"smoother variant {variant}: {ms:.3f} ms, {by/ms/1e6:.0f} GB/s")
