@@ -254,13 +254,15 @@ __global__ void __launch_bounds__(TW) k_smooth(Grid fg, Coef A, Src src, OmegaSr
 }
 
 // ---------------- residual (+ restriction) ---------------------------------
-// d = g - A x0 (stencil.cpp:148-153), optionally stored; x0 optionally stored;
+// d = g - A x0 (stencil.cpp:148-153), or with neg the smoother defect
+// A x0 - g (smoother.cpp:393-394), optionally stored; x0 optionally stored;
 // optionally g_c = R d (transfer.cpp:72-101) for the next coarser level.
 // Strip stride TW-4, halo 2 columns; segments of `seg` rows (seg even).
 template <int TW, int PF, class Coef, class Src>
 __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const double* __restrict__ g,
                                               double* __restrict__ dout, double* __restrict__ x0out,
-                                              Grid cg, RestrictW rw, double* __restrict__ gc, int seg) {
+                                              Grid cg, RestrictW rw, double* __restrict__ gc, int seg,
+                                              int neg, OmegaSrc om) {
     const bool STORE_D = dout != nullptr, STORE_X0 = x0out != nullptr, RESTRICT = gc != nullptr;
     constexpr int OUTW = TW - 4;
     __shared__ double xs[2][TW];
@@ -273,6 +275,9 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
     const bool col_in = i >= 0 && i < fg.nx;
     const bool owner = col_in && t >= 2 && t < TW - 2;
     src.prepare(i);
+    if constexpr (std::is_same<Src, SrcCorrect>::value) {
+        src.omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && t == 0);
+    }
 
     double a = 0.0, b = 0.0, c = 0.0;  // x0 rows J-2, J-1, J in own column
     const int Jbeg = j0 - 1;
@@ -308,7 +313,10 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
             const double xr = t < TW - 1 ? xs[(J - 1) & 1][t + 1] : 0.0;
             xs[J & 1][t] = x0;
             double d = 0.0;
-            if (col_in && R >= 0 && R < fg.ny) d = gR - stencil_apply(A, i, R, b, xl, xr, a, c);
+            if (col_in && R >= 0 && R < fg.ny) {
+                const double ax = stencil_apply(A, i, R, b, xl, xr, a, c);
+                d = neg ? ax - gR : gR - ax;  // smoother defect (Ax - g) or residual (g - Ax)
+            }
             if (STORE_D && owner && R >= j0 && R < j1) dout[fg.at(i, R)] = d;
             if (RESTRICT) dr[R & 3][t] = d;
             __syncthreads();

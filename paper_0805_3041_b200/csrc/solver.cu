@@ -27,6 +27,7 @@
 #include "../../include/gmg_b200.h"
 #include "common.cuh"
 #include "host_setup.h"
+#include "gs.cuh"
 #include "march.cuh"
 #include "seqsum.cuh"
 
@@ -115,6 +116,9 @@ struct gmg_problem {
     gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records
     int rec_cap = 0;
     unsigned long long* ss_stats = nullptr;  // [8] exact-sum engine counters (seqsum.cuh)
+    double* gs_edge = nullptr;               // Gauss-Seidel wavefront warp-edge rows
+    int* gs_prog = nullptr;                  // and their progress counters
+    int gs_warps = 0;
     double* sums = nullptr;  // [0..1] omega sums, [2] residual norm^2, [3] misc
     int* nz = nullptr;
     int* status = nullptr;
@@ -383,7 +387,8 @@ double* smooth_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const
 
 template <class Coef, class Src>
 void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, const double* g,
-                    double* dout, double* x0out, double* gc) {
+                    double* dout, double* x0out, double* gc, int neg = 0,
+                    OmegaSrc om = OmegaSrc{nullptr, nullptr, 1.0, nullptr}) {
     const int seg = seg_rows(L.nx, L.ny);
     dim3 grid((L.nx + (kTW - 4) - 1) / (kTW - 4), (L.ny + seg - 1) / seg);
     Grid cg{0, 0, 0};
@@ -394,7 +399,8 @@ void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src,
         rw = C.rw;
     }
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
-    k_resid<kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg);
+    k_resid<kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg, neg,
+                                                          om);
     CK(cudaGetLastError());
 }
 
@@ -407,6 +413,78 @@ void launch_resid(gmg_problem* p, const Lev& L, const double* u, const double* e
         else
             launch_resid_t(p, L, A, SrcU{u, L.grid()}, g, dout, x0out, gc);
     });
+}
+
+// Defect A x0 - g of a smoothing start (any source), optionally storing x0.
+void launch_defect_src(gmg_problem* p, const Lev& L, const SmoothSrc& s, const double* g, double* dout,
+                       double* x0out) {
+    with_coef(L, [&](const auto& A) {
+        switch (s.kind) {
+            case S_ZERO:
+                launch_resid_t(p, L, A, SrcZero{}, g, dout, x0out, nullptr, 1);
+                break;
+            case S_U:
+                launch_resid_t(p, L, A, SrcU{s.u, L.grid()}, g, dout, x0out, nullptr, 1);
+                break;
+            case S_PROLONG:
+                launch_resid_t(p, L, A, SrcProlong{prolong_from(p, L.l - 1, s.uc), L.nx, L.ny, 0.0}, g, dout,
+                               x0out, nullptr, 1);
+                break;
+            case S_CORRECT:
+                launch_resid_t(p, L, A, SrcCorrect{s.u, L.grid(), prolong_from(p, L.l - 1, s.uc), 0.0, 0.0}, g,
+                               dout, x0out, nullptr, 1, s.om);
+                break;
+            default:
+                throw GmgError{GMG_ERR_LOGIC, "defect: bad source"};
+        }
+    });
+}
+
+// One lexicographic Gauss-Seidel/SOR smooth_step: x' = x - damp * (D + om L)^{-1} (A x - g).
+void launch_gs_wave(gmg_problem* p, const Lev& L, const double* d, const double* x, double* xo, double om,
+                    double damp) {
+    const int warps = (L.ny + 31) / 32;
+    if (warps > p->gs_warps) throw GmgError{GMG_ERR_LOGIC, "gs: workspace too small"};
+    const int threads = std::min(1024, warps * 32);
+    const int blocks = (warps * 32 + threads - 1) / threads;
+    CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
+    with_coef(L, [&](const auto& A) {
+        k_gs_wave<<<blocks, threads, 0, p->st>>>(L.grid(), A, d, x, xo, om, damp, p->gs_edge, p->gs_prog);
+    });
+    CK(cudaGetLastError());
+}
+
+// `steps` Gauss-Seidel smoothing steps from source s (a non-u start is
+// materialised in bufA; outputs then alternate). Uses DD as defect scratch.
+double* gs_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const double* g, double* bufA,
+                 double* bufB, double om, double damp) {
+    if (steps == 0) {
+        launch_smooth(p, L, 0, s, g, bufA, damp);
+        return bufA;
+    }
+    double* d = L.buf[DD];
+    const double* x;
+    double* out;
+    if (s.kind == S_U) {  // x0 = u in place
+        launch_defect_src(p, L, s, g, d, nullptr);
+        x = s.u;
+        out = (bufA != s.u) ? bufA : bufB;
+    } else {  // materialise x0 in bufA (never the buffer a source reads)
+        launch_defect_src(p, L, s, g, d, bufA);
+        x = bufA;
+        out = bufB;
+    }
+    for (int k = 0; k < steps; ++k) {
+        launch_gs_wave(p, L, d, x, out, om, damp);
+        if (k + 1 == steps) break;
+        SmoothSrc n;
+        n.kind = S_U;
+        n.u = out;
+        launch_defect_src(p, L, n, g, d, nullptr);
+        x = out;
+        out = (out == bufA) ? bufB : bufA;
+    }
+    return out;
 }
 
 void launch_restrict(gmg_problem* p, int fine_level, const double* f, double* c) {
@@ -450,6 +528,13 @@ struct Driver {
     gmg_problem* p;
     gmg_cycle_desc sp;
 
+    // smooth_step x `steps` with the configured preconditioner (setup_smoothers)
+    double* smooth(const Lev& L, int steps, const SmoothSrc& s, const double* g, double* a, double* b) {
+        if (sp.smoother_kind == GMG_SMOOTHER_GAUSS_SEIDEL || sp.smoother_kind == GMG_SMOOTHER_SOR)
+            return gs_steps(p, L, steps, s, g, a, b, sp.smoother_omega, sp.smoothing_omega);
+        return smooth_steps(p, L, steps, s, g, a, b, sp.smoothing_omega);
+    }
+
     // gmg::mg_cycle (cycle.cpp:69-100) on level l from start s with rhs g.
     const double* visit(int l, SmoothSrc s, const double* g) {
         Lev& L = p->lev(l);
@@ -461,12 +546,11 @@ struct Driver {
             }
             double* a = (s.u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
             double* b = (a == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
-            return smooth_steps(p, L, std::max(1, sp.pre_steps + sp.post_steps), s, g, a, b,
-                                sp.smoothing_omega);
+            return smooth(L, std::max(1, sp.pre_steps + sp.post_steps), s, g, a, b);
         }
         double* a = (s.u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
         double* b = (a == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
-        double* u = smooth_steps(p, L, sp.pre_steps, s, g, a, b, sp.smoothing_omega);
+        double* u = smooth(L, sp.pre_steps, s, g, a, b);
         double* other = (u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
         const bool adaptive = sp.adaptive_correction != 0;
         Lev& C = p->lev(l - 1);
@@ -490,7 +574,7 @@ struct Driver {
         } else {
             cs.om = OmegaSrc{nullptr, nullptr, sp.correction_omega, p->status};
         }
-        return smooth_steps(p, L, sp.post_steps, cs, g, other, u, sp.smoothing_omega);
+        return smooth(L, sp.post_steps, cs, g, other, u);
     }
 
     // One outer cycle: x_out = cycle(x_in); r = b - A x_out -> DCAS[L]; norm^2 -> sums[2].
@@ -587,7 +671,8 @@ void check_smoother(const gmg_cycle_desc& sp) {
         default:
             throw std::invalid_argument("smoother: unknown kind");
     }
-    if (sp.smoother_kind != GMG_SMOOTHER_JACOBI)
+    if (sp.smoother_kind != GMG_SMOOTHER_JACOBI && sp.smoother_kind != GMG_SMOOTHER_GAUSS_SEIDEL &&
+        sp.smoother_kind != GMG_SMOOTHER_SOR)
         throw GmgError{GMG_ERR_UNSUPPORTED, "smoother kind not implemented on the device yet"};
 }
 
@@ -699,6 +784,8 @@ void free_problem(gmg_problem* p) {
     cudaFree(p->flags);
     cudaFree(p->recs);
     cudaFree(p->ss_stats);
+    cudaFree(p->gs_edge);
+    cudaFree(p->gs_prog);
     cudaFree(p->sums);
     cudaFree(p->nz);
     cudaFree(p->status);
@@ -851,6 +938,14 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
         CK(cudaMalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
         CK(cudaMalloc(&p->ss_stats, 8 * sizeof(unsigned long long)));
+        int maxny = 0, maxnx = 0;
+        for (const Lev& Lq : p->lv) {
+            maxny = std::max(maxny, Lq.ny);
+            maxnx = std::max(maxnx, Lq.nx);
+        }
+        p->gs_warps = (maxny + 31) / 32;
+        CK(cudaMalloc(&p->gs_edge, (size_t)p->gs_warps * maxnx * sizeof(double)));
+        CK(cudaMalloc(&p->gs_prog, p->gs_warps * sizeof(int)));
         CK(cudaMemset(p->ss_stats, 0, 8 * sizeof(unsigned long long)));
         CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
@@ -1026,8 +1121,12 @@ int gmg_dev_smooth_step(gmg_problem* p, int level, int kind, double somega, doub
         SmoothSrc s;
         s.kind = S_U;
         s.u = L.buf[U0];
-        launch_smooth(p, L, 1, s, L.buf[GRHS], L.buf[U1], omega_damp);
-        download(p, L, out, L.buf[U1], cudaMemcpyDeviceToHost);
+        double* r = L.buf[U1];
+        if (kind == GMG_SMOOTHER_GAUSS_SEIDEL || kind == GMG_SMOOTHER_SOR)
+            r = gs_steps(p, L, 1, s, L.buf[GRHS], L.buf[U1], L.buf[DCAS], somega, omega_damp);
+        else
+            launch_smooth(p, L, 1, s, L.buf[GRHS], L.buf[U1], omega_damp);
+        download(p, L, out, r, cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
     });
 }

@@ -53,10 +53,11 @@ def test_per_level_operators_bitexact(problems, gi):
         b = Oracle.random_vector(n, 20 + l)
         assert bits_equal(gmg.apply(d, l, x), o.apply(l, x)), ("apply", l)
         assert bits_equal(gmg.residual(d, l, x, b), o.residual(l, x, b)), ("residual", l)
-        for damp in (0.7, 1.0, 0.35):
-            got = gmg.smooth_step(d, l, "jacobi", 1.0, x, b, damp)
-            want = o.smooth_step(l, "jacobi", 1.0, damp, x, b)
-            assert bits_equal(got, want), ("smooth_step", l, damp, first_mismatch(got, want))
+        for kind, som in (("jacobi", 1.0), ("jacobi", 1.3), ("gauss_seidel", 1.0), ("sor", 1.4), ("sor", 0.6)):
+            for damp in (0.7, 1.0, 0.35):
+                got = gmg.smooth_step(d, l, kind, som, x, b, damp)
+                want = o.smooth_step(l, kind, som, damp, x, b)
+                assert bits_equal(got, want), ("smooth_step", kind, som, l, damp, first_mismatch(got, want))
         if l >= 2:
             assert bits_equal(gmg.restriction(d, l, x), o.restriction(l, x)), ("restriction", l)
             c = Oracle.random_vector(d.n(l - 1), 30 + l)
@@ -139,13 +140,14 @@ def test_axpy(problems):
     assert bits_equal(y, want)
 
 
+@pytest.mark.parametrize("smoother", ["jacobi", "gauss_seidel"])
 @pytest.mark.parametrize("cycle", ["V", "W"])
 @pytest.mark.parametrize("gi", [0, 2, 3], ids=["cart", "cyl", "sph"])
-def test_mg_cycle_bitexact(problems, cycle, gi):
+def test_mg_cycle_bitexact(problems, cycle, gi, smoother):
     d, o = problems[gi]
     L = d.num_levels
     for adaptive in (True, False):
-        spec = dict(cycle=cycle, smoother="jacobi", pre_steps=2, post_steps=1, adaptive_correction=adaptive,
+        spec = dict(cycle=cycle, smoother=smoother, pre_steps=2, post_steps=1, adaptive_correction=adaptive,
                     correction_omega=3.0)
         for l in range(1, L + 1):
             u0 = Oracle.random_vector(d.n(l), 40 + l)
@@ -234,6 +236,39 @@ def test_repeated_solves_are_deterministic(gpu):
         x = x0.copy()
         hs.append(gmg.solve(d, b, spec, x).residual_history)
     assert bits_equal(hs[0], hs[1])
+
+
+C2_FIXTURES = [f"c2_eps{e}_s{k}" for e in ("1", "0.1", "0.01", "0.001") for k in (1, 2, 4)]
+
+
+@pytest.mark.parametrize("name", C2_FIXTURES)
+def test_c2_gauss_seidel_matches_reference_golden(gpu, name):
+    """BASELINE configs[1]: anisotropic -eps u_xx - u_yy on 1023^2 (10 levels), random start,
+    lexicographic Gauss-Seidel s+s, adaptive omega_l, up to 50 cycles — bit for bit."""
+    g, d, b, x, spec = run_fixture(name)
+    rep = gmg.solve(d, b, spec, x)
+    want = unhex(g["history"])
+    assert rep.iterations == g["iterations"] and rep.converged == g["converged"]
+    assert bits_equal(rep.residual_history, want), first_mismatch(rep.residual_history, want)
+    assert bits_equal(x[:8], unhex(g["x_head"])) and bits_equal(x[-8:], unhex(g["x_tail"]))
+
+
+@pytest.mark.parametrize("smoother,som", [("gauss_seidel", 1.0), ("sor", 1.3)])
+@pytest.mark.parametrize("cycle", ["V", "W", "F"])
+def test_gs_solves_bitexact_vs_oracle(gpu, smoother, som, cycle):
+    for coords, grading, coarse in (("cartesian", (1.0, 1.0), (1, 1)), ("spherical", (1.05, 0.97), (2, 3))):
+        args = (5, coarse[0], coarse[1], grading, coords, 0.3, 1.0)
+        d, o = gmg.MultilevelProblem(*args), Oracle(*args)
+        n = d.n(5)
+        b = gmg.random_vector(n, 1)
+        x0 = gmg.random_vector(n, 2)
+        kw = dict(cycle=cycle, smoother=smoother, smoother_omega=som, pre_steps=2, post_steps=3, tolerance=1e-11,
+                  max_cycles=30)
+        xg, xo = x0.copy(), x0.copy()
+        rg = gmg.solve(d, b, gmg.CycleSpec(**kw), xg)
+        ro = o.solve(OSpec(**kw), b, xo)
+        assert rg.iterations == ro.iterations and bits_equal(rg.residual_history, ro.history)
+        assert bits_equal(xg, xo)
 
 
 @pytest.mark.slow
