@@ -25,8 +25,10 @@ CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
 
 SOURCES_CU = ["solver.cu"]
 SOURCES_CPP = ["host_setup.cpp"]
-DEPS = ["common.cuh", "march.cuh", "seqsum.cuh", "seqsum_core.h", "host_setup.h",
-        os.path.join("..", "..", "include", "gmg_b200.h")]
+def _deps():
+    """Every header the sources may include (all of csrc/ plus the C ABI)."""
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp"))]
+    return hs + [os.path.join(ROOT, "include", "gmg_b200.h")]
 
 
 def _newer(target: str, sources) -> bool:
@@ -48,7 +50,7 @@ def _run(cmd, log):
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     log = os.path.join(BUILD, "build.log")
-    deps = [os.path.join(CSRC, d) for d in DEPS]
+    deps = _deps()
     objs = []
     for src in SOURCES_CU:
         s = os.path.join(CSRC, src)

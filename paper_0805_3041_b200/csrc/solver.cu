@@ -445,11 +445,18 @@ void launch_gs_wave(gmg_problem* p, const Lev& L, const double* d, const double*
                     double damp) {
     const int warps = (L.ny + 31) / 32;
     if (warps > p->gs_warps) throw GmgError{GMG_ERR_LOGIC, "gs: workspace too small"};
-    const int threads = std::min(1024, warps * 32);
-    const int blocks = (warps * 32 + threads - 1) / threads;
+    const int blocks = (warps + kGsWarps - 1) / kGsWarps;
+    if (blocks > 148) throw GmgError{GMG_ERR_UNSUPPORTED, "gs: more rows than one co-resident wavefront"};
     CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
     with_coef(L, [&](const auto& A) {
-        k_gs_wave<<<blocks, threads, 0, p->st>>>(L.grid(), A, d, x, xo, om, damp, p->gs_edge, p->gs_prog);
+        using C = std::decay_t<decltype(A)>;
+        static bool attr = false;
+        if (!attr) {
+            set_smem(k_gs_wave<C>, gs_smem());
+            attr = true;
+        }
+        k_gs_wave<<<blocks, kGsWarps * 32, gs_smem(), p->st>>>(L.grid(), A, d, x, xo, om, damp, p->gs_edge,
+                                                                p->gs_prog);
     });
     CK(cudaGetLastError());
 }
