@@ -292,7 +292,7 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
             st = make_state(s);
             if (brk) st = make_state(st.s + r.pb);
         } else if (brk) {
-            const double sb = g.len ? compose(st.M + g.Q[st.M & 1], st.E) : st.s;
+            const double sb = g.len ? compose(st.M + ((st.M & 1) ? g.Q[1] : g.Q[0]), st.E) : st.s;
             st = make_state(sb + r.pb);
         } else {
             seg_apply(g, st);

@@ -277,7 +277,7 @@ __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 // ---- walk ---------------------------------------------------------------------
 // grid (nch, NS); block kSsT; dynamic smem (kSsC + kSsC/32) doubles.
 template <class TG>
-__global__ void __launch_bounds__(kSsT) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
+__global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
     extern __shared__ double tm[];
     __shared__ double swd[8];
     __shared__ SegF sws[8];
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
                 const uint64_t E = (bits >> 52) & 0x7ffu;
                 const int v = (ties && (bits & 1u)) ? 1 : 0;
                 const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
-                const long long Qi = r.Q[v], mni = r.mn[v], mxi = r.mx[v];
+                const long long Qi = v ? r.Q[1] : r.Q[0], mni = v ? r.mn[1] : r.mn[0], mxi = v ? r.mx[1] : r.mx[0];
                 const bool neg = bits >> 63;
                 // |M| = mant; for a negative sum M + x ranges over -(mant - x)
                 const long long lo_v = neg ? mant - mxi : mant + mni;

@@ -127,11 +127,15 @@ SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
     r.neg = a.neg;
     r.len = a.len + b.len;
     r.bad = a.bad | b.bad | (a.E != b.E) | (a.neg != b.neg);
+    // (selects, not b.Q[pb]: a runtime index would force the struct to local memory)
+#pragma unroll
     for (int p = 0; p < 2; ++p) {
         const int64_t qa = a.Q[p];
-        const int pb = static_cast<int>((p + qa) & 1);
-        r.Q[p] = qa + b.Q[pb];
-        const int64_t bmn = qa + b.mn[pb], bmx = qa + b.mx[pb];
+        const bool odd = ((p + qa) & 1) != 0;
+        const int64_t bq = odd ? b.Q[1] : b.Q[0];
+        const int64_t bmn = qa + (odd ? b.mn[1] : b.mn[0]);
+        const int64_t bmx = qa + (odd ? b.mx[1] : b.mx[0]);
+        r.Q[p] = qa + bq;
         r.mn[p] = a.mn[p] < bmn ? a.mn[p] : bmn;
         r.mx[p] = a.mx[p] > bmx ? a.mx[p] : bmx;
     }
@@ -142,15 +146,16 @@ SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
 SS_HD bool seg_valid(const Seg& g, const State& st) {
     if (g.len == 0) return !g.bad;
     if (g.bad || st.E == 0 || st.E != g.E || (st.M < 0) != (g.neg != 0)) return false;
-    const int p = static_cast<int>(st.M & 1);
-    if (!g.neg) return st.M + g.mn[p] >= kLo && st.M + g.mx[p] <= kHi;
-    return st.M + g.mx[p] <= -kLo && st.M + g.mn[p] >= -kHi;
+    const bool odd = (st.M & 1) != 0;
+    const int64_t mn = odd ? g.mn[1] : g.mn[0], mx = odd ? g.mx[1] : g.mx[0];
+    if (!g.neg) return st.M + mn >= kLo && st.M + mx <= kHi;
+    return st.M + mx <= -kLo && st.M + mn >= -kHi;
 }
 
 // Apply a valid segment.
 SS_HD void seg_apply(const Seg& g, State& st) {
     if (g.len == 0) return;
-    st.M += g.Q[st.M & 1];
+    st.M += (st.M & 1) ? g.Q[1] : g.Q[0];
     st.s = compose(st.M, st.E);
 }
 
