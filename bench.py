@@ -153,7 +153,7 @@ def usable_threads(n_dof):
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 32 << 30
-    per_solve = 70 * 8 * n_dof  # measured peak transient of one reference F-cycle (~70 vectors)
+    per_solve = 20 * 8 * n_dof  # peak transient of one reference solve (~140 B/DOF measured at C5)
     shared = 60 * n_dof  # operators + b
     by_mem = max(1, int((avail * 0.8 - shared) // per_solve))
     return max(1, min(cores, by_mem))

@@ -278,7 +278,7 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
         }
         approx = acc;
     }
-    recs.push_back(rec_make(carry, false, 0.0, static_cast<uint32_t>(n)));
+    recs.push_back(rec_make(carry, false, 0.0, static_cast<uint32_t>(n - 1)));
     long long nlit = 0, prev = -1;
     State st = make_state(0.0);
     for (const Rec& r : recs) {
@@ -288,7 +288,7 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
         if (!seg_valid(g, st)) {
             ++nlit;
             double s = st.s;
-            for (long long k = prev + 1; k < std::min(kb, n); ++k) s = s + p[k];
+            for (long long k = prev + 1; k < (brk ? kb : kb + 1); ++k) s = s + p[k];
             st = make_state(s);
             if (brk) st = make_state(st.s + r.pb);
         } else if (brk) {
@@ -297,7 +297,7 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
         } else {
             seg_apply(g, st);
         }
-        prev = brk ? kb : n - 1;
+        prev = kb;
     }
     if (stats) {
         stats[0] = nch;

@@ -34,7 +34,8 @@ constexpr int kSsEPT = 32;            // terms per thread
 constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
-constexpr int kSsRMax = 256;          // records a chunk may store; more -> literal re-sum
+constexpr int kSsRMax = 256;          // records a chunk may store; more -> exact re-walk
+constexpr int kSsRunCap = 16;         // a merged run never spans more than this many chunks
 
 // Per-sum look-back state (flags, ticket and total zeroed before each walk).
 struct SsState {
@@ -353,14 +354,17 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
     SegF tot;
     const SegF carry = block_excl_segscan(x, sws, &tot);
     const bool last = c == nch - 1;
-    const int R = tot.cnt + (last ? 1 : 0);
+    // every kSsRunCap-th chunk closes its run with a no-break record, so a
+    // speculation failure never re-walks more than kSsRunCap chunks
+    const bool close = last || (c % kSsRunCap) == kSsRunCap - 1;
+    const int R = tot.cnt + (close ? 1 : 0);
     const bool literal = R > kSsRMax;
 
     // (5) run carry + record offset by look-back over chunks (aggregate
     //     published first, so no chunk waits on a predecessor's look-back)
     SegF mine = tot;
     mine.cnt = literal ? 1 : R;
-    if (literal) {
+    if (literal || close) {
         mine.f = 1;
         mine.g = gmg_ss::seg_empty();
     }
@@ -410,9 +414,9 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
             }
         }
     }
-    if (last && t == kSsT - 1) {
+    if (close && t == kSsT - 1) {
         const gmg_ss::Seg g = tot.f ? tot.g : gmg_ss::seg_merge(cin.g, tot.g);
-        out[R - 1] = gmg_ss::rec_make(g, false, 0.0, (uint32_t)n);
+        out[R - 1] = gmg_ss::rec_make(g, false, 0.0, (uint32_t)(base + clen - 1));
     }
 }
 
@@ -436,6 +440,62 @@ __device__ double literal_sum(const TG& tg, int s, double a, long long k0, long 
     const int m = (int)(k1 - k);
     for (int j = 0; j < m; ++j) a = a + __shfl_sync(0xffffffffu, nxt, j);
     return __shfl_sync(0xffffffffu, a, 0);
+}
+
+// Exact sum of terms [k0, k1) added to sv, by one warp with the integer model:
+// 32 terms at a time, an inclusive prefix of q = RN(p/u) across lanes, commit
+// up to the first lane that breaks (binade exit, tie, huge term), real add for
+// that lane, restart after it. Bit-identical to literal adds, ~5 cycles/term
+// when breaks are sparse.
+template <class TG>
+__device__ double warp_walk(const TG& tg, int s, double sv, long long k0, long long k1) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    double nxt = (k0 + lane < k1) ? tg.term(s, k0 + lane) : 0.0;
+    for (long long k = k0; k < k1; k += 32) {
+        const double p = nxt;
+        nxt = (k + 32 + lane < k1) ? tg.term(s, k + 32 + lane) : 0.0;
+        const int m = (int)min(32LL, k1 - k);
+        int start = 0;
+        while (start < m) {
+            const uint64_t bits = gmg_ss::dbits(sv);
+            const int E = (int)((bits >> 52) & 0x7ff);
+            if (E < gmg_ss::kEMin || E > gmg_ss::kEMax) {  // zero/subnormal/huge: one real add
+                sv = sv + __shfl_sync(full, p, start);
+                ++start;
+                continue;
+            }
+            const double inv_u = gmg_ss::bitsd((uint64_t)(2098 - E) << 52);
+            const bool mine = lane >= start && lane < m;
+            const double xv = p * inv_u;
+            const double fl = floor(xv);
+            const double fr = xv - fl;
+            const bool bad = !(xv < gmg_ss::kTwo52 && xv > -gmg_ss::kTwo52) || fr == 0.5;
+            long long q = (mine && !bad) ? (long long)fl + (fr > 0.5 ? 1 : 0) : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(full, q, o);
+                if (lane >= o) q += y;
+            }
+            const bool neg = bits >> 63;
+            const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
+            const long long Mn = neg ? mant - q : mant + q;  // |M| after this lane
+            const bool ok = !bad && Mn >= gmg_ss::kLo && Mn <= gmg_ss::kHi;
+            const unsigned failm = __ballot_sync(full, mine && !ok);
+            const int f = failm ? __ffs(failm) - 1 : m;
+            if (f > start) {
+                const long long P = __shfl_sync(full, q, f - 1);
+                sv = gmg_ss::compose(neg ? -(mant - P) : mant + P, E);  // signed M + P
+            }
+            if (f < m) {
+                sv = sv + __shfl_sync(full, p, f);
+                start = f + 1;
+            } else {
+                start = m;
+            }
+        }
+    }
+    return sv;
 }
 
 // grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays,
@@ -492,17 +552,19 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
                 const double u = gmg_ss::bitsd((E - 52) << 52);
                 double s1 = ne ? sv + (double)Qi * u : sv;
                 if (!ok) {
-                    // re-sum this record's range literally (through kb for literal chunks)
-                    const long long k1 = min(lit ? kb + 1 : kb, n);
+                    // re-walk this record's range exactly from the true state (the break
+                    // element, if any, is applied below; otherwise kb is inclusive)
+                    const long long k1 = min(brk ? kb : kb + 1, n);
                     const long long c0 = clock64();
-                    s1 = literal_sum(tg, s, sv, prev + 1, k1);
+                    // dense breaks (literal chunk): plain adds; a failed run: integer walk
+                    s1 = lit ? literal_sum(tg, s, sv, prev + 1, k1) : warp_walk(tg, s, sv, prev + 1, k1);
                     cyc_lit += clock64() - c0;
                     ++n_lit;
                     n_litterms += k1 - (prev + 1);
                 }
                 sv = brk ? s1 + pb : s1;
                 n_brk += brk;
-                prev = (lit || brk) ? kb : n - 1;
+                prev = kb;
             }
         } else if (b + 1 < nb) {
             gmg_ss::Rec* B = buf + ((b + 1) & 1) * kSsBatch;

@@ -212,12 +212,13 @@ SS_HD void real_add(State& st, double p) {
 }
 
 // Record as stored for the chain: the merged run of elements since the previous
-// record's break element, then optionally one break element at global index kb
-// (applied with a real add). The run's elements are exactly (prev.kb, kb), so a
-// record that fails validation is re-summed literally over that range. 64 bytes.
+// record, then optionally one break element at global index kb (applied with a
+// real add). A record covers exactly the elements (prev.kb, kb]; with a break
+// the last of them is the break element. A record that fails validation is
+// re-walked exactly over its range. 64 bytes.
 //   meta: E (11b) | neg<<11 | has_break<<12 | bad<<13 | literal<<14 | nonempty<<15
-// `literal` marks a chunk with too many breaks to store: the chain re-sums
-// (prev.kb, kb] literally (kb = the chunk's last element).
+// `literal` marks a chunk with too many breaks to store: the chain re-walks
+// (prev.kb, kb] (kb = the chunk's last element).
 struct Rec {
     int64_t Q[2], mn[2], mx[2];
     double pb;
