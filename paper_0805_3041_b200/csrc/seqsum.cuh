@@ -112,6 +112,7 @@ __device__ __forceinline__ SegF segf_shfl(const SegF& x, int src, bool up, int o
     r.g.E = m2 & 0x7ff;
     r.g.neg = (m2 >> 11) & 1;
     r.g.bad = (m2 >> 12) & 1;
+    r.g.tied = 1;
     r.f = (m2 >> 13) & 1;
     return r;
 }
@@ -149,6 +150,7 @@ __device__ __forceinline__ SegF agg_load(const unsigned char* base, int c) {
     v.g.E = meta & 0x7ff;
     v.g.neg = (meta >> 11) & 1;
     v.g.bad = (meta >> 12) & 1;
+    v.g.tied = 1;
     v.f = (meta >> 13) & 1;
     v.g.len = __ldcg(&p->len);
     v.cnt = __ldcg(&p->cnt);
@@ -164,9 +166,7 @@ __device__ double lookback_d(int c, const int* flag, const double* agg, const do
         const int idx = p - lane;
         int f = 2;
         if (idx >= 0) {
-            do {
-                f = ld_flag(flag + idx);
-            } while (f == 0);
+            while ((f = ld_flag(flag + idx)) == 0) __nanosleep(64);
         }
         __threadfence();
         const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
@@ -196,9 +196,7 @@ __device__ SegF lookback_seg(int c, const int* flag, const unsigned char* agg, c
         const int idx = p - lane;
         int f = 2;
         if (idx >= 0) {
-            do {
-                f = ld_flag(flag + idx);
-            } while (f == 0);
+            while ((f = ld_flag(flag + idx)) == 0) __nanosleep(64);
         }
         __threadfence();
         const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
@@ -345,6 +343,8 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
         }
     }
     if (r == 0) lead = cur;
+    gmg_ss::seg_finish(cur);
+    gmg_ss::seg_finish(lead);
 
     // (4) merge runs across threads; records = breaks (+ the final record)
     SegF x = segf_id();

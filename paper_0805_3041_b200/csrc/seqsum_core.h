@@ -106,8 +106,20 @@ struct Seg {
     int neg;   // sign of the running sum inside the segment
     int len;   // number of elements; 0 = empty (identity for merge)
     int bad;   // 1 = produced by merging incompatible segments (forces a fallback)
+    int tied;  // walking only: a tie occurred (variant 1 is tracked separately from then on)
     int64_t Q[2], mn[2], mx[2];
 };
+
+// Before a walked segment is merged or stored: without a tie both parity
+// variants are identical, and only variant 0 was maintained.
+SS_HD void seg_finish(Seg& g) {
+    if (!g.tied) {
+        g.Q[1] = g.Q[0];
+        g.mn[1] = g.mn[0];
+        g.mx[1] = g.mx[0];
+    }
+    g.tied = 1;
+}
 
 SS_HD Seg seg_empty() {
     Seg s;
@@ -115,11 +127,14 @@ SS_HD Seg seg_empty() {
     s.neg = 0;
     s.len = 0;
     s.bad = 0;
+    s.tied = 1;
     for (int p = 0; p < 2; ++p) s.Q[p] = s.mn[p] = s.mx[p] = 0;
     return s;
 }
 
-SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
+SS_HD Seg seg_merge(Seg a, Seg b) {
+    seg_finish(a);
+    seg_finish(b);
     if (a.len == 0 && !a.bad) return b;
     if (b.len == 0 && !b.bad) return a;
     Seg r;
@@ -127,6 +142,7 @@ SS_HD Seg seg_merge(const Seg& a, const Seg& b) {
     r.neg = a.neg;
     r.len = a.len + b.len;
     r.bad = a.bad | b.bad | (a.E != b.E) | (a.neg != b.neg);
+    r.tied = 1;
     // (selects, not b.Q[pb]: a runtime index would force the struct to local memory)
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
@@ -185,20 +201,35 @@ SS_HD bool walk_try(State& st, Seg& cur, double p) {
     if (cur.len == 0) {
         cur.E = st.E;
         cur.neg = st.M < 0;
+        cur.tied = 0;
         for (int v = 0; v < 2; ++v) cur.Q[v] = cur.mn[v] = cur.mx[v] = 0;
     }
-    for (int v = 0; v < 2; ++v) {
-        // variant v: segment entered with parity v; current parity (v + Q[v]) & 1
-        const int64_t q = tie ? n + ((v + cur.Q[v] + n) & 1) : qr;
-        const int64_t P = cur.Q[v] + q;
+    if (!cur.tied && !tie) {
+        // fast path: both variants identical so far, only variant 0 is kept
+        const int64_t P = cur.Q[0] + qr;
         if (cur.len == 0) {
-            cur.mn[v] = P;
-            cur.mx[v] = P;
+            cur.mn[0] = P;
+            cur.mx[0] = P;
         } else {
-            cur.mn[v] = P < cur.mn[v] ? P : cur.mn[v];
-            cur.mx[v] = P > cur.mx[v] ? P : cur.mx[v];
+            cur.mn[0] = P < cur.mn[0] ? P : cur.mn[0];
+            cur.mx[0] = P > cur.mx[0] ? P : cur.mx[0];
         }
-        cur.Q[v] = P;
+        cur.Q[0] = P;
+    } else {
+        if (!cur.tied) seg_finish(cur);  // first tie: variant 1 starts as a copy
+        for (int v = 0; v < 2; ++v) {
+            // variant v: segment entered with parity v; current parity (v + Q[v]) & 1
+            const int64_t q = tie ? n + ((v + cur.Q[v] + n) & 1) : qr;
+            const int64_t P = cur.Q[v] + q;
+            if (cur.len == 0) {
+                cur.mn[v] = P;
+                cur.mx[v] = P;
+            } else {
+                cur.mn[v] = P < cur.mn[v] ? P : cur.mn[v];
+                cur.mx[v] = P > cur.mx[v] ? P : cur.mx[v];
+            }
+            cur.Q[v] = P;
+        }
     }
     st.M = Mn;
     cur.len += 1;
@@ -226,7 +257,8 @@ struct Rec {
     uint32_t kb;
 };
 
-SS_HD Rec rec_make(const Seg& g, bool has_break, double pb, uint32_t kb) {
+SS_HD Rec rec_make(Seg g, bool has_break, double pb, uint32_t kb) {
+    seg_finish(g);
     Rec r;
     for (int p = 0; p < 2; ++p) {
         r.Q[p] = g.Q[p];
@@ -250,6 +282,7 @@ SS_HD Seg rec_seg(const Rec& r) {
     g.E = static_cast<int>(r.meta & 0x7ff);
     g.neg = static_cast<int>((r.meta >> 11) & 1);
     g.bad = static_cast<int>((r.meta >> 13) & 1);
+    g.tied = 1;
     g.len = static_cast<int>((r.meta >> 15) & 1);  // emptiness only
     for (int p = 0; p < 2; ++p) {
         g.Q[p] = r.Q[p];
