@@ -169,9 +169,11 @@ int gmg_dev_axpy(gmg_problem* p, long long n, double alpha, const double* x, dou
 int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int variant, int reps,
                           double* ms_per_launch, double* bytes_per_launch);
 /* Exact-order summation engine counters accumulated since the last reset:
- * [0] sums, [1] records, [2] chain SM cycles, [3] of which literal re-sums,
- * [4] break adds, [5] literal re-sums, [6] terms re-summed literally, [7] chunks. */
-int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out8);
+ * [0] sums, [1] records, [2] chain SM cycles, [3] of which re-walks,
+ * [4] break adds, [5] re-walked ranges, [6] terms re-walked, [7] chunks,
+ * [8..12] walk-kernel SM cycles per phase (load, prefix look-back, thread walk,
+ * block merge, run/offset look-back), [13] walk CTAs. out16 holds 16 values. */
+int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out16);
 /* Number of kernels one solver cycle launches (from the captured graph). */
 int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* count);
 

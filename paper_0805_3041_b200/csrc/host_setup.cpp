@@ -260,21 +260,21 @@ double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* s
                 if (e < clen) ts += p[base + e];
             }
             acc += ts;
-            State st = make_state(pred);
-            Seg cur = seg_empty();
+            Walker wk;
+            walker_init(wk, pred);
             for (int m = 0; m < EPT; ++m) {
                 const int e = t * EPT + m;
                 if (e >= clen) break;
                 const double v = p[base + e];
-                if (!walk_try(st, cur, v)) {
+                if (!walker_try(wk, v)) {
                     ++nbreaks;
-                    recs.push_back(rec_make(seg_merge(carry, cur), true, v, static_cast<uint32_t>(base + e)));
+                    recs.push_back(rec_make(seg_merge(carry, walker_seg(wk)), true, v, static_cast<uint32_t>(base + e)));
                     carry = seg_empty();
-                    cur = seg_empty();
-                    real_add(st, v);
+                    walker_open(wk);
+                    walker_real_add(wk, v);
                 }
             }
-            carry = seg_merge(carry, cur);
+            carry = seg_merge(carry, walker_seg(wk));
         }
         approx = acc;
     }

@@ -48,7 +48,8 @@ struct SsState {
     unsigned char* cagg;   // [nch] ChunkAgg
     unsigned char* cincl;  // [nch] ChunkAgg
     gmg_ss::Rec* recs;
-    unsigned long long* stats;  // [8] calls, records, -, -, break adds, literal ranges, literal terms, chunks
+    unsigned long long* stats;  // [16] calls, records, chain cycles, re-walk cycles, break adds, re-walks,
+                                //      re-walked terms, chunks; walk phase cycles [8..13]
 };
 struct SsPair {
     SsState s[kSsMaxSums];
@@ -287,23 +288,31 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
     const int s = blockIdx.y;
     const SsState& S = sts.s[s];
     const int t = threadIdx.x;
+    long long ph[7];
+    ph[0] = clock64();
     if (t == 0) s_chunk = atomicAdd(S.ticket, 1);
     __syncthreads();
     const int c = s_chunk;
     const long long base = (long long)c * kSsC;
     const int clen = (int)min((long long)kSsC, n - base);
 
-    // (1) terms: striped (coalesced) loads into shared memory
-#pragma unroll 8
-    for (int m = 0; m < kSsEPT; ++m) {
-        const int kl = m * kSsT + t;
-        tm[ss_pad(kl)] = kl < clen ? tg.term(s, base + kl) : 0.0;
+    // (1) terms: striped (coalesced) loads, all in flight before the smem stores
+    {
+        double v[kSsEPT];
+#pragma unroll
+        for (int m = 0; m < kSsEPT; ++m) {
+            const int kl = m * kSsT + t;
+            v[m] = kl < clen ? tg.term(s, base + kl) : 0.0;
+        }
+#pragma unroll
+        for (int m = 0; m < kSsEPT; ++m) tm[ss_pad(m * kSsT + t)] = v[m];
     }
     __syncthreads();
     const int e0 = t * kSsEPT;
     const int ne = max(0, min(kSsEPT, clen - e0));
     double ts = 0.0;
     for (int m = 0; m < ne; ++m) ts += tm[ss_pad(e0 + m)];
+    ph[1] = clock64();
 
     // (2) approximate prefix by look-back
     const double tot_approx = block_sum_d(ts, swd);
@@ -328,23 +337,26 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
     }
     __syncthreads();
     const double pred = s_pre + block_excl_sum_d(ts, swd);
+    ph[2] = clock64();
 
     // (3) thread walk, pass 1: leading segment, trailing segment, break count
-    gmg_ss::State st = gmg_ss::make_state(pred);
-    gmg_ss::Seg cur = gmg_ss::seg_empty(), lead = gmg_ss::seg_empty();
+    gmg_ss::Walker wk;
+    gmg_ss::walker_init(wk, pred);
+    gmg_ss::Seg lead = gmg_ss::seg_empty();
     int r = 0;
     for (int m = 0; m < ne; ++m) {
         const double p = tm[ss_pad(e0 + m)];
-        if (!gmg_ss::walk_try(st, cur, p)) {
-            if (r == 0) lead = cur;
+        if (!gmg_ss::walker_try(wk, p)) {
+            if (r == 0) lead = gmg_ss::walker_seg(wk);
             ++r;
-            cur = gmg_ss::seg_empty();
-            gmg_ss::real_add(st, p);
+            gmg_ss::walker_open(wk);
+            gmg_ss::walker_real_add(wk, p);
         }
     }
+    const gmg_ss::Seg cur = gmg_ss::walker_seg(wk);
     if (r == 0) lead = cur;
-    gmg_ss::seg_finish(cur);
-    gmg_ss::seg_finish(lead);
+    __syncthreads();
+    ph[3] = clock64();
 
     // (4) merge runs across threads; records = breaks (+ the final record)
     SegF x = segf_id();
@@ -353,6 +365,7 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
     x.cnt = r;
     SegF tot;
     const SegF carry = block_excl_segscan(x, sws, &tot);
+    ph[4] = clock64();
     const bool last = c == nch - 1;
     // every kSsRunCap-th chunk closes its run with a no-break record, so a
     // speculation failure never re-walks more than kSsRunCap chunks
@@ -389,6 +402,11 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
         }
     }
     __syncthreads();
+    ph[5] = clock64();
+    if (t == 0 && S.stats) {
+        for (int q = 0; q < 5; ++q) atomicAdd(S.stats + 8 + q, (unsigned long long)(ph[q + 1] - ph[q]));
+        atomicAdd(S.stats + 13, 1ull);
+    }
     const SegF cin = s_carry;  // run since the last break before this chunk; cnt = offset
     gmg_ss::Rec* out = S.recs + cin.cnt;
     if (literal) {
@@ -400,17 +418,17 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
         const int pos = carry.cnt;
         gmg_ss::Seg first = carry.g;
         if (!carry.f) first = gmg_ss::seg_merge(cin.g, first);
-        st = gmg_ss::make_state(pred);
-        cur = gmg_ss::seg_empty();
+        gmg_ss::walker_init(wk, pred);
         int k = 0;
         for (int m = 0; m < ne; ++m) {
             const double p = tm[ss_pad(e0 + m)];
-            if (!gmg_ss::walk_try(st, cur, p)) {
-                const gmg_ss::Seg g = k == 0 ? gmg_ss::seg_merge(first, cur) : cur;
+            if (!gmg_ss::walker_try(wk, p)) {
+                const gmg_ss::Seg sg = gmg_ss::walker_seg(wk);
+                const gmg_ss::Seg g = k == 0 ? gmg_ss::seg_merge(first, sg) : sg;
                 out[pos + k] = gmg_ss::rec_make(g, true, p, (uint32_t)(base + e0 + m));
                 ++k;
-                cur = gmg_ss::seg_empty();
-                gmg_ss::real_add(st, p);
+                gmg_ss::walker_open(wk);
+                gmg_ss::walker_real_add(wk, p);
             }
         }
     }

@@ -236,6 +236,128 @@ SS_HD bool walk_try(State& st, Seg& cur, double p) {
     return true;
 }
 
+// fp64 speculative walker: the same decisions as walk_try, with the integer
+// state and the open segment kept as exactly-representable doubles (|M| < 2^53,
+// |prefix| < 2^53 inside a valid segment), so the per-term fast path is a
+// handful of fp64 ops instead of emulated 64-bit integer arithmetic. Ties and
+// segment closing convert to int64 (exact).
+struct Walker {
+    double s;      // speculated running sum (exact; authoritative when E == 0)
+    int E;         // binade of s (0 = unusable: zero/subnormal/huge)
+    double inv_u;  // 2^(1075-E)
+    double u;      // 2^(E-1075)
+    double M;      // signed integer significand of s
+    int len, tied, segE, segneg;  // open segment
+    double Q[2], mn[2], mx[2];
+};
+
+SS_HD void walker_set(Walker& w, double s) {
+    w.s = s;
+    const uint64_t b = dbits(s);
+    const int E = static_cast<int>((b >> 52) & 0x7ff);
+    if (E < kEMin || E > kEMax) {
+        w.E = 0;
+        w.M = 0.0;
+        w.inv_u = w.u = 0.0;
+        return;
+    }
+    w.E = E;
+    w.inv_u = bitsd(static_cast<uint64_t>(1075 + 1023 - E) << 52);
+    w.u = bitsd(static_cast<uint64_t>(E - 52) << 52);
+    w.M = s * w.inv_u;  // exact
+}
+SS_HD void walker_open(Walker& w) {
+    w.len = 0;
+    w.tied = 0;
+    w.segE = 0;
+    w.segneg = 0;
+    for (int v = 0; v < 2; ++v) w.Q[v] = w.mn[v] = w.mx[v] = 0.0;
+}
+SS_HD void walker_init(Walker& w, double s) {
+    walker_set(w, s);
+    walker_open(w);
+}
+// the open segment as a finished Seg (int64 fields)
+SS_HD Seg walker_seg(const Walker& w) {
+    Seg g = seg_empty();
+    if (w.len == 0) return g;
+    g.E = w.segE;
+    g.neg = w.segneg;
+    g.len = w.len;
+    g.bad = 0;
+    g.tied = 1;
+    const int v1 = w.tied ? 1 : 0;
+    g.Q[0] = static_cast<int64_t>(w.Q[0]);
+    g.mn[0] = static_cast<int64_t>(w.mn[0]);
+    g.mx[0] = static_cast<int64_t>(w.mx[0]);
+    g.Q[1] = static_cast<int64_t>(w.Q[v1]);
+    g.mn[1] = static_cast<int64_t>(w.mn[v1]);
+    g.mx[1] = static_cast<int64_t>(w.mx[v1]);
+    return g;
+}
+SS_HD bool walker_try(Walker& w, double p) {
+    if (w.E == 0) return false;
+    const double x = p * w.inv_u;  // exact power-of-two scaling
+    if (!(x < kTwo52 && x > -kTwo52)) return false;
+#ifdef __CUDA_ARCH__
+    const double q = rint(x);
+    const double fa = fabs(x - q);
+#else
+    const double q = __builtin_rint(x);
+    const double fa = __builtin_fabs(x - q);
+#endif
+    const bool tie = fa == 0.5;
+    double qs = q;
+    double lower = 0.0;
+    if (tie) {  // round the total to even: depends on the parity of M
+        lower = x - 0.5;
+        qs = ((static_cast<int64_t>(w.M) + static_cast<int64_t>(lower)) & 1) ? lower + 1.0 : lower;
+    }
+    const double Mn = w.M + qs;
+#ifdef __CUDA_ARCH__
+    const double aM = fabs(Mn);
+#else
+    const double aM = __builtin_fabs(Mn);
+#endif
+    if (aM < static_cast<double>(kLo) || aM > static_cast<double>(kHi)) return false;
+    if (w.len == 0) {
+        w.segE = w.E;
+        w.segneg = w.M < 0.0;
+    }
+    if (!w.tied && !tie) {
+        const double P = w.Q[0] + qs;
+        w.mn[0] = w.len == 0 ? P : (P < w.mn[0] ? P : w.mn[0]);
+        w.mx[0] = w.len == 0 ? P : (P > w.mx[0] ? P : w.mx[0]);
+        w.Q[0] = P;
+    } else {
+        if (!w.tied) {
+            w.Q[1] = w.Q[0];
+            w.mn[1] = w.mn[0];
+            w.mx[1] = w.mx[0];
+            w.tied = 1;
+        }
+        for (int v = 0; v < 2; ++v) {
+            double qv = qs;
+            if (tie) {
+                const int64_t par = (v + static_cast<int64_t>(w.Q[v]) + static_cast<int64_t>(lower)) & 1;
+                qv = par ? lower + 1.0 : lower;
+            }
+            const double P = w.Q[v] + qv;
+            w.mn[v] = w.len == 0 ? P : (P < w.mn[v] ? P : w.mn[v]);
+            w.mx[v] = w.len == 0 ? P : (P > w.mx[v] ? P : w.mx[v]);
+            w.Q[v] = P;
+        }
+    }
+    w.M = Mn;
+    w.len += 1;
+    return true;
+}
+// the reference's own step s = s + p from the walker's exact state
+SS_HD void walker_real_add(Walker& w, double p) {
+    const double s = (w.E != 0 ? w.M * w.u : w.s) + p;
+    walker_set(w, s);
+}
+
 // The reference's own step s = s + p, from the exact (integer) state.
 SS_HD void real_add(State& st, double p) {
     const double s = (st.E != 0 ? compose(st.M, st.E) : st.s) + p;

@@ -115,7 +115,7 @@ struct gmg_problem {
     int* flags = nullptr;            // per sum: ticket, total, flag[nch], cflag[nch]
     gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records
     int rec_cap = 0;
-    unsigned long long* ss_stats = nullptr;  // [8] exact-sum engine counters (seqsum.cuh)
+    unsigned long long* ss_stats = nullptr;  // [16] exact-sum engine counters (seqsum.cuh)
     double* gs_edge = nullptr;               // Gauss-Seidel wavefront warp-edge rows
     int* gs_prog = nullptr;                  // and their progress counters
     int gs_warps = 0;
@@ -944,7 +944,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
         p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
         CK(cudaMalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
-        CK(cudaMalloc(&p->ss_stats, 8 * sizeof(unsigned long long)));
+        CK(cudaMalloc(&p->ss_stats, 16 * sizeof(unsigned long long)));
         int maxny = 0, maxnx = 0;
         for (const Lev& Lq : p->lv) {
             maxny = std::max(maxny, Lq.ny);
@@ -953,7 +953,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         p->gs_warps = (maxny + 31) / 32;
         CK(cudaMalloc(&p->gs_edge, (size_t)p->gs_warps * maxnx * sizeof(double)));
         CK(cudaMalloc(&p->gs_prog, p->gs_warps * sizeof(int)));
-        CK(cudaMemset(p->ss_stats, 0, 8 * sizeof(unsigned long long)));
+        CK(cudaMemset(p->ss_stats, 0, 16 * sizeof(unsigned long long)));
         CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
         CK(cudaMalloc(&p->nz, sizeof(int)));
@@ -1312,13 +1312,13 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
     });
 }
 
-int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out8) {
+int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out8) {  // 16 values
     return guarded([&] {
         checked(p);
         std::lock_guard<std::mutex> lk(p->mu);
         CK(cudaStreamSynchronize(p->st));
-        CK(cudaMemcpy(out8, p->ss_stats, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        if (reset) CK(cudaMemset(p->ss_stats, 0, 8 * sizeof(unsigned long long)));
+        CK(cudaMemcpy(out8, p->ss_stats, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        if (reset) CK(cudaMemset(p->ss_stats, 0, 16 * sizeof(unsigned long long)));
     });
 }
 

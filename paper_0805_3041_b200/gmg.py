@@ -428,8 +428,9 @@ def cycle_kernel_count(prob: MultilevelProblem, spec: CycleSpec) -> int:
 
 def seqsum_stats(prob: MultilevelProblem, reset: bool = True) -> dict:
     """Exact-order summation engine counters since the last reset."""
-    a = (C.c_ulonglong * 8)()
+    a = (C.c_ulonglong * 16)()
     _check(lib().gmg_dev_seqsum_stats(prob._h, int(reset), a))
-    keys = ["sums", "records", "chain_cycles", "literal_cycles", "break_adds", "literal_ranges",
-            "literal_terms", "chunks"]
+    keys = ["sums", "records", "chain_cycles", "rewalk_cycles", "break_adds", "rewalks",
+            "rewalk_terms", "chunks", "walk_load", "walk_prefix_lookback", "walk_thread_walk",
+            "walk_block_merge", "walk_run_lookback", "walk_ctas"]
     return dict(zip(keys, list(a)))
