@@ -272,6 +272,20 @@ def test_gs_solves_bitexact_vs_oracle(gpu, smoother, som, cycle):
 
 
 @pytest.mark.slow
+def test_c5_full_size_first_cycle(gpu):
+    """BASELINE configs[4] at full size (16383^2 interior, 14 levels, eps=1e-2, jacobi 3+3, random
+    start): the reference's first F-cycle (r0, r1) and solution, bit for bit."""
+    g, d, b, x, spec = run_fixture("c5_1cycle")
+    rep = gmg.solve(d, b, spec, x)
+    assert rep.iterations == 1
+    assert bits_equal(rep.residual_history, unhex(g["history"])), \
+        first_mismatch(rep.residual_history, unhex(g["history"]))
+    assert bits_equal(x[:8], unhex(g["x_head"])) and bits_equal(x[-8:], unhex(g["x_tail"]))
+    import hashlib
+    assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == g["x_sha256"]
+
+
+@pytest.mark.slow
 def test_c4_full_size_history(gpu):
     """BASELINE configs[3] at full size (8191^2 interior, 13 levels): the
     reference's 12-cycle history, bit for bit."""
