@@ -29,6 +29,7 @@
 #include "host_setup.h"
 #include "gs.cuh"
 #include "march.cuh"
+#include "march2.cuh"
 #include "seqsum.cuh"
 
 using namespace gmg_dev;
@@ -323,24 +324,68 @@ void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src
     CK(cudaGetLastError());
 }
 
+template <int M, class Coef, class Src>
+void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, OmegaSrc om,
+                      const double* g, double* out, double wd) {
+    constexpr int H = (M + 1) & ~1;
+    constexpr int OUTW = 2 * kTW - 2 * H;
+    constexpr int PF = sizeof(typename Src::Raw) > 32 ? 2 : 3;
+    const int seg = seg_rows(L.nx, L.ny);
+    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.ny + seg - 1) / seg);
+    k_smooth2<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
+    CK(cudaGetLastError());
+}
+
+template <int M, int SK, class Coef>
+void launch_smooth3_t(gmg_problem* p, const Lev& L, const Coef& A, const double* u, const double* uc,
+                      OmegaSrc om, const double* g, double* out, double wd) {
+    constexpr int D = 6;
+    constexpr int H = (M + 1) & ~1;
+    constexpr int OUTW = 2 * kTW - 2 * H;
+    using SM = Smooth3Smem<M, kTW, D, SK, Coef>;
+    static bool attr = false;
+    if (!attr) {
+        set_smem(k_smooth3<M, kTW, D, SK, Coef>, sizeof(SM));
+        attr = true;
+    }
+    Prolong P{};
+    if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
+    const int seg = seg_rows(L.nx, L.ny);
+    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.ny + seg - 1) / seg);
+    k_smooth3<M, kTW, D, SK, Coef><<<grid, kTW, sizeof(SM), p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
+    CK(cudaGetLastError());
+}
+
+// levels at least this wide stream their inputs through the cp.async ring (k_smooth3)
+constexpr int kRingMinNx = 255;
+
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
                        double* out, double wd) {
+    if (L.nx >= kRingMinNx) {
+        switch (s.kind) {
+            case S_ZERO: launch_smooth3_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
+            case S_U: launch_smooth3_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
+            case S_PROLONG: launch_smooth3_t<M, K3_PROLONG>(p, L, A, nullptr, s.uc, s.om, g, out, wd); return;
+            case S_CORRECT: launch_smooth3_t<M, K3_CORRECT>(p, L, A, s.u, s.uc, s.om, g, out, wd); return;
+            default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
+        }
+    }
     switch (s.kind) {
         case S_ZERO:
-            launch_smooth_t<M>(p, L, A, SrcZero{}, s.om, g, out, wd);
+            launch_smooth2_t<M>(p, L, A, Src2Zero{}, s.om, g, out, wd);
             break;
         case S_U:
-            launch_smooth_t<M>(p, L, A, SrcU{s.u, L.grid()}, s.om, g, out, wd);
+            launch_smooth2_t<M>(p, L, A, Src2U{s.u, L.grid()}, s.om, g, out, wd);
             break;
         case S_PROLONG: {
-            SrcProlong src{prolong_from(p, L.l - 1, s.uc), L.nx, L.ny, 0.0};
-            launch_smooth_t<M>(p, L, A, src, s.om, g, out, wd);
+            Src2Prolong src{prolong_from(p, L.l - 1, s.uc), L.nx, L.ny, 0.0};
+            launch_smooth2_t<M>(p, L, A, src, s.om, g, out, wd);
             break;
         }
         case S_CORRECT: {
-            SrcCorrect src{s.u, L.grid(), prolong_from(p, L.l - 1, s.uc), 0.0, 0.0};
-            launch_smooth_t<M>(p, L, A, src, s.om, g, out, wd);
+            Src2Correct src{s.u, L.grid(), prolong_from(p, L.l - 1, s.uc), 0.0, 0.0};
+            launch_smooth2_t<M>(p, L, A, src, s.om, g, out, wd);
             break;
         }
         default:
