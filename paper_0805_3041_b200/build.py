@@ -40,7 +40,7 @@ def _newer(target: str, sources) -> bool:
 
 def _run(cmd, log):
     r = subprocess.run(cmd, capture_output=True, text=True)
-    with open(log, "a") as f:
+    with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr + "\n")
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -58,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _newer(o, [s, *deps]):
             if verbose:
                 print("nvcc", src, flush=True)
-            _run([NVCC, *NVFLAGS, "-c", s, "-o", o], log)
+            _run([NVCC, *NVFLAGS, "-c", s, "-o", o], o + ".log")
         objs.append(o)
     for src in SOURCES_CPP:
         s = os.path.join(CSRC, src)
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _newer(o, [s, *deps]):
             if verbose:
                 print("g++", src, flush=True)
-            _run(["g++", *CXXFLAGS, "-c", s, "-o", o], log)
+            _run(["g++", *CXXFLAGS, "-c", s, "-o", o], o + ".log")
         objs.append(o)
     if force or _newer(LIB, objs):
         _run([NVCC, "-shared", *ARCH, "-Xcompiler", "-fPIC", *objs, "-o", LIB], log)

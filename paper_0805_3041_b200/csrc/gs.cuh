@@ -20,7 +20,8 @@
 //   * All CTAs are co-resident (grid <= 148 CTAs of kGsWarps warps), so the
 //     spin-waits on predecessors always make progress.
 // The critical path per anti-diagonal is one division by c (a multiplication
-// when c is a power of two) + two multiply-subtracts + one shuffle.
+// when c is a power of two) + two multiply-subtracts + one shuffle. The same
+// kernel runs ILU(0)'s two triangular solves (policies below).
 #pragma once
 
 #include "common.cuh"
@@ -53,11 +54,60 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// dynamic smem: kGsWarps * 2 * 32 * kGsStride doubles
+// The recurrence a wave solves, z_k = finish(rhs_k - a1_k*z_left - a2_k*z_up):
+//   Gauss-Seidel/SOR   a1 = om*w, a2 = om*s, finish = /c        (smoother.cpp:297-309)
+//   ILU(0) forward     a1 = lw,   a2 = ls,   finish = identity  (smoother.cpp:318-325)
+//   ILU(0) backward    reversed order, a1 = e, a2 = n, finish = /d (smoother.cpp:326-334)
+// A policy gives a1/a2/finish at physical (i, j). REV runs the wave from the
+// last node backwards (logical (i, j) = physical (nx-1-i, ny-1-j)); UPDATE
+// writes x - damp*z, otherwise z itself.
 template <class Coef>
-__global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Coef A, const double* __restrict__ d,
+struct GsPolicy {
+    static constexpr bool REV = false, UPDATE = true;
+    Coef A;
+    double om;
+    __device__ __forceinline__ void coefs(int i, int j, double& a1, double& a2) const {
+        double C, Wc, E, S, N;
+        A.load(i, j, C, Wc, E, S, N);
+        a1 = om * Wc;
+        a2 = om * S;
+    }
+    __device__ __forceinline__ double finish(double acc, int i, int j) const { return A.div_by_c(acc, i, j); }
+};
+
+struct IluFwdPolicy {
+    static constexpr bool REV = false, UPDATE = false;
+    const double *lw, *ls;
+    long long pitch;
+    __device__ __forceinline__ void coefs(int i, int j, double& a1, double& a2) const {
+        a1 = __ldg(lw + (long long)j * pitch + i);
+        a2 = __ldg(ls + (long long)j * pitch + i);
+    }
+    __device__ __forceinline__ double finish(double acc, int, int) const { return acc; }
+};
+
+template <class Coef>
+struct IluBwdPolicy {
+    static constexpr bool REV = true, UPDATE = true;
+    Coef A;
+    const double* dp;
+    long long pitch;
+    __device__ __forceinline__ void coefs(int i, int j, double& a1, double& a2) const {
+        double C, Wc, E, S, N;
+        A.load(i, j, C, Wc, E, S, N);
+        a1 = E;
+        a2 = N;
+    }
+    __device__ __forceinline__ double finish(double acc, int i, int j) const {
+        return acc / __ldg(dp + (long long)j * pitch + i);
+    }
+};
+
+// dynamic smem: kGsWarps * 2 * 32 * kGsStride doubles
+template <class Pol>
+__global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, const double* __restrict__ d,
                                                            const double* __restrict__ x, double* __restrict__ xo,
-                                                           double om, double damp, double* __restrict__ gedge,
+                                                           double damp, double* __restrict__ gedge,
                                                            int* __restrict__ gprog) {
     extern __shared__ double stg[];
     __shared__ double ring[kGsWarps][kGsRing];
@@ -89,9 +139,10 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Coef A, const
         if (col < nx) {
             const int slot = (b % kGsSlots) * kGsBlk + lane;
             for (int rr = 0; rr < rows; ++rr) {
-                const long long k = g.at(col, W * 32 + rr);
+                const int jr = W * 32 + rr;
+                const long long k = Pol::REV ? g.at(nx - 1 - col, g.ny - 1 - jr) : g.at(col, jr);
                 cp_async8(sd + rr * kGsStride + slot, d + k);
-                cp_async8(sx + rr * kGsStride + slot, x + k);
+                if (Pol::UPDATE) cp_async8(sx + rr * kGsStride + slot, x + k);
             }
         }
         cp_commit();
@@ -142,14 +193,19 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Coef A, const
         if (row_ok && i >= 0 && i < nx) {
             const int slot = ((i / kGsBlk) % kGsSlots) * kGsBlk + (i & (kGsBlk - 1));
             const double dk = sd[lane * kGsStride + slot];
-            const double xk = sx[lane * kGsStride + slot];
-            double C, Wc, E, S, N;
-            A.load(i, j, C, Wc, E, S, N);
+            const int pi = Pol::REV ? nx - 1 - i : i, pj = Pol::REV ? g.ny - 1 - j : j;
+            double a1, a2;
+            pol.coefs(pi, pj, a1, a2);
             double acc = dk;
-            if (i > 0) acc = acc - om * Wc * zl;
-            if (j > 0) acc = acc - om * S * zup;
-            z = A.div_by_c(acc, i, j);
-            xo[g.at(i, j)] = xk - damp * z;
+            if (i > 0) acc = acc - a1 * zl;
+            if (j > 0) acc = acc - a2 * zup;
+            z = pol.finish(acc, pi, pj);
+            if (Pol::UPDATE) {
+                const double xk = sx[lane * kGsStride + slot];
+                xo[g.at(pi, pj)] = xk - damp * z;
+            } else {
+                xo[g.at(pi, pj)] = z;
+            }
             zl = z;
             if (lane == 31) {
                 if (to_ring) {

@@ -240,6 +240,30 @@ std::string check_nested(const Level& coarse, const Level& fine) {
 // threads and chunks, one record per break (+ the final record), replayed from
 // the exact state with literal re-sums of any record that fails validation.
 // stats: [0] chunks, [1] records, [2] literal re-sums, [3] breaks.
+void factor_ilu0(int nx, int ny, const double* c, const double* w, const double* e, const double* s,
+                 const double* n, double* lw, double* ls, double* d) {
+    // row-major sweep: the pivot of node k needs the pivots of its west and
+    // south neighbours, which the sweep has already produced
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            const std::size_t k = static_cast<std::size_t>(j) * nx + i;
+            double piv = c[k];
+            double a = 0.0, b = 0.0;
+            if (i > 0) {
+                a = w[k] / d[k - 1];
+                piv -= a * e[k - 1];
+            }
+            if (j > 0) {
+                b = s[k] / d[k - nx];
+                piv -= b * n[k - nx];
+            }
+            if (piv <= 0.0) throw std::runtime_error("ilu0 factorization: nonpositive pivot");
+            lw[k] = a;
+            ls[k] = b;
+            d[k] = piv;
+        }
+}
+
 double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* stats) {
     using namespace gmg_ss;
     const long long C = static_cast<long long>(T) * EPT;

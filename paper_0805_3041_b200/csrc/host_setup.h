@@ -44,6 +44,12 @@ void restrict_weights(const std::vector<double>& xf, const std::vector<double>& 
 // require_nested (transfer.cpp:10-22); returns an error message or "".
 std::string check_nested(const Level& coarse, const Level& fine);
 
+// factor_ilu0 (smoother.cpp:187-210) on the reference arrays: lw, ls, d
+// (nx*ny each; ue/un are the operator's e/n). Throws std::runtime_error
+// "ilu0 factorization: nonpositive pivot".
+void factor_ilu0(int nx, int ny, const double* c, const double* w, const double* e, const double* s,
+                 const double* n, double* lw, double* ls, double* d);
+
 // CPU emulation of the device exact-order summation engine.
 double seqsum_emulate(const double* terms, long long n, int threads, int ept, long long* stats);
 

@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "host_setup.h"
 #include "gs.cuh"
+#include "linesm.cuh"
 #include "march.cuh"
 #include "march2.cuh"
 #include "seqsum.cuh"
@@ -90,8 +91,23 @@ struct Lev {
     RestrictW rw{};                       // restriction weights (this level as coarse)
     double* wmem = nullptr;
     std::vector<double> hx, hy;
+    double* scr[2] = {nullptr, nullptr};  // smoother scratch (adi/gsadi/ilu0), allocated on demand
+    double* scrmem = nullptr;
     Grid grid() const { return Grid{nx, ny, pitch}; }
     long long n() const { return (long long)nx * ny; }
+};
+
+// Per-level device state of one SmootherSpec (gmg::setup, smoother.cpp:230-273).
+struct SmLev {
+    double* mem = nullptr;
+    LineFactors fx{}, fy{};                                    // factor_lines_x / _y
+    const double *lw = nullptr, *ls = nullptr, *dp = nullptr;  // factor_ilu0
+    double rich = 0.0;                                         // richardson_omega()
+};
+struct SmSetup {
+    int kind = 0;
+    double omega = 0.0;
+    std::vector<SmLev> lev;
 };
 
 }  // namespace
@@ -125,6 +141,8 @@ struct gmg_problem {
     int* status = nullptr;
     double* hostbuf = nullptr;  // pinned: {norm^2, status}
     std::map<std::string, std::array<cudaGraphExec_t, 2>> graphs;
+    std::map<std::pair<int, unsigned long long>, SmSetup> smsetups;  // (kind, omega bits)
+    double* linebuf = nullptr;  // k_gstri scratch: 2 x max(nx, ny)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     Lev& lev(int l) { return lv.at(l - 1); }
 };
@@ -485,33 +503,127 @@ void launch_defect_src(gmg_problem* p, const Lev& L, const SmoothSrc& s, const d
     });
 }
 
-// One lexicographic Gauss-Seidel/SOR smooth_step: x' = x - damp * (D + om L)^{-1} (A x - g).
-void launch_gs_wave(gmg_problem* p, const Lev& L, const double* d, const double* x, double* xo, double om,
-                    double damp) {
+// One wavefront pass of policy `pol` (gs.cuh) over level L.
+template <class Pol>
+void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, const double* x, double* xo,
+                 double damp) {
     const int warps = (L.ny + 31) / 32;
     if (warps > p->gs_warps) throw GmgError{GMG_ERR_LOGIC, "gs: workspace too small"};
     const int blocks = (warps + kGsWarps - 1) / kGsWarps;
     if (blocks > 148) throw GmgError{GMG_ERR_UNSUPPORTED, "gs: more rows than one co-resident wavefront"};
     CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
+    static bool attr = false;
+    if (!attr) {
+        set_smem(k_gs_wave<Pol>, gs_smem());
+        attr = true;
+    }
+    k_gs_wave<Pol><<<blocks, kGsWarps * 32, gs_smem(), p->st>>>(L.grid(), pol, d, x, xo, damp, p->gs_edge,
+                                                                 p->gs_prog);
+    CK(cudaGetLastError());
+}
+
+// One lexicographic Gauss-Seidel/SOR smooth_step: x' = x - damp * (D + om L)^{-1} (A x - g).
+void launch_gs_wave(gmg_problem* p, const Lev& L, const double* d, const double* x, double* xo, double om,
+                    double damp) {
     with_coef(L, [&](const auto& A) {
         using C = std::decay_t<decltype(A)>;
-        static bool attr = false;
-        if (!attr) {
-            set_smem(k_gs_wave<C>, gs_smem());
-            attr = true;
-        }
-        k_gs_wave<<<blocks, kGsWarps * 32, gs_smem(), p->st>>>(L.grid(), A, d, x, xo, om, damp, p->gs_edge,
-                                                                p->gs_prog);
+        launch_wave(p, L, GsPolicy<C>{A, om}, d, x, xo, damp);
+    });
+}
+
+bool uses_x_lines(int k) {
+    return k == GMG_SMOOTHER_TRI_X || k == GMG_SMOOTHER_ADI || k == GMG_SMOOTHER_GSTRI_X || k == GMG_SMOOTHER_GSADI;
+}
+bool uses_y_lines(int k) {
+    return k == GMG_SMOOTHER_TRI_Y || k == GMG_SMOOTHER_ADI || k == GMG_SMOOTHER_GSTRI_Y || k == GMG_SMOOTHER_GSADI;
+}
+
+template <int DIR, int MODE>
+void launch_line(gmg_problem* p, const Lev& L, const LineFactors& f, const double* rhs, double* ybuf,
+                 const double* x, const double* z1, double* out, double damp) {
+    const int nl = DIR == 0 ? L.ny : L.nx;
+    k_line<DIR, MODE><<<(nl + kLineT - 1) / kLineT, kLineT, 0, p->st>>>(L.grid(), f, rhs, ybuf, x, z1, out, damp);
+    CK(cudaGetLastError());
+}
+
+template <int DIR, int MODE>
+void launch_gstri(gmg_problem* p, const Lev& L, double om, const LineFactors& f, const double* rhs,
+                  const double* x, const double* z1, double* out, double damp) {
+    const int nmax = std::max(p->lev(p->L).nx, p->lev(p->L).ny);
+    with_coef(L, [&](const auto& A) {
+        using C = std::decay_t<decltype(A)>;
+        k_gstri<DIR, MODE, C><<<1, 32, 0, p->st>>>(L.grid(), A, om, f, rhs, x, z1, out, p->linebuf,
+                                                   p->linebuf + nmax, damp);
     });
     CK(cudaGetLastError());
 }
 
-// `steps` Gauss-Seidel smoothing steps from source s (a non-u start is
+// One smooth_step (smoother.cpp:389-399) of a non-Jacobi kind, given the
+// defect d = A x - g (in DD, which it may overwrite): out = x - damp*C^{-1} d
+// with C^{-1} applied as in apply_preconditioner (smoother.cpp:275-386).
+void pc_apply(gmg_problem* p, const Lev& L, const gmg_cycle_desc& sp, const SmLev* m, double* d,
+              const double* x, double* out) {
+    const double damp = sp.smoothing_omega, om = sp.smoother_omega;
+    switch (sp.smoother_kind) {
+        case GMG_SMOOTHER_GAUSS_SEIDEL:
+        case GMG_SMOOTHER_SOR:
+            launch_gs_wave(p, L, d, x, out, om, damp);
+            return;
+        case GMG_SMOOTHER_RICHARDSON: {
+            dim3 gr((L.nx + 127) / 128, L.ny);
+            k_rich_update<<<gr, 128, 0, p->st>>>(L.grid(), d, x, out, m->rich, damp);
+            CK(cudaGetLastError());
+            return;
+        }
+        case GMG_SMOOTHER_ILU0:
+            launch_wave(p, L, IluFwdPolicy{m->lw, m->ls, L.pitch}, d, nullptr, L.scr[0], damp);
+            with_coef(L, [&](const auto& A) {
+                using C = std::decay_t<decltype(A)>;
+                launch_wave(p, L, IluBwdPolicy<C>{A, m->dp, L.pitch}, L.scr[0], x, out, damp);
+            });
+            return;
+        case GMG_SMOOTHER_TRI_X:
+            launch_line<0, LO_UPDATE>(p, L, m->fx, d, d, x, nullptr, out, damp);
+            return;
+        case GMG_SMOOTHER_TRI_Y:
+            launch_line<1, LO_UPDATE>(p, L, m->fy, d, d, x, nullptr, out, damp);
+            return;
+        case GMG_SMOOTHER_ADI:
+        case GMG_SMOOTHER_GSADI: {
+            // z1 = C_x^{-1} d; t = d - A z1; z = z1 + C_y^{-1} t (smoother.cpp:351-361, 375-384)
+            double* z1 = L.scr[0];
+            double* t = L.scr[1];
+            const bool gs = sp.smoother_kind == GMG_SMOOTHER_GSADI;
+            if (gs)
+                launch_gstri<0, LO_Z>(p, L, om, m->fx, d, nullptr, nullptr, z1, damp);
+            else
+                launch_line<0, LO_Z>(p, L, m->fx, d, t, nullptr, nullptr, z1, damp);
+            with_coef(L, [&](const auto& A) {
+                launch_resid_t(p, L, A, SrcU{z1, L.grid()}, d, t, nullptr, nullptr);
+            });
+            if (gs)
+                launch_gstri<1, LO_SUM_UPDATE>(p, L, om, m->fy, t, x, z1, out, damp);
+            else
+                launch_line<1, LO_SUM_UPDATE>(p, L, m->fy, t, t, x, z1, out, damp);
+            return;
+        }
+        case GMG_SMOOTHER_GSTRI_X:
+            launch_gstri<0, LO_UPDATE>(p, L, om, m->fx, d, x, nullptr, out, damp);
+            return;
+        case GMG_SMOOTHER_GSTRI_Y:
+            launch_gstri<1, LO_UPDATE>(p, L, om, m->fy, d, x, nullptr, out, damp);
+            return;
+        default:
+            throw GmgError{GMG_ERR_LOGIC, "smooth: kind has no preconditioner kernel"};
+    }
+}
+
+// `steps` smooth_steps of a non-Jacobi kind from source s (a non-u start is
 // materialised in bufA; outputs then alternate). Uses DD as defect scratch.
-double* gs_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const double* g, double* bufA,
-                 double* bufB, double om, double damp) {
+double* pc_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const double* g, double* bufA,
+                 double* bufB, const gmg_cycle_desc& sp, const SmLev* m) {
     if (steps == 0) {
-        launch_smooth(p, L, 0, s, g, bufA, damp);
+        launch_smooth(p, L, 0, s, g, bufA, sp.smoothing_omega);
         return bufA;
     }
     double* d = L.buf[DD];
@@ -527,7 +639,7 @@ double* gs_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const dou
         out = bufB;
     }
     for (int k = 0; k < steps; ++k) {
-        launch_gs_wave(p, L, d, x, out, om, damp);
+        pc_apply(p, L, sp, m, d, x, out);
         if (k + 1 == steps) break;
         SmoothSrc n;
         n.kind = S_U;
@@ -579,12 +691,12 @@ void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc,
 struct Driver {
     gmg_problem* p;
     gmg_cycle_desc sp;
+    const SmSetup* sm = nullptr;  // setup_smoothers products (null for jacobi / GS / SOR)
 
     // smooth_step x `steps` with the configured preconditioner (setup_smoothers)
     double* smooth(const Lev& L, int steps, const SmoothSrc& s, const double* g, double* a, double* b) {
-        if (sp.smoother_kind == GMG_SMOOTHER_GAUSS_SEIDEL || sp.smoother_kind == GMG_SMOOTHER_SOR)
-            return gs_steps(p, L, steps, s, g, a, b, sp.smoother_omega, sp.smoothing_omega);
-        return smooth_steps(p, L, steps, s, g, a, b, sp.smoothing_omega);
+        if (sp.smoother_kind == GMG_SMOOTHER_JACOBI) return smooth_steps(p, L, steps, s, g, a, b, sp.smoothing_omega);
+        return pc_steps(p, L, steps, s, g, a, b, sp, sm ? &sm->lev[L.l - 1] : nullptr);
     }
 
     // gmg::mg_cycle (cycle.cpp:69-100) on level l from start s with rhs g.
@@ -674,6 +786,8 @@ std::string spec_key(const gmg_cycle_desc& s) {
     return buf;
 }
 
+const SmSetup* find_smoother(gmg_problem* p, const gmg_cycle_desc& sp);
+
 std::array<cudaGraphExec_t, 2>& get_graphs(gmg_problem* p, const gmg_cycle_desc& sp) {
     const std::string key = spec_key(sp);
     auto it = p->graphs.find(key);
@@ -683,7 +797,7 @@ std::array<cudaGraphExec_t, 2>& get_graphs(gmg_problem* p, const gmg_cycle_desc&
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(p->st, cudaStreamCaptureModeThreadLocal));
         try {
-            Driver d{p, sp};
+            Driver d{p, sp, find_smoother(p, sp)};
             d.cycle(p->X[par], p->X[1 - par]);
         } catch (...) {
             cudaStreamEndCapture(p->st, &g);
@@ -723,9 +837,6 @@ void check_smoother(const gmg_cycle_desc& sp) {
         default:
             throw std::invalid_argument("smoother: unknown kind");
     }
-    if (sp.smoother_kind != GMG_SMOOTHER_JACOBI && sp.smoother_kind != GMG_SMOOTHER_GAUSS_SEIDEL &&
-        sp.smoother_kind != GMG_SMOOTHER_SOR)
-        throw GmgError{GMG_ERR_UNSUPPORTED, "smoother kind not implemented on the device yet"};
 }
 
 // checks the reference performs inside mg_cycle / smooth_step (cycle.cpp:75-76, smoother.cpp:391)
@@ -759,11 +870,162 @@ int fetch_status(gmg_problem* p) {
     return s;
 }
 
+// The reference's five operator arrays of a level (c, w, e, s, n), rebuilt
+// from the device classes: CONST/ROWX with their exact zeros toward the
+// boundary, FIELD downloaded.
+void host_coefs(gmg_problem* p, const Lev& L, std::vector<double> (&a)[5]) {
+    const size_t N = (size_t)L.n();
+    for (auto& v : a) v.assign(N, 0.0);
+    if (L.kind == 2) {
+        for (int q = 0; q < 5; ++q)
+            download(p, L, a[q].data(), L.coefmem + q * L.elems + L.off0, cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+        return;
+    }
+    std::vector<double> row[5];
+    if (L.kind == 1) {
+        for (int q = 0; q < 5; ++q) {
+            row[q].resize(L.nx);
+            CK(cudaMemcpy(row[q].data(), L.coefmem + q * L.nx, L.nx * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+    } else {
+        const double v[5] = {L.cconst.c, L.cconst.w, L.cconst.e, L.cconst.s, L.cconst.n};
+        for (int q = 0; q < 5; ++q) row[q].assign(L.nx, v[q]);
+    }
+    for (int j = 0; j < L.ny; ++j)
+        for (int i = 0; i < L.nx; ++i) {
+            const size_t k = (size_t)j * L.nx + i;
+            a[0][k] = row[0][i];
+            a[1][k] = (L.kind == 1 || i > 0) ? row[1][i] : 0.0;
+            a[2][k] = (L.kind == 1 || i + 1 < L.nx) ? row[2][i] : 0.0;
+            a[3][k] = j > 0 ? row[3][i] : 0.0;
+            a[4][k] = j + 1 < L.ny ? row[4][i] : 0.0;
+        }
+}
+
+void ensure_scratch(gmg_problem* p, Lev& L) {
+    if (L.scrmem) return;
+    CK(cudaMalloc(&L.scrmem, 2 * L.elems * sizeof(double)));
+    CK(cudaMemsetAsync(L.scrmem, 0, 2 * L.elems * sizeof(double), p->st));
+    L.scr[0] = L.scrmem + L.off0;
+    L.scr[1] = L.scrmem + L.elems + L.off0;
+}
+
+// richardson setup (smoother.cpp:240-251): power_apply_A(op, 20) (:212-227)
+// from mt19937(0x2d5a11) uniform(-1,1), exact-order norms, then the clamp.
+double richardson_omega(gmg_problem* p, Lev& L, double omega) {
+    std::vector<double> x0((size_t)L.n());
+    std::mt19937 rng(0x2d5a11u);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    for (double& v : x0) v = dist(rng);
+    double* xa = L.buf[U0];
+    double* ya = L.buf[U1];
+    upload(p, L, xa, x0.data(), cudaMemcpyHostToDevice);
+    double lambda = 0.0;
+    for (int t = 0; t < 20; ++t) {
+        with_coef(L, [&](const auto& A) {
+            dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
+            k_apply_simple<<<gr, b, 0, p->st>>>(L.grid(), A, xa, ya);
+        });
+        CK(cudaGetLastError());
+        norm_sum(p, L, ya, p->sums + 3, GMG_REDUCE_EXACT);
+        lambda = std::sqrt(fetch_scalar(p, p->sums + 3));
+        if (lambda == 0.0) break;
+        k_div_scalar<<<dim3((L.nx + 127) / 128, L.ny), 128, 0, p->st>>>(L.grid(), ya, lambda);
+        CK(cudaGetLastError());
+        std::swap(xa, ya);
+    }
+    if (lambda > 0.0 && omega > 1.0 / lambda) return 0.9 / lambda;
+    return omega;
+}
+
+unsigned long long dbits(double v) {
+    unsigned long long b;
+    std::memcpy(&b, &v, sizeof b);
+    return b;
+}
+
+// setup_smoothers (cycle.cpp:32-38): every level, in level order, with the
+// reference's error messages. Cached per (kind, omega); null for the kinds
+// without setup products (jacobi, gauss_seidel, sor).
+const SmSetup* ensure_smoother(gmg_problem* p, int kind, double omega) {
+    if (kind == GMG_SMOOTHER_JACOBI || kind == GMG_SMOOTHER_GAUSS_SEIDEL || kind == GMG_SMOOTHER_SOR) return nullptr;
+    const auto key = std::make_pair(kind, dbits(omega));
+    auto it = p->smsetups.find(key);
+    if (it != p->smsetups.end()) return &it->second;
+    SmSetup S;
+    S.kind = kind;
+    S.omega = omega;
+    S.lev.resize(p->L);
+    try {
+        for (int l = 1; l <= p->L; ++l) {
+            Lev& L = p->lev(l);
+            SmLev& m = S.lev[l - 1];
+            if (kind == GMG_SMOOTHER_RICHARDSON) {
+                m.rich = richardson_omega(p, L, omega);
+            } else if (kind == GMG_SMOOTHER_ILU0) {
+                std::vector<double> a[5];
+                host_coefs(p, L, a);
+                const size_t N = (size_t)L.n();
+                std::vector<double> lw(N), ls(N), dp(N);
+                gmg_host::factor_ilu0(L.nx, L.ny, a[0].data(), a[1].data(), a[2].data(), a[3].data(), a[4].data(),
+                                      lw.data(), ls.data(), dp.data());
+                CK(cudaMalloc(&m.mem, 3 * L.elems * sizeof(double)));
+                CK(cudaMemsetAsync(m.mem, 0, 3 * L.elems * sizeof(double), p->st));
+                double* q[3] = {m.mem + L.off0, m.mem + L.elems + L.off0, m.mem + 2 * L.elems + L.off0};
+                upload(p, L, q[0], lw.data(), cudaMemcpyHostToDevice);
+                upload(p, L, q[1], ls.data(), cudaMemcpyHostToDevice);
+                upload(p, L, q[2], dp.data(), cudaMemcpyHostToDevice);
+                CK(cudaStreamSynchronize(p->st));
+                m.lw = q[0];
+                m.ls = q[1];
+                m.dp = q[2];
+                ensure_scratch(p, L);
+            } else {
+                const bool fx = uses_x_lines(kind), fy = uses_y_lines(kind);
+                const int nset = (int)fx + (int)fy;
+                CK(cudaMalloc(&m.mem, 3 * nset * L.elems * sizeof(double)));
+                CK(cudaMemsetAsync(m.mem, 0, 3 * nset * L.elems * sizeof(double), p->st));
+                CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+                double* base = m.mem + L.off0;
+                with_coef(L, [&](const auto& A) {
+                    if (fx) {
+                        m.fx = LineFactors{base, base + L.elems, base + 2 * L.elems};
+                        k_tri_factor<0><<<(L.ny + 127) / 128, 128, 0, p->st>>>(
+                            L.grid(), A, omega, base, base + L.elems, base + 2 * L.elems, p->status);
+                        base += 3 * L.elems;
+                    }
+                    if (fy) {
+                        m.fy = LineFactors{base, base + L.elems, base + 2 * L.elems};
+                        k_tri_factor<1><<<(L.nx + 127) / 128, 128, 0, p->st>>>(
+                            L.grid(), A, omega, base, base + L.elems, base + 2 * L.elems, p->status);
+                    }
+                });
+                CK(cudaGetLastError());
+                if (fetch_status(p) == 4) {
+                    CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+                    throw std::runtime_error("tri factorization: zero pivot");
+                }
+                if (kind == GMG_SMOOTHER_ADI || kind == GMG_SMOOTHER_GSADI) ensure_scratch(p, L);
+            }
+        }
+    } catch (...) {
+        for (auto& m : S.lev) cudaFree(m.mem);
+        throw;
+    }
+    return &p->smsetups.emplace(key, std::move(S)).first->second;
+}
+
+const SmSetup* find_smoother(gmg_problem* p, const gmg_cycle_desc& sp) {
+    return ensure_smoother(p, sp.smoother_kind, sp.smoother_omega);
+}
+
 // gmg::solve (cycle.cpp:146-194). b, x in device layout already (B, X[0]).
 void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep, int* final_par) {
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     check_smoother(sp);
+    ensure_smoother(p, sp.smoother_kind, sp.smoother_omega);
     const int L = p->L;
     Lev& F = p->lev(L);
     CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
@@ -821,7 +1083,11 @@ void free_problem(gmg_problem* p) {
     for (auto& kv : p->graphs)
         for (auto g : kv.second)
             if (g) cudaGraphExecDestroy(g);
+    for (auto& kv : p->smsetups)
+        for (auto& m : kv.second.lev) cudaFree(m.mem);
+    cudaFree(p->linebuf);
     for (auto& L : p->lv) {
+        cudaFree(L.scrmem);
         cudaFree(L.mem);
         cudaFree(L.coefmem);
         cudaFree(L.wmem);
@@ -998,6 +1264,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         p->gs_warps = (maxny + 31) / 32;
         CK(cudaMalloc(&p->gs_edge, (size_t)p->gs_warps * maxnx * sizeof(double)));
         CK(cudaMalloc(&p->gs_prog, p->gs_warps * sizeof(int)));
+        CK(cudaMalloc(&p->linebuf, 2 * (size_t)std::max(maxnx, maxny) * sizeof(double)));
         CK(cudaMemset(p->ss_stats, 0, 16 * sizeof(unsigned long long)));
         CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
@@ -1105,13 +1372,14 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "mg_cycle");
         check_smoother(*spec);
+        const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
         check_cycle(p, *spec);
         Lev& L = p->lev(level);
         // stage u0 in X-side scratch: use DD for g and DCAS for u0 of this level
         upload(p, L, L.buf[DCAS], u0, cudaMemcpyHostToDevice);
         upload(p, L, L.buf[GRHS], g, cudaMemcpyHostToDevice);
         CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
-        Driver d{p, *spec};
+        Driver d{p, *spec, sm};
         SmoothSrc s;
         s.kind = S_U;
         s.u = L.buf[DCAS];
@@ -1166,18 +1434,20 @@ int gmg_dev_smooth_step(gmg_problem* p, int level, int kind, double somega, doub
         sp.smoother_kind = kind;
         sp.smoother_omega = somega;
         check_smoother(sp);
+        const SmSetup* sm = ensure_smoother(p, kind, somega);
         if (!(omega_damp > 0.0)) throw std::invalid_argument("omega: damping must be > 0");
         Lev& L = p->lev(level);
+        sp.smoothing_omega = omega_damp;
         upload(p, L, L.buf[U0], x, cudaMemcpyHostToDevice);
         upload(p, L, L.buf[GRHS], b, cudaMemcpyHostToDevice);
         SmoothSrc s;
         s.kind = S_U;
         s.u = L.buf[U0];
         double* r = L.buf[U1];
-        if (kind == GMG_SMOOTHER_GAUSS_SEIDEL || kind == GMG_SMOOTHER_SOR)
-            r = gs_steps(p, L, 1, s, L.buf[GRHS], L.buf[U1], L.buf[DCAS], somega, omega_damp);
-        else
+        if (kind == GMG_SMOOTHER_JACOBI)
             launch_smooth(p, L, 1, s, L.buf[GRHS], L.buf[U1], omega_damp);
+        else
+            r = pc_steps(p, L, 1, s, L.buf[GRHS], L.buf[U1], L.buf[DCAS], sp, sm ? &sm->lev[level - 1] : nullptr);
         download(p, L, out, r, cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
     });
@@ -1363,7 +1633,10 @@ int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out8) { 
         std::lock_guard<std::mutex> lk(p->mu);
         CK(cudaStreamSynchronize(p->st));
         CK(cudaMemcpy(out8, p->ss_stats, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-        if (reset) CK(cudaMemset(p->ss_stats, 0, 16 * sizeof(unsigned long long)));
+        if (reset) {
+            CK(cudaMemsetAsync(p->ss_stats, 0, 16 * sizeof(unsigned long long), p->st));
+            CK(cudaStreamSynchronize(p->st));
+        }
     });
 }
 
@@ -1372,10 +1645,11 @@ int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* 
         checked(p);
         std::lock_guard<std::mutex> lk(p->mu);
         check_smoother(*spec);
+        const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
         check_cycle(p, *spec);
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(p->st, cudaStreamCaptureModeThreadLocal));
-        Driver d{p, *spec};
+        Driver d{p, *spec, sm};
         d.cycle(p->X[0], p->X[1]);
         CK(cudaStreamEndCapture(p->st, &g));
         size_t nn = 0;
