@@ -522,6 +522,8 @@ template <class TG>
 __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out) {
     extern __shared__ unsigned char smraw[];
     gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
+    __shared__ longlong2 cD[32];  // per record of the current group: signed run steps (parity 0, 1)
+    __shared__ double2 cPB[32];   // break term (-0.0 if none), tie flag
     const int s = blockIdx.x;
     const SsState& S = sts.s[s];
     const int t = threadIdx.x;
@@ -543,46 +545,88 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
         const gmg_ss::Rec* A = buf + (b & 1) * kSsBatch;
         const int cnt = min(kSsBatch, total - b * kSsBatch);
         if (t < 32) {
-#pragma unroll 2
-            for (int q = 0; q < cnt; ++q) {
-                const gmg_ss::Rec& r = A[q];
+            // Speculate serially, validate in parallel. For 32 records at a time:
+            //  (1) each lane decodes one record into the state-independent operands of
+            //      its fast step: in a valid run the sum keeps its binade and sign, so
+            //      s + Q*u is the integer add bits + D on the representation (D = +-Q,
+            //      one value per tie parity), then the break's real add (+(-0.0), the
+            //      exact identity, for a record without a break);
+            //  (2) the warp applies the 32 fast steps in order (~7 instructions each,
+            //      the only serial dependence is on the sum's bits);
+            //  (3) each lane validates its record against the state it was applied to;
+            //      from the first failure on, results are discarded, that record is
+            //      re-summed exactly from the true state and speculation resumes.
+            const int lane = t;
+            int q0 = 0;
+            while (q0 < cnt) {
+                const int gn = min(32, cnt - q0);
+                const bool act = lane < gn;
+                const gmg_ss::Rec& r = A[q0 + (act ? lane : 0)];
                 const uint32_t meta = r.meta;
-                const long long kb = r.kb;
                 const bool brk = (meta >> 12) & 1u, lit = (meta >> 14) & 1u, ne = (meta >> 15) & 1u;
                 const uint64_t Er = meta & 0x7ffu;
                 const bool negr = (meta >> 11) & 1u, badr = (meta >> 13) & 1u;
-                const bool ties = r.Q[0] != r.Q[1] || r.mn[0] != r.mn[1] || r.mx[0] != r.mx[1];
-                const double pb = r.pb;
-                // critical path: the bits of the exact sum give E, the integer
-                // significand and its parity directly
-                const uint64_t bits = gmg_ss::dbits(sv);
-                const uint64_t E = (bits >> 52) & 0x7ffu;
-                const int v = (ties && (bits & 1u)) ? 1 : 0;
-                const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
-                const long long Qi = v ? r.Q[1] : r.Q[0], mni = v ? r.mn[1] : r.mn[0], mxi = v ? r.mx[1] : r.mx[0];
-                const bool neg = bits >> 63;
-                // |M| = mant; for a negative sum M + x ranges over -(mant - x)
-                const long long lo_v = neg ? mant - mxi : mant + mni;
-                const long long hi_v = neg ? mant - mni : mant + mxi;
-                const bool ok_run = E >= (uint64_t)gmg_ss::kEMin && E <= (uint64_t)gmg_ss::kEMax && E == Er &&
-                                    neg == negr && lo_v >= gmg_ss::kLo && hi_v <= gmg_ss::kHi;
-                const bool ok = !lit && !badr && (!ne || ok_run);
-                const double u = gmg_ss::bitsd((E - 52) << 52);
-                double s1 = ne ? sv + (double)Qi * u : sv;
-                if (!ok) {
-                    // re-walk this record's range exactly from the true state (the break
-                    // element, if any, is applied below; otherwise kb is inclusive)
-                    const long long k1 = min(brk ? kb : kb + 1, n);
-                    const long long c0 = clock64();
-                    // dense breaks (literal chunk): plain adds; a failed run: integer walk
-                    s1 = lit ? literal_sum(tg, s, sv, prev + 1, k1) : warp_walk(tg, s, sv, prev + 1, k1);
-                    cyc_lit += clock64() - c0;
-                    ++n_lit;
-                    n_litterms += k1 - (prev + 1);
+                const bool ties = (r.Q[0] != r.Q[1]) | (r.mn[0] != r.mn[1]) | (r.mx[0] != r.mx[1]);
+                const long long D0 = ne ? (negr ? -r.Q[0] : r.Q[0]) : 0;
+                const long long D1 = ne ? (negr ? -r.Q[1] : r.Q[1]) : 0;
+                const long long kbl = r.kb;
+                cD[lane] = make_longlong2(D0, D1);
+                cPB[lane] = make_double2(brk ? r.pb : -0.0, __longlong_as_double(ties ? 1ll : 0ll));
+                __syncwarp();
+                double x = sv, before = sv;
+#pragma unroll 4
+                for (int k = 0; k < gn; ++k) {
+                    if (lane == k) before = x;
+                    const longlong2 dd = cD[k];
+                    const double2 pt = cPB[k];
+                    const uint64_t bits = gmg_ss::dbits(x);
+                    const long long D = (bits & (uint64_t)__double_as_longlong(pt.y)) ? dd.y : dd.x;
+                    x = gmg_ss::bitsd(bits + (uint64_t)D) + pt.x;
                 }
-                sv = brk ? s1 + pb : s1;
-                n_brk += brk;
-                prev = kb;
+                // (3) validation of record lane against `before`
+                bool ok = true;
+                if (act) {
+                    const uint64_t bits = gmg_ss::dbits(before);
+                    const uint64_t E = (bits >> 52) & 0x7ffu;
+                    const bool v = ties && (bits & 1u);
+                    const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
+                    const long long mni = v ? r.mn[1] : r.mn[0], mxi = v ? r.mx[1] : r.mx[0];
+                    const bool neg = bits >> 63;
+                    const long long lo_v = neg ? mant - mxi : mant + mni;
+                    const long long hi_v = neg ? mant - mni : mant + mxi;
+                    const bool ok_run = E >= (uint64_t)gmg_ss::kEMin && E <= (uint64_t)gmg_ss::kEMax && E == Er &&
+                                        neg == negr && lo_v >= gmg_ss::kLo && hi_v <= gmg_ss::kHi;
+                    ok = !lit && !badr && (!ne || ok_run);
+                }
+                const unsigned fail = __ballot_sync(0xffffffffu, !ok);
+                const unsigned brkm = __ballot_sync(0xffffffffu, act && brk);
+                __syncwarp();
+                if (!fail) {
+                    sv = x;
+                    prev = __shfl_sync(0xffffffffu, kbl, gn - 1);
+                    n_brk += __popc(brkm);
+                    q0 += gn;
+                    continue;
+                }
+                const int f = __ffs(fail) - 1;
+                n_brk += __popc(brkm & ((2u << f) - 1u));
+                sv = __shfl_sync(0xffffffffu, before, f);
+                const long long pf = f > 0 ? __shfl_sync(0xffffffffu, kbl, f - 1) : prev;
+                const gmg_ss::Rec& rf = A[q0 + f];
+                const bool brk_f = (rf.meta >> 12) & 1u, lit_f = (rf.meta >> 14) & 1u;
+                const long long kb_f = rf.kb;
+                // re-walk the failed record's range exactly from the true state (the break
+                // element, if any, is applied below; otherwise kb is inclusive)
+                const long long k1 = min(brk_f ? kb_f : kb_f + 1, n);
+                const long long c0 = clock64();
+                // dense breaks (literal chunk): plain adds; a failed run: integer walk
+                const double s1 = lit_f ? literal_sum(tg, s, sv, pf + 1, k1) : warp_walk(tg, s, sv, pf + 1, k1);
+                cyc_lit += clock64() - c0;
+                ++n_lit;
+                n_litterms += k1 - (pf + 1);
+                sv = brk_f ? s1 + rf.pb : s1;
+                prev = kb_f;
+                q0 += f + 1;
             }
         } else if (b + 1 < nb) {
             gmg_ss::Rec* B = buf + ((b + 1) & 1) * kSsBatch;
@@ -604,6 +648,32 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
             atomicAdd(S.stats + 6, n_litterms);
             atomicAdd(S.stats + 7, (unsigned long long)((n + kSsC - 1) / kSsC));
         }
+    }
+}
+
+// Small sums (n <= kSsDirect): the reference's loop literally. The CTA stages
+// the terms in shared memory (coalesced, all loads in flight), then one thread
+// adds them left to right from s = 0.0 (stencil.cpp:9-26). One launch instead of
+// walk + chain: on the coarse levels the engine's phases are pure latency.
+constexpr int kSsDirect = 4096;
+template <class TG>
+__global__ void __launch_bounds__(256) k_ss_direct(TG tg, int n, double* __restrict__ out) {
+    extern __shared__ double tv[];
+    const int s = blockIdx.x;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) tv[k] = tg.term(s, k);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        int k = 0;
+        for (; k + 8 <= n; k += 8) {
+            double v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = tv[k + j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a = a + v[j];
+        }
+        for (; k < n; ++k) a = a + tv[k];
+        out[s] = a;
     }
 }
 

@@ -303,6 +303,11 @@ void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int mode) {
         CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
         return;
     }
+    if (mode == GMG_REDUCE_EXACT && n <= kSsDirect) {
+        k_ss_direct<TG><<<NS, 256, n * sizeof(double), p->st>>>(tg, (int)n, out);
+        CK(cudaGetLastError());
+        return;
+    }
     if (mode == GMG_REDUCE_FAST) {
         k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
         k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out);
