@@ -277,7 +277,7 @@ __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 // ---- walk ---------------------------------------------------------------------
 // grid (nch, NS); block kSsT; dynamic smem (kSsC + kSsC/32) doubles.
 template <class TG>
-__global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
+__global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
     extern __shared__ double tm[];
     __shared__ double swd[8];
     __shared__ SegF sws[8];
@@ -439,24 +439,42 @@ __global__ void __launch_bounds__(kSsT, 2) k_ss_walk(TG tg, long long n, int nch
 }
 
 // ---- chain --------------------------------------------------------------------
-// Literal left-to-right adds over terms [k0, k1) of sum s, by one warp: lanes
-// load 32 consecutive terms (next batch prefetched), lane 0's order of adds.
+// Both re-sum paths read terms through a register ring of kSsRing batches of 32
+// (lane = term within a batch), so ~kSsRing*256 B per warp are in flight and the
+// walk is not bound by one memory round trip per batch.
+constexpr int kSsRing = 8;
+
+// Literal left-to-right adds over terms [k0, k1) of sum s, by one warp: lane 0's
+// order of adds on shuffled terms (every lane computes the same chain).
 template <class TG>
 __device__ double literal_sum(const TG& tg, int s, double a, long long k0, long long k1) {
     const int lane = threadIdx.x & 31;
-    double nxt = (k0 + lane < k1) ? tg.term(s, k0 + lane) : 0.0;
-    long long k = k0;
-    for (; k + 32 <= k1; k += 32) {
-        const double cur = nxt;
-        nxt = (k + 32 + lane < k1) ? tg.term(s, k + 32 + lane) : 0.0;
-        double v[32];
+    double ring[kSsRing];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __shfl_sync(0xffffffffu, cur, j);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) a = a + v[j];
+    for (int r = 0; r < kSsRing; ++r) {
+        const long long k = k0 + r * 32 + lane;
+        ring[r] = k < k1 ? tg.term(s, k) : 0.0;
     }
-    const int m = (int)(k1 - k);
-    for (int j = 0; j < m; ++j) a = a + __shfl_sync(0xffffffffu, nxt, j);
+    for (long long k = k0; k < k1; k += 32 * kSsRing) {
+#pragma unroll
+        for (int r = 0; r < kSsRing; ++r) {
+            const long long kb = k + r * 32;
+            if (kb >= k1) break;
+            const double cur = ring[r];
+            const long long kn = kb + 32 * kSsRing + lane;
+            ring[r] = kn < k1 ? tg.term(s, kn) : 0.0;
+            const int m = (int)min(32LL, k1 - kb);
+            if (m == 32) {
+                double v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __shfl_sync(0xffffffffu, cur, j);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) a = a + v[j];
+            } else {
+                for (int j = 0; j < m; ++j) a = a + __shfl_sync(0xffffffffu, cur, j);
+            }
+        }
+    }
     return __shfl_sync(0xffffffffu, a, 0);
 }
 
@@ -469,47 +487,58 @@ template <class TG>
 __device__ double warp_walk(const TG& tg, int s, double sv, long long k0, long long k1) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
-    double nxt = (k0 + lane < k1) ? tg.term(s, k0 + lane) : 0.0;
-    for (long long k = k0; k < k1; k += 32) {
-        const double p = nxt;
-        nxt = (k + 32 + lane < k1) ? tg.term(s, k + 32 + lane) : 0.0;
-        const int m = (int)min(32LL, k1 - k);
-        int start = 0;
-        while (start < m) {
-            const uint64_t bits = gmg_ss::dbits(sv);
-            const int E = (int)((bits >> 52) & 0x7ff);
-            if (E < gmg_ss::kEMin || E > gmg_ss::kEMax) {  // zero/subnormal/huge: one real add
-                sv = sv + __shfl_sync(full, p, start);
-                ++start;
-                continue;
-            }
-            const double inv_u = gmg_ss::bitsd((uint64_t)(2098 - E) << 52);
-            const bool mine = lane >= start && lane < m;
-            const double xv = p * inv_u;
-            const double fl = floor(xv);
-            const double fr = xv - fl;
-            const bool bad = !(xv < gmg_ss::kTwo52 && xv > -gmg_ss::kTwo52) || fr == 0.5;
-            long long q = (mine && !bad) ? (long long)fl + (fr > 0.5 ? 1 : 0) : 0;
+    double ring[kSsRing];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const long long y = __shfl_up_sync(full, q, o);
-                if (lane >= o) q += y;
-            }
-            const bool neg = bits >> 63;
-            const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
-            const long long Mn = neg ? mant - q : mant + q;  // |M| after this lane
-            const bool ok = !bad && Mn >= gmg_ss::kLo && Mn <= gmg_ss::kHi;
-            const unsigned failm = __ballot_sync(full, mine && !ok);
-            const int f = failm ? __ffs(failm) - 1 : m;
-            if (f > start) {
-                const long long P = __shfl_sync(full, q, f - 1);
-                sv = gmg_ss::compose(neg ? -(mant - P) : mant + P, E);  // signed M + P
-            }
-            if (f < m) {
-                sv = sv + __shfl_sync(full, p, f);
-                start = f + 1;
-            } else {
-                start = m;
+    for (int r = 0; r < kSsRing; ++r) {
+        const long long k = k0 + r * 32 + lane;
+        ring[r] = k < k1 ? tg.term(s, k) : 0.0;
+    }
+    for (long long kr = k0; kr < k1; kr += 32 * kSsRing) {
+#pragma unroll
+        for (int r = 0; r < kSsRing; ++r) {
+            const long long k = kr + r * 32;
+            if (k >= k1) break;
+            const double p = ring[r];
+            const long long kn = k + 32 * kSsRing + lane;
+            ring[r] = kn < k1 ? tg.term(s, kn) : 0.0;
+            const int m = (int)min(32LL, k1 - k);
+            int start = 0;
+            while (start < m) {
+                const uint64_t bits = gmg_ss::dbits(sv);
+                const int E = (int)((bits >> 52) & 0x7ff);
+                if (E < gmg_ss::kEMin || E > gmg_ss::kEMax) {  // zero/subnormal/huge: one real add
+                    sv = sv + __shfl_sync(full, p, start);
+                    ++start;
+                    continue;
+                }
+                const double inv_u = gmg_ss::bitsd((uint64_t)(2098 - E) << 52);
+                const bool mine = lane >= start && lane < m;
+                const double xv = p * inv_u;
+                const double fl = floor(xv);
+                const double fr = xv - fl;
+                const bool bad = !(xv < gmg_ss::kTwo52 && xv > -gmg_ss::kTwo52) || fr == 0.5;
+                long long q = (mine && !bad) ? (long long)fl + (fr > 0.5 ? 1 : 0) : 0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long y = __shfl_up_sync(full, q, o);
+                    if (lane >= o) q += y;
+                }
+                const bool neg = bits >> 63;
+                const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
+                const long long Mn = neg ? mant - q : mant + q;  // |M| after this lane
+                const bool ok = !bad && Mn >= gmg_ss::kLo && Mn <= gmg_ss::kHi;
+                const unsigned failm = __ballot_sync(full, mine && !ok);
+                const int f = failm ? __ffs(failm) - 1 : m;
+                if (f > start) {
+                    const long long P = __shfl_sync(full, q, f - 1);
+                    sv = gmg_ss::compose(neg ? -(mant - P) : mant + P, E);  // signed M + P
+                }
+                if (f < m) {
+                    sv = sv + __shfl_sync(full, p, f);
+                    start = f + 1;
+                } else {
+                    start = m;
+                }
             }
         }
     }
@@ -619,8 +648,11 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
                 // element, if any, is applied below; otherwise kb is inclusive)
                 const long long k1 = min(brk_f ? kb_f : kb_f + 1, n);
                 const long long c0 = clock64();
-                // dense breaks (literal chunk): plain adds; a failed run: integer walk
-                const double s1 = lit_f ? literal_sum(tg, s, sv, pf + 1, k1) : warp_walk(tg, s, sv, pf + 1, k1);
+                // plain left-to-right adds: a failed record sits where the sum crosses
+                // binades often, and there the literal chain (~6 cycles/term) beats the
+                // warp's integer walk, which restarts at every break
+                (void)lit_f;
+                const double s1 = literal_sum(tg, s, sv, pf + 1, k1);
                 cyc_lit += clock64() - c0;
                 ++n_lit;
                 n_litterms += k1 - (pf + 1);
