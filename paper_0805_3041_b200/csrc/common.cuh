@@ -21,9 +21,13 @@ namespace gmg_dev {
 
 constexpr int kWarp = 32;
 
+// Rows [w0, w1) are the rows a kernel produces (the whole grid, or one rank's
+// slab of it when a level is sharded); domain tests always use the
+// full [0, ny).
 struct Grid {
     int nx, ny;
     long long pitch;
+    int w0 = 0, w1 = 0;
     __host__ __device__ long long at(int i, int j) const { return (long long)j * pitch + i; }
     __host__ __device__ bool inside(int i, int j) const { return i >= 0 && i < nx && j >= 0 && j < ny; }
 };

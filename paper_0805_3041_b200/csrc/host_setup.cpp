@@ -264,6 +264,33 @@ void factor_ilu0(int nx, int ny, const double* c, const double* w, const double*
         }
 }
 
+SlabPlan slab_plan(const std::vector<int>& ny, int world, int min_rows, int halo) {
+    const int L = static_cast<int>(ny.size());
+    SlabPlan sp;
+    sp.Ls = L + 1;
+    if (world > 1)
+        for (int l = 1; l <= L; ++l)
+            if (ny[l - 1] >= min_rows && ny[l - 1] >= world * halo) {
+                sp.Ls = l;
+                break;
+            }
+    sp.w0.assign(L, std::vector<int>(world, 0));
+    sp.w1.assign(L, std::vector<int>(world, 0));
+    for (int l = 1; l <= L; ++l)
+        for (int r = 0; r < world; ++r) {
+            if (l < sp.Ls) {
+                sp.w1[l - 1][r] = ny[l - 1];
+            } else if (l == sp.Ls) {
+                sp.w0[l - 1][r] = static_cast<int>(static_cast<long long>(r) * ny[l - 1] / world);
+                sp.w1[l - 1][r] = static_cast<int>(static_cast<long long>(r + 1) * ny[l - 1] / world);
+            } else {
+                sp.w0[l - 1][r] = r == 0 ? 0 : 2 * sp.w0[l - 2][r];
+                sp.w1[l - 1][r] = r == world - 1 ? ny[l - 1] : 2 * sp.w1[l - 2][r];
+            }
+        }
+    return sp;
+}
+
 double seqsum_emulate(const double* p, long long n, int T, int EPT, long long* stats) {
     using namespace gmg_ss;
     const long long C = static_cast<long long>(T) * EPT;

@@ -50,6 +50,20 @@ std::string check_nested(const Level& coarse, const Level& fine);
 void factor_ilu0(int nx, int ny, const double* c, const double* w, const double* e, const double* s,
                  const double* n, double* lw, double* ls, double* d);
 
+// Row-slab partition of a hierarchy over `world` ranks (DESIGN.md §7,
+// SURVEY.md §8e). Levels l >= Ls (the first level with at least min_rows
+// interior rows and at least `halo` rows per rank) are split into contiguous
+// row windows; coarser levels are replicated on every rank. On Ls the rows are
+// divided evenly; each finer level doubles the boundaries, so a coarse row's
+// restriction stencil (fine rows 2Q..2Q+2) and a fine row's prolongation
+// parents stay on the owning rank up to one halo row.
+// w0/w1 are [level-1][rank]; replicated levels get [0, ny) for every rank.
+struct SlabPlan {
+    int Ls = 0;  // first sharded level (num_levels + 1 if none)
+    std::vector<std::vector<int>> w0, w1;
+};
+SlabPlan slab_plan(const std::vector<int>& ny, int world, int min_rows, int halo);
+
 // CPU emulation of the device exact-order summation engine.
 double seqsum_emulate(const double* terms, long long n, int threads, int ept, long long* stats);
 

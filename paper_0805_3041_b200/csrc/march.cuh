@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(TW) k_smooth(Grid fg, Coef A, Src src, OmegaSr
 
     const int t = threadIdx.x;
     const int i = blockIdx.x * OUTW - M + t;
-    const int j0 = blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.ny);
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
     const bool col_in = i >= 0 && i < fg.nx;
     const bool owner = col_in && t >= M && t < TW - M;
 
@@ -270,8 +270,8 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
 
     const int t = threadIdx.x;
     const int i = blockIdx.x * OUTW - 2 + t;
-    const int j0 = blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.ny);
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
     const bool col_in = i >= 0 && i < fg.nx;
     const bool owner = col_in && t >= 2 && t < TW - 2;
     src.prepare(i);
@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(TW) k_omega_terms(Grid fg, Coef A, SrcProlong 
     __shared__ double xs[2][TW];
     const int t = threadIdx.x;
     const int i = blockIdx.x * OUTW - 1 + t;
-    const int j0 = blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.ny);
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
     const bool col_in = i >= 0 && i < fg.nx;
     const bool owner = col_in && t >= 1 && t < TW - 1;
     src.prepare(i);

@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(TW) k_smooth2(Grid fg, Coef A, Src src, OmegaS
 
     const int t = threadIdx.x;
     const int i = blockIdx.x * OUTW - H + 2 * t;  // even
-    const int j0 = blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.ny);
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
     const bool in0 = i >= 0 && i < fg.nx, in1 = i + 1 >= 0 && i + 1 < fg.nx;
     const bool owner = 2 * t >= H && 2 * t < 2 * TW - H;
 
@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(TW) k_smooth3(Grid fg, Coef A, const double* _
 
     const int t = threadIdx.x;
     const int i = blockIdx.x * OUTW - H + 2 * t;  // even
-    const int j0 = blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.ny);
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
     const bool in0 = i >= 0 && i < fg.nx, in1 = i + 1 >= 0 && i + 1 < fg.nx;
     const bool owner = 2 * t >= H && 2 * t < 2 * TW - H;
     const int m0 = (i - 2 * t) / 2 - 1;  // first coarse column staged (slot 0)

@@ -277,7 +277,8 @@ __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 // ---- walk ---------------------------------------------------------------------
 // grid (nch, NS); block kSsT; dynamic smem (kSsC + kSsC/32) doubles.
 template <class TG>
-__global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch, SsPair sts) {
+__global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
+                                                       const double* __restrict__ pre0) {
     extern __shared__ double tm[];
     __shared__ double swd[8];
     __shared__ SegF sws[8];
@@ -316,9 +317,11 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 
     // (2) approximate prefix by look-back
     const double tot_approx = block_sum_d(ts, swd);
+    // pre0: approximate sum of the terms before this range (earlier row slabs)
+    const double base_pre = pre0 ? pre0[s] : 0.0;
     if (t == 0) {
         if (c == 0) {
-            S.incl[0] = tot_approx;
+            S.incl[0] = base_pre + tot_approx;
             st_flag(S.flag, 2);
         } else {
             S.agg[c] = tot_approx;
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
         }
     }
     if (t < 32) {
-        const double pre = c == 0 ? 0.0 : lookback_d(c, S.flag, S.agg, S.incl);
+        const double pre = c == 0 ? base_pre : lookback_d(c, S.flag, S.agg, S.incl);
         if (t == 0) {
             s_pre = pre;
             if (c > 0) {
@@ -548,7 +551,8 @@ __device__ double warp_walk(const TG& tg, int s, double sv, long long k0, long l
 // grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays,
 // warps 1.. stage the next batch.
 template <class TG>
-__global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out) {
+__global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out,
+                                                 const double* __restrict__ start) {
     extern __shared__ unsigned char smraw[];
     gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
     __shared__ longlong2 cD[32];  // per record of the current group: signed run steps (parity 0, 1)
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
     // sum stays inside one binade whose spacing is u = 2^(E-1075), so
     // s + Q*u is exact (Q*u: power-of-two scaling; the result is representable)
     // and the integer state is M = s * 2^(1075-E), also exact.
-    double sv = 0.0;
+    double sv = start ? start[s] : 0.0;  // exact state entering this range (earlier row slabs)
     long long prev = -1;  // global index of the last element consumed
     unsigned long long n_brk = 0, n_lit = 0, n_litterms = 0, cyc_lit = 0;
     const long long cyc0 = clock64();
@@ -689,13 +693,14 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
 // walk + chain: on the coarse levels the engine's phases are pure latency.
 constexpr int kSsDirect = 4096;
 template <class TG>
-__global__ void __launch_bounds__(256) k_ss_direct(TG tg, int n, double* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_ss_direct(TG tg, int n, double* __restrict__ out,
+                                                   const double* __restrict__ start) {
     extern __shared__ double tv[];
     const int s = blockIdx.x;
     for (int k = threadIdx.x; k < n; k += blockDim.x) tv[k] = tg.term(s, k);
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0;
+        double a = start ? start[s] : 0.0;
         int k = 0;
         for (; k + 8 <= n; k += 8) {
             double v[8];

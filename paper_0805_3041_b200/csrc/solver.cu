@@ -8,6 +8,7 @@
 // replayed; the host only reads back the residual norm to run the reference's
 // stopping and divergence tests.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <array>
@@ -93,7 +94,9 @@ struct Lev {
     std::vector<double> hx, hy;
     double* scr[2] = {nullptr, nullptr};  // smoother scratch (adi/gsadi/ilu0), allocated on demand
     double* scrmem = nullptr;
-    Grid grid() const { return Grid{nx, ny, pitch}; }
+    int w0 = 0, w1 = 0;  // owned rows; [0, ny) unless the level is sharded
+    Grid grid() const { return Grid{nx, ny, pitch, w0, w1}; }
+    int rows() const { return w1 - w0; }
     long long n() const { return (long long)nx * ny; }
 };
 
@@ -108,6 +111,35 @@ struct SmSetup {
     int kind = 0;
     double omega = 0.0;
     std::vector<SmLev> lev;
+};
+
+// ---- NCCL, loaded on first use (only the row-slab multi-process mode needs it) ----
+typedef struct {
+    char internal[128];
+} NcclId;
+enum { kNcclFloat64 = 8 };
+struct NcclApi {
+    int (*getUniqueId)(NcclId*) = nullptr;
+    int (*commInitRank)(void**, int, NcclId, int) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*bcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
+    const char* (*errStr)(int) = nullptr;
+};
+
+// Row-slab distribution shared by the slabs of one solve.
+struct DistCtx {
+    int world = 1;
+    int Ls = 0;       // first sharded level
+    int H = 4;        // halo rows exchanged (>= fused smoothing steps per launch)
+    bool local = true;  // virtual ranks: all slabs in this process on one stream
+    void* comm = nullptr;  // ncclComm_t (multi-process mode)
+    std::vector<gmg_problem*> slabs;  // local mode: slab r = rank r (slab 0 owns the others)
+    std::vector<std::vector<int>> w0, w1;  // [level-1][rank]
 };
 
 }  // namespace
@@ -143,6 +175,10 @@ struct gmg_problem {
     std::map<std::string, std::array<cudaGraphExec_t, 2>> graphs;
     std::map<std::pair<int, unsigned long long>, SmSetup> smsetups;  // (kind, omega bits)
     double* linebuf = nullptr;  // k_gstri scratch: 2 x max(nx, ny)
+    // row-slab mode: rank of this slab and the shared context (null: single GPU)
+    int rank = 0;
+    std::shared_ptr<DistCtx> dist;
+    double* dscr = nullptr;  // [0,8): approx totals + nz; [8,16): rank prefix; [16,24): start; [32,..): gathered
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     Lev& lev(int l) { return lv.at(l - 1); }
 };
@@ -205,7 +241,8 @@ __global__ void k_coarse_chol(const double* __restrict__ band, int n, int bw, Gr
 }
 
 // Fast (tree-order) reduction finisher: sums the chunk partials of S1.
-__global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, double* __restrict__ out) {
+__global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, double* __restrict__ out,
+                             const double* __restrict__ start) {
     __shared__ double red[32];
     for (int s = 0; s < ns; ++s) {
         double a = 0.0;
@@ -216,7 +253,7 @@ __global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, d
         if (threadIdx.x == 0) {
             double t = 0.0;
             for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-            out[s] = t;
+            out[s] = start ? start[s] + t : t;
         }
         __syncthreads();
     }
@@ -286,40 +323,85 @@ SsPair ss_state(gmg_problem* p, int nch) {
     return sp;
 }
 
-// Sums of TG's NS term sequences, each bit-identical to the reference's
-// left-to-right loop (mode EXACT) or in tree order (mode FAST); out[s].
 template <class TG>
-void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int mode) {
-    constexpr int NS = TG::NS;
-    const int nch = (int)((n + kSsC - 1) / kSsC);
-    if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
+void seqsum_attrs() {
     static bool attr_done = false;
     if (!attr_done) {
         set_smem(k_ss_walk<TG>, ss_walk_smem());
         set_smem(k_ss_chain<TG>, ss_chain_smem());
         attr_done = true;
     }
-    if (n == 0) {  // the reference's loop leaves s = 0.0
-        CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
-        return;
-    }
-    if (mode == GMG_REDUCE_EXACT && n <= kSsDirect) {
-        k_ss_direct<TG><<<NS, 256, n * sizeof(double), p->st>>>(tg, (int)n, out);
-        CK(cudaGetLastError());
-        return;
-    }
-    if (mode == GMG_REDUCE_FAST) {
-        k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
-        k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out);
-        CK(cudaGetLastError());
-        return;
-    }
+}
+
+// Sums of TG's NS term sequences, each bit-identical to the reference's
+// left-to-right loop (mode EXACT) or in tree order (mode FAST); out[s].
+// start (device, NS values, may be null): exact state entering the range, i.e.
+// the sum of the terms before it (earlier row slabs); pre0: an approximation of
+// the same, used only to seed the speculative walk. Split in two phases so
+// that row slabs can run their walks concurrently and chain in rank order.
+template <class TG>
+void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) {
+    constexpr int NS = TG::NS;
+    const int nch = (int)((n + kSsC - 1) / kSsC);
+    if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
+    seqsum_attrs<TG>();
+    if (n <= kSsDirect) return;  // the direct kernel needs no walk
     const SsPair sp = ss_state(p, nch);
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
-    k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp);
-    k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, sp, out);
+    k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp, pre0);
     CK(cudaGetLastError());
+}
+
+template <class TG>
+void seqsum_chain(gmg_problem* p, const TG& tg, long long n, double* out, const double* start) {
+    constexpr int NS = TG::NS;
+    if (n == 0) {  // the reference's loop leaves s unchanged (0.0 for a whole sum)
+        if (start)
+            CK(cudaMemcpyAsync(out, start, NS * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
+        else
+            CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
+        return;
+    }
+    if (n <= kSsDirect) {
+        k_ss_direct<TG><<<NS, 256, n * sizeof(double), p->st>>>(tg, (int)n, out, start);
+        CK(cudaGetLastError());
+        return;
+    }
+    const int nch = (int)((n + kSsC - 1) / kSsC);
+    const SsPair sp = ss_state(p, nch);
+    k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, sp, out, start);
+    CK(cudaGetLastError());
+}
+
+// tree-order partial sums of the NS sequences into out (fast mode; also the
+// approximate totals that seed the walks of later row slabs)
+template <class TG>
+void seqsum_fast(gmg_problem* p, const TG& tg, long long n, double* out, const double* start) {
+    constexpr int NS = TG::NS;
+    const int nch = (int)((n + kSsC - 1) / kSsC);
+    if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
+    if (n == 0) {
+        if (start)
+            CK(cudaMemcpyAsync(out, start, NS * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
+        else
+            CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
+        return;
+    }
+    k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
+    k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out, start);
+    CK(cudaGetLastError());
+}
+
+template <class TG>
+void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int mode, const double* start = nullptr,
+            const double* pre0 = nullptr) {
+    if (mode == GMG_REDUCE_FAST) {
+        seqsum_fast(p, tg, n, out, start);
+        return;
+    }
+    seqsum_walk(p, tg, n, pre0);
+    seqsum_chain(p, tg, n, out, start);
 }
 
 Prolong prolong_from(gmg_problem* p, int coarse_level, const double* uc) {
@@ -341,8 +423,8 @@ template <int M, class Coef, class Src>
 void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, OmegaSrc om,
                      const double* g, double* out, double wd) {
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
-    const int seg = seg_rows(L.nx, L.ny);
-    dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.ny + seg - 1) / seg);
+    const int seg = seg_rows(L.nx, L.rows());
+    dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.rows() + seg - 1) / seg);
     k_smooth<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
     CK(cudaGetLastError());
 }
@@ -353,8 +435,8 @@ void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& sr
     constexpr int H = (M + 1) & ~1;
     constexpr int OUTW = 2 * kTW - 2 * H;
     constexpr int PF = sizeof(typename Src::Raw) > 32 ? 2 : 3;
-    const int seg = seg_rows(L.nx, L.ny);
-    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.ny + seg - 1) / seg);
+    const int seg = seg_rows(L.nx, L.rows());
+    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
     k_smooth2<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
     CK(cudaGetLastError());
 }
@@ -373,8 +455,8 @@ void launch_smooth3_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     }
     Prolong P{};
     if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
-    const int seg = seg_rows(L.nx, L.ny);
-    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.ny + seg - 1) / seg);
+    const int seg = seg_rows(L.nx, L.rows());
+    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
     k_smooth3<M, kTW, D, SK, Coef><<<grid, kTW, sizeof(SM), p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
     CK(cudaGetLastError());
 }
@@ -457,8 +539,8 @@ template <class Coef, class Src>
 void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, const double* g,
                     double* dout, double* x0out, double* gc, int neg = 0,
                     OmegaSrc om = OmegaSrc{nullptr, nullptr, 1.0, nullptr}) {
-    const int seg = seg_rows(L.nx, L.ny);
-    dim3 grid((L.nx + (kTW - 4) - 1) / (kTW - 4), (L.ny + seg - 1) / seg);
+    const int seg = seg_rows(L.nx, L.rows());
+    dim3 grid((L.nx + (kTW - 4) - 1) / (kTW - 4), (L.rows() + seg - 1) / seg);
     Grid cg{0, 0, 0};
     RestrictW rw{};
     if (gc) {
@@ -677,8 +759,8 @@ void norm_sum(gmg_problem* p, const Lev& L, const double* v, double* out, int mo
 // adaptive_omega sums for corr = P uc: terms materialised by k_omega_terms.
 void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc, int mode) {
     CK(cudaMemsetAsync(p->nz, 0, sizeof(int), p->st));
-    const int seg = seg_rows(L.nx, L.ny);
-    dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.ny + seg - 1) / seg);
+    const int seg = seg_rows(L.nx, L.rows());
+    dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.rows() + seg - 1) / seg);
     SrcProlong src{prolong_from(p, L.l - 1, uc), L.nx, L.ny, 0.0};
     double* T0 = p->T;
     double* T1 = p->T + p->lev(p->L).n();
@@ -691,96 +773,412 @@ void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc,
 }
 
 // ---------------------------------------------------------------------------
+// row-slab transport: halo rows, gathers, the exact-sum handoff
+// ---------------------------------------------------------------------------
+NcclApi& nccl() {
+    static NcclApi a;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+            a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+            a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+            a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+            a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+            a.bcast = reinterpret_cast<decltype(a.bcast)>(dlsym(h, "ncclBroadcast"));
+            a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(h, "ncclAllGather"));
+            a.groupStart = reinterpret_cast<decltype(a.groupStart)>(dlsym(h, "ncclGroupStart"));
+            a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+            a.errStr = reinterpret_cast<decltype(a.errStr)>(dlsym(h, "ncclGetErrorString"));
+        }
+    }
+    if (!a.send || !a.recv || !a.bcast || !a.allGather || !a.groupStart || !a.groupEnd || !a.commInitRank)
+        throw GmgError{GMG_ERR_UNSUPPORTED, "row-slab mode needs libnccl.so.2"};
+    return a;
+}
+#define NC(x)                                                                                   \
+    do {                                                                                        \
+        const int r_ = (x);                                                                     \
+        if (r_ != 0) throw GmgError{GMG_ERR_CUDA, std::string("nccl: ") + nccl().errStr(r_)};   \
+    } while (0)
+
+// buffer ids: level buffers U0..DD, and the finest level's x ping-pong and b
+enum BufId { B_X0 = 10, B_X1 = 11, B_B = 12 };
+double* bufptr(gmg_problem* q, int l, int id) {
+    if (id == B_X0) return q->X[0];
+    if (id == B_X1) return q->X[1];
+    if (id == B_B) return q->B;
+    return q->lev(l).buf[id];
+}
+
+// rows [a, b) of a level-l buffer, as whole pitched rows
+struct RowSpan {
+    double* p;
+    size_t count;
+};
+RowSpan rows_of(gmg_problem* q, int l, int id, int a, int b) {
+    const Lev& L = q->lev(l);
+    return RowSpan{bufptr(q, l, id) + (long long)a * L.pitch, (size_t)std::max(0, b - a) * (size_t)L.pitch};
+}
+
+// Refresh `rows` halo rows on both sides of every slab boundary of level l.
+void dist_halo(const std::vector<gmg_problem*>& S, DistCtx& D, int l, int id, int rows) {
+    const auto& w0 = D.w0[l - 1];
+    const auto& w1 = D.w1[l - 1];
+    cudaStream_t st = S[0]->st;
+    if (D.local) {
+        for (int r = 0; r + 1 < D.world; ++r) {
+            const int e = w1[r];  // == w0[r + 1]
+            const RowSpan up = rows_of(S[r], l, id, e - rows, e), upd = rows_of(S[r + 1], l, id, e - rows, e);
+            CK(cudaMemcpyAsync(upd.p, up.p, up.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            const RowSpan dn = rows_of(S[r + 1], l, id, e, e + rows), dnd = rows_of(S[r], l, id, e, e + rows);
+            CK(cudaMemcpyAsync(dnd.p, dn.p, dn.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
+        return;
+    }
+    gmg_problem* q = S[0];
+    const int r = q->rank;
+    NcclApi& n = nccl();
+    NC(n.groupStart());
+    if (r > 0) {
+        const RowSpan mine = rows_of(q, l, id, w0[r], w0[r] + rows), theirs = rows_of(q, l, id, w0[r] - rows, w0[r]);
+        NC(n.send(mine.p, mine.count, kNcclFloat64, r - 1, D.comm, st));
+        NC(n.recv(theirs.p, theirs.count, kNcclFloat64, r - 1, D.comm, st));
+    }
+    if (r + 1 < D.world) {
+        const RowSpan mine = rows_of(q, l, id, w1[r] - rows, w1[r]), theirs = rows_of(q, l, id, w1[r], w1[r] + rows);
+        NC(n.send(mine.p, mine.count, kNcclFloat64, r + 1, D.comm, st));
+        NC(n.recv(theirs.p, theirs.count, kNcclFloat64, r + 1, D.comm, st));
+    }
+    NC(n.groupEnd());
+}
+
+// Every rank's rows [a[r], b[r]) of a level-l buffer to every rank.
+void dist_gather(const std::vector<gmg_problem*>& S, DistCtx& D, int l, int id, const std::vector<int>& a,
+                 const std::vector<int>& b) {
+    cudaStream_t st = S[0]->st;
+    if (D.local) {
+        for (int r = 0; r < D.world; ++r)
+            for (int t = 0; t < D.world; ++t)
+                if (t != r) {
+                    const RowSpan src = rows_of(S[r], l, id, a[r], b[r]), dst = rows_of(S[t], l, id, a[r], b[r]);
+                    if (src.count)
+                        CK(cudaMemcpyAsync(dst.p, src.p, src.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                }
+        return;
+    }
+    NcclApi& n = nccl();
+    NC(n.groupStart());
+    for (int r = 0; r < D.world; ++r) {
+        const RowSpan sp = rows_of(S[0], l, id, a[r], b[r]);
+        if (sp.count) NC(n.bcast(sp.p, sp.p, sp.count, kNcclFloat64, r, D.comm, st));
+    }
+    NC(n.groupEnd());
+}
+
+// The coarse rows that rank r's slab of sharded level l restricts into (the
+// centre fine row 2Q+1 lies in the slab): [w0/2, w1/2).
+void threshold_rows(const DistCtx& D, int l, std::vector<int>& a, std::vector<int>& b) {
+    a.resize(D.world);
+    b.resize(D.world);
+    for (int r = 0; r < D.world; ++r) {
+        a[r] = D.w0[l - 1][r] / 2;
+        b[r] = D.w1[l - 1][r] / 2;
+    }
+}
+
+__global__ void k_nz_to_d(const int* __restrict__ nz, double* __restrict__ out) { out[0] = nz[0] ? 1.0 : 0.0; }
+
+// From the gathered per-rank approximate totals g[r*8 + k] (k < NS; k == NS:
+// nz flag): pre[k] = sum over ranks below `rank` (seeds the walk), nz = OR,
+// and for the fast mode the rank-ordered total.
+__global__ void k_dist_prefix(const double* __restrict__ g, int rank, int world, int ns, int with_nz,
+                              double* __restrict__ pre, int* __restrict__ nz, double* __restrict__ total) {
+    if (threadIdx.x != 0) return;
+    for (int k = 0; k < ns; ++k) {
+        double a = 0.0, t = 0.0;
+        for (int r = 0; r < world; ++r) {
+            if (r < rank) a += g[r * 8 + k];
+            t += g[r * 8 + k];
+        }
+        pre[k] = a;
+        if (total) total[k] = t;
+    }
+    if (with_nz) {
+        int any = 0;
+        for (int r = 0; r < world; ++r) any |= g[r * 8 + ns] != 0.0;
+        *nz = any;
+    }
+}
+
+// A reduction over a sharded level: slab r sums the terms of its own rows.
+// EXACT: walks run per slab from approximate rank prefixes, then the chains run
+// in rank order, each starting from the exact state its predecessor ended in,
+// and the last rank's result is broadcast: the reference's k order exactly.
+// `make(q)` returns {term generator, term count} for slab q.
+template <class MakeTG>
+void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int out_off, int mode, bool with_nz) {
+    using TG = decltype(make(S[0]).first);
+    constexpr int NS = TG::NS;
+    if (!D) {
+        auto tn = make(S[0]);
+        seqsum(S[0], tn.first, tn.second, S[0]->sums + out_off, mode);
+        return;
+    }
+    cudaStream_t st = S[0]->st;
+    // 1. approximate totals (and the nz flag) of every slab, gathered everywhere
+    for (auto* q : S) {
+        auto tn = make(q);
+        seqsum_fast(q, tn.first, tn.second, q->dscr, nullptr);
+        if (with_nz) k_nz_to_d<<<1, 1, 0, st>>>(q->nz, q->dscr + NS);
+    }
+    CK(cudaGetLastError());
+    if (D->local) {
+        for (auto* q : S)
+            for (auto* t : S)
+                CK(cudaMemcpyAsync(t->dscr + 32 + 8 * q->rank, q->dscr, 8 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   st));
+    } else {
+        NC(nccl().allGather(S[0]->dscr, S[0]->dscr + 32, 8, kNcclFloat64, D->comm, st));
+    }
+    for (auto* q : S)
+        k_dist_prefix<<<1, 32, 0, st>>>(q->dscr + 32, q->rank, D->world, NS, with_nz ? 1 : 0, q->dscr + 8, q->nz,
+                                        mode == GMG_REDUCE_FAST ? q->sums + out_off : nullptr);
+    CK(cudaGetLastError());
+    if (mode == GMG_REDUCE_FAST) return;
+    // 2. walks (independent), 3. chains in rank order, 4. broadcast of the total
+    for (auto* q : S) {
+        auto tn = make(q);
+        seqsum_walk(q, tn.first, tn.second, q->dscr + 8);
+    }
+    if (D->local) {
+        for (size_t r = 0; r < S.size(); ++r) {
+            auto tn = make(S[r]);
+            seqsum_chain(S[r], tn.first, tn.second, S[r]->sums + out_off, r ? S[r - 1]->sums + out_off : nullptr);
+        }
+        for (size_t r = 0; r + 1 < S.size(); ++r)
+            CK(cudaMemcpyAsync(S[r]->sums + out_off, S.back()->sums + out_off, NS * sizeof(double),
+                               cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    gmg_problem* q = S[0];
+    const int r = q->rank;
+    NcclApi& n = nccl();
+    if (r > 0) NC(n.recv(q->dscr + 16, NS, kNcclFloat64, r - 1, D->comm, st));
+    auto tn = make(q);
+    seqsum_chain(q, tn.first, tn.second, q->sums + out_off, r ? q->dscr + 16 : nullptr);
+    if (r + 1 < D->world) NC(n.send(q->sums + out_off, NS, kNcclFloat64, r + 1, D->comm, st));
+    NC(n.bcast(q->sums + out_off, q->sums + out_off, NS, kNcclFloat64, D->world - 1, D->comm, st));
+}
+
+// ---------------------------------------------------------------------------
 // cycle driver (recorded into a CUDA graph)
 // ---------------------------------------------------------------------------
+// A smoothing start in buffer ids (SmoothSrc with per-slab pointers).
+struct SrcId {
+    Start kind = S_ZERO;
+    int u = -1;   // level-l buffer (S_U, S_CORRECT)
+    int uc = -1;  // level-(l-1) buffer (S_PROLONG, S_CORRECT)
+    bool adaptive = false;
+};
+
 struct Driver {
-    gmg_problem* p;
+    std::vector<gmg_problem*> S;  // the slabs this process drives, in rank order (one without row slabs)
     gmg_cycle_desc sp;
     const SmSetup* sm = nullptr;  // setup_smoothers products (null for jacobi / GS / SOR)
 
-    // smooth_step x `steps` with the configured preconditioner (setup_smoothers)
-    double* smooth(const Lev& L, int steps, const SmoothSrc& s, const double* g, double* a, double* b) {
-        if (sp.smoother_kind == GMG_SMOOTHER_JACOBI) return smooth_steps(p, L, steps, s, g, a, b, sp.smoothing_omega);
-        return pc_steps(p, L, steps, s, g, a, b, sp, sm ? &sm->lev[L.l - 1] : nullptr);
+    gmg_problem* p() const { return S[0]; }
+    DistCtx* D() const { return S[0]->dist.get(); }
+    bool sharded(int l) const { return D() && l >= D()->Ls; }
+    void halo(int l, int id, int rows) {
+        if (sharded(l)) dist_halo(S, *D(), l, id, rows);
+    }
+    // after a restriction from sharded level l into replicated level l-1
+    void gather_threshold(int l, int id_coarse) {
+        if (!sharded(l) || sharded(l - 1)) return;
+        std::vector<int> a, b;
+        threshold_rows(*D(), l, a, b);
+        dist_gather(S, *D(), l - 1, id_coarse, a, b);
+    }
+    SmoothSrc resolve(gmg_problem* q, int l, const SrcId& s) const {
+        SmoothSrc r;
+        r.kind = s.kind;
+        if (s.u >= 0) r.u = bufptr(q, l, s.u);
+        if (s.uc >= 0) r.uc = bufptr(q, l - 1, s.uc);
+        r.om = s.adaptive ? OmegaSrc{q->sums, q->nz, 0.0, q->status}
+                          : OmegaSrc{nullptr, nullptr, sp.correction_omega, q->status};
+        return r;
+    }
+
+    // smooth_step x `steps` with the configured preconditioner (setup_smoothers);
+    // outputs alternate a, b. Returns the id of the result.
+    int smooth(int l, int steps, SrcId s, int g, int a, int b) {
+        if (sp.smoother_kind != GMG_SMOOTHER_JACOBI) {
+            if (D()) throw GmgError{GMG_ERR_UNSUPPORTED, "row slabs: only the jacobi smoother is sharded"};
+            gmg_problem* q = p();
+            const Lev& L = q->lev(l);
+            const double* r = pc_steps(q, L, steps, resolve(q, l, s), bufptr(q, l, g), bufptr(q, l, a),
+                                       bufptr(q, l, b), sp, sm ? &sm->lev[l - 1] : nullptr);
+            return r == bufptr(q, l, a) ? a : b;
+        }
+        if (sharded(l)) {
+            const int H = D()->H;
+            halo(l, g, H);
+            if (s.u >= 0) halo(l, s.u, H);
+            if (s.uc >= 0) halo(l - 1, s.uc, H);
+        }
+        int dst = a;
+        int left = steps;
+        bool first = true;
+        while (first || left > 0) {
+            const int M = std::min(left, kMaxFuse);
+            for (auto* q : S)
+                launch_smooth(q, q->lev(l), M, resolve(q, l, s), bufptr(q, l, g), bufptr(q, l, dst),
+                              sp.smoothing_omega);
+            left -= M;
+            first = false;
+            s = SrcId{};
+            s.kind = S_U;
+            s.u = dst;
+            if (left > 0) {
+                halo(l, dst, D() ? D()->H : 0);
+                dst = (dst == a) ? b : a;
+            }
+        }
+        return dst;
     }
 
     // gmg::mg_cycle (cycle.cpp:69-100) on level l from start s with rhs g.
-    const double* visit(int l, SmoothSrc s, const double* g) {
-        Lev& L = p->lev(l);
+    int visit(int l, SrcId s, int g) {
+        const int u_in = s.kind == S_U ? s.u : -1;
+        const int a = (u_in == U0) ? U1 : U0;
+        const int b = (a == U0) ? U1 : U0;
         if (l == 1) {
             // coarse_solve (cycle.cpp:57-65)
-            if ((unsigned long long)L.n() <= sp.coarse_direct_max_neq) {
-                launch_coarse(p, g, L.buf[U0]);
-                return L.buf[U0];
+            if ((unsigned long long)p()->lev(1).n() <= sp.coarse_direct_max_neq) {
+                for (auto* q : S) launch_coarse(q, bufptr(q, 1, g), q->lev(1).buf[U0]);
+                return U0;
             }
-            double* a = (s.u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
-            double* b = (a == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
-            return smooth(L, std::max(1, sp.pre_steps + sp.post_steps), s, g, a, b);
+            return smooth(1, std::max(1, sp.pre_steps + sp.post_steps), s, g, a, b);
         }
-        double* a = (s.u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
-        double* b = (a == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
-        double* u = smooth(L, sp.pre_steps, s, g, a, b);
-        double* other = (u == L.buf[U0]) ? L.buf[U1] : L.buf[U0];
+        const int u = smooth(l, sp.pre_steps, s, g, a, b);
+        const int other = (u == U0) ? U1 : U0;
         const bool adaptive = sp.adaptive_correction != 0;
-        Lev& C = p->lev(l - 1);
-        launch_resid(p, L, u, nullptr, g, adaptive ? L.buf[DD] : nullptr, nullptr, C.buf[GRHS]);
-        SmoothSrc z;
-        z.kind = S_ZERO;
-        const double* uc = visit(l - 1, z, C.buf[GRHS]);
+        // the post-smoothing start u + w*P uc reads u within the halo; the residual needs 2 rows
+        halo(l, u, D() ? D()->H : 0);
+        for (auto* q : S) {
+            Lev& L = q->lev(l);
+            launch_resid(q, L, L.buf[u], nullptr, bufptr(q, l, g), adaptive ? L.buf[DD] : nullptr, nullptr,
+                         q->lev(l - 1).buf[GRHS]);
+        }
+        gather_threshold(l, GRHS);
+        SrcId z;
+        int uc = visit(l - 1, z, GRHS);
         if (sp.cycle == GMG_CYCLE_W) {
-            SmoothSrc w;
+            SrcId w;
             w.kind = S_U;
             w.u = uc;
-            uc = visit(l - 1, w, C.buf[GRHS]);
+            uc = visit(l - 1, w, GRHS);
         }
-        SmoothSrc cs;
+        if (sharded(l - 1)) halo(l - 1, uc, D()->H);
+        SrcId cs;
         cs.kind = S_CORRECT;
         cs.u = u;
         cs.uc = uc;
-        if (adaptive) {
-            omega_sums(p, L, L.buf[DD], uc, sp.reduction);
-            cs.om = OmegaSrc{p->sums, p->nz, 0.0, p->status};
-        } else {
-            cs.om = OmegaSrc{nullptr, nullptr, sp.correction_omega, p->status};
+        cs.adaptive = adaptive;
+        if (adaptive) omega_sums_d(l, uc);
+        return smooth(l, sp.post_steps, cs, g, other, u);
+    }
+
+    // adaptive_omega sums (cycle.cpp:40-51) for corr = P uc over each slab's rows
+    void omega_sums_d(int l, int uc) {
+        for (auto* q : S) {
+            Lev& L = q->lev(l);
+            CK(cudaMemsetAsync(q->nz, 0, sizeof(int), q->st));
+            const int seg = seg_rows(L.nx, L.rows());
+            dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.rows() + seg - 1) / seg);
+            SrcProlong src{prolong_from(q, l - 1, q->lev(l - 1).buf[uc]), L.nx, L.ny, 0.0};
+            double* T0 = q->T;
+            double* T1 = q->T + q->lev(q->L).n();
+            with_coef(L, [&](const auto& A) {
+                using C = std::decay_t<decltype(A)>;
+                k_omega_terms<kTW, 2, C><<<grid, kTW, 0, q->st>>>(L.grid(), A, src, L.buf[DD], T0, T1, q->nz, seg);
+            });
+            CK(cudaGetLastError());
         }
-        return smooth(L, sp.post_steps, cs, g, other, u);
+        dist_sum(S, sharded(l) ? D() : nullptr, [&](gmg_problem* q) {
+            const Lev& L = q->lev(l);
+            const long long o = (long long)L.w0 * L.nx;
+            return std::make_pair(ArrTerms{q->T + o, q->T + q->lev(q->L).n() + o}, (long long)L.rows() * L.nx);
+        }, 0, sp.reduction, true);
+    }
+
+    // exact-order ||v||^2 of a level-l buffer over the owned rows -> sums[off]
+    void norm_d(int l, int id, int off) {
+        dist_sum(S, sharded(l) ? D() : nullptr, [&](gmg_problem* q) {
+            const Lev& L = q->lev(l);
+            Grid gv{L.nx, L.rows(), L.pitch, 0, L.rows()};
+            return std::make_pair(NormTerms{bufptr(q, l, id) + (long long)L.w0 * L.pitch, gv, 1.0 / L.nx},
+                                  (long long)L.rows() * L.nx);
+        }, off, sp.reduction, false);
+    }
+
+    // residual of x (+ e) against b on the finest level -> DCAS[L], x0 -> xout, restricted -> DCAS[L-1]
+    void final_resid(int xin, int e, int xout, bool restrict_) {
+        const int L = p()->L;
+        if (sharded(L)) {
+            halo(L, xin, 2);
+            if (e >= 0) halo(L, e, 2);
+        }
+        for (auto* q : S) {
+            Lev& F = q->lev(L);
+            launch_resid(q, F, bufptr(q, L, xin), e >= 0 ? F.buf[e] : nullptr, q->B, F.buf[DCAS], bufptr(q, L, xout),
+                         restrict_ ? q->lev(L - 1).buf[DCAS] : nullptr);
+        }
+        if (restrict_) gather_threshold(L, DCAS);
     }
 
     // One outer cycle: x_out = cycle(x_in); r = b - A x_out -> DCAS[L]; norm^2 -> sums[2].
-    void cycle(const double* xin, double* xout) {
-        const int L = p->L;
-        Lev& F = p->lev(L);
-        const double* e;
+    void cycle(int xin, int xout) {
+        const int L = p()->L;
         if (sp.cycle == GMG_CYCLE_F) {
             // fcycle_pass (cycle.cpp:119-142): DCAS[L], DCAS[L-1] are current
-            for (int l = L - 1; l >= 2; --l) launch_restrict(p, l, p->lev(l).buf[DCAS], p->lev(l - 1).buf[DCAS]);
-            SmoothSrc z;
-            z.kind = S_ZERO;
+            for (int l = L - 1; l >= 2; --l) {
+                if (sharded(l)) halo(l, DCAS, 1);
+                for (auto* q : S) launch_restrict(q, l, q->lev(l).buf[DCAS], q->lev(l - 1).buf[DCAS]);
+                gather_threshold(l, DCAS);
+            }
+            SrcId z;
             if (L == 1) {
-                SmoothSrc s0;
+                SrcId s0;
                 s0.kind = S_U;
                 s0.u = xin;
-                e = visit(1, s0, p->B);
-                launch_resid(p, F, e, nullptr, p->B, F.buf[DCAS], xout, nullptr);
+                const int e = visit_top(s0);
+                final_resid(e, -1, xout, false);
             } else {
-                e = visit(1, z, p->lev(1).buf[DCAS]);
+                int e = visit(1, z, DCAS);
                 for (int l = 2; l <= L; ++l) {
-                    SmoothSrc s;
+                    SrcId s;
                     s.kind = S_PROLONG;
                     s.uc = e;
-                    e = visit(l, s, p->lev(l).buf[DCAS]);
+                    e = visit(l, s, DCAS);
                 }
-                launch_resid(p, F, xin, e, p->B, F.buf[DCAS], xout, p->lev(L - 1).buf[DCAS]);
+                final_resid(xin, e, xout, true);
             }
         } else {
-            SmoothSrc s0;
+            SrcId s0;
             s0.kind = S_U;
             s0.u = xin;
-            e = visit(L, s0, p->B);
-            launch_resid(p, F, e, nullptr, p->B, F.buf[DCAS], xout, nullptr);
+            const int e = visit_top(s0);
+            final_resid(e, -1, xout, false);
         }
-        norm_sum(p, F, F.buf[DCAS], p->sums + 2, sp.reduction);
+        norm_d(L, DCAS, 2);
     }
+
+    // visit of the finest level with rhs b (V/W cycles, single level)
+    int visit_top(SrcId s0) { return visit(p()->L, s0, B_B); }
 };
 
 std::string spec_key(const gmg_cycle_desc& s) {
@@ -793,6 +1191,12 @@ std::string spec_key(const gmg_cycle_desc& s) {
 
 const SmSetup* find_smoother(gmg_problem* p, const gmg_cycle_desc& sp);
 
+// the slabs a driver on this handle runs: all virtual ranks of a local cluster, else itself
+std::vector<gmg_problem*> driver_slabs(gmg_problem* p) {
+    if (p->dist && p->dist->local) return p->dist->slabs;
+    return {p};
+}
+
 std::array<cudaGraphExec_t, 2>& get_graphs(gmg_problem* p, const gmg_cycle_desc& sp) {
     const std::string key = spec_key(sp);
     auto it = p->graphs.find(key);
@@ -802,8 +1206,8 @@ std::array<cudaGraphExec_t, 2>& get_graphs(gmg_problem* p, const gmg_cycle_desc&
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(p->st, cudaStreamCaptureModeThreadLocal));
         try {
-            Driver d{p, sp, find_smoother(p, sp)};
-            d.cycle(p->X[par], p->X[1 - par]);
+            Driver d{driver_slabs(p), sp, find_smoother(p, sp)};
+            d.cycle(par == 0 ? B_X0 : B_X1, par == 0 ? B_X1 : B_X0);
         } catch (...) {
             cudaStreamEndCapture(p->st, &g);
             if (g) cudaGraphDestroy(g);
@@ -1157,6 +1561,8 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         L.l = l;
         L.nx = ld.nx;
         L.ny = ld.ny;
+        L.w0 = 0;
+        L.w1 = ld.ny;
         L.pitch = ((ld.nx + 31) / 32) * 32;
         L.off0 = (size_t)L.pitch + 32;
         L.elems = L.off0 + (size_t)(L.ny + 1) * L.pitch + 64;
@@ -1384,14 +1790,14 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
         upload(p, L, L.buf[DCAS], u0, cudaMemcpyHostToDevice);
         upload(p, L, L.buf[GRHS], g, cudaMemcpyHostToDevice);
         CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
-        Driver d{p, *spec, sm};
-        SmoothSrc s;
+        Driver d{{p}, *spec, sm};
+        SrcId s;
         s.kind = S_U;
-        s.u = L.buf[DCAS];
+        s.u = DCAS;
         // visit() writes level-l results into U0/U1, so g must not alias them: it lives in GRHS,
         // which the recursion only writes on level l-1.
-        const double* r = d.visit(level, s, L.buf[GRHS]);
-        download(p, L, u, r, cudaMemcpyDeviceToHost);
+        const int r = d.visit(level, s, GRHS);
+        download(p, L, u, L.buf[r], cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
         if (spec->adaptive_correction && fetch_status(p) == 3)
             throw std::runtime_error("adaptive_omega: correction has nonpositive energy");
@@ -1654,8 +2060,8 @@ int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* 
         check_cycle(p, *spec);
         cudaGraph_t g = nullptr;
         CK(cudaStreamBeginCapture(p->st, cudaStreamCaptureModeThreadLocal));
-        Driver d{p, *spec, sm};
-        d.cycle(p->X[0], p->X[1]);
+        Driver d{driver_slabs(p), *spec, sm};
+        d.cycle(B_X0, B_X1);
         CK(cudaStreamEndCapture(p->st, &g));
         size_t nn = 0;
         CK(cudaGraphGetNodes(g, nullptr, &nn));
