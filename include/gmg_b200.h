@@ -117,6 +117,20 @@ typedef struct gmg_solve_report {
 
 typedef struct gmg_problem gmg_problem;
 
+/* Row-slab distribution. Levels with at least
+ * min_rows interior rows (and 4 rows per rank) are split into contiguous row
+ * slabs, coarser levels are replicated. rank < 0: all `world` slabs live in
+ * this process on one device (virtual ranks, exchanges are device copies);
+ * rank >= 0: this process's slab of an NCCL group, nccl_id from
+ * gmg_dist_unique_id on rank 0 (128 bytes). No reference counterpart: the
+ * reference is single-threaded; results are bit-identical to gmg::solve. */
+typedef struct gmg_slab_desc {
+    int world;
+    int rank;
+    int min_rows;
+    const unsigned char* nccl_id;
+} gmg_slab_desc;
+
 /* Thread-local text of the last failure (exception message in the reference). */
 const char* gmg_last_error(void);
 /* Library build string (arch, reduction engine version). */
@@ -129,6 +143,15 @@ int gmg_dev_num_levels(const gmg_problem* p);
 int gmg_dev_level_shape(const gmg_problem* p, int level, int* nx, int* ny);
 /* operator storage chosen at create: 0 = constant 5-point, 1 = x-varying rows, 2 = full field */
 int gmg_dev_level_coef_kind(const gmg_problem* p, int level);
+/* Row-slab problems (see gmg_slab_desc). Only gmg_dev_solve / _solve_devptr and
+ * the queries below accept such a handle; the Jacobi smoother is sharded. */
+int gmg_dev_problem_create_slabs(const gmg_problem_desc* desc, const gmg_slab_desc* slabs,
+                                 gmg_problem** out);
+int gmg_dist_unique_id(unsigned char* id128);
+/* rank, world and the first sharded level (num_levels + 1: none) of a handle */
+int gmg_dev_dist_info(const gmg_problem* p, int* rank, int* world, int* first_sharded_level);
+/* rows [w0, w1) of `level` this slab owns ([0, ny) when the level is replicated) */
+int gmg_dev_level_window(const gmg_problem* p, int level, int* w0, int* w1);
 
 /* ---- the hot path ---------------------------------------------------------- */
 /* gmg::solve: b read, x_inout carries the start vector in and the solution out.
@@ -183,6 +206,14 @@ int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* 
 int gmg_host_problem_create(int num_levels, int coarse_nx, int coarse_ny, double grading_x,
                             double grading_y, int coords, double alpha, double beta, int device,
                             gmg_problem** out);
+/* gmg_host_problem_create for row slabs. */
+int gmg_host_problem_create_slabs(int num_levels, int coarse_nx, int coarse_ny, double grading_x,
+                                  double grading_y, int coords, double alpha, double beta, int device,
+                                  const gmg_slab_desc* slabs, gmg_problem** out);
+/* The row-slab partition (no device work): first sharded level and, per level
+ * and rank, the owned rows; w0/w1 are [num_levels][world], level-major. */
+int gmg_host_slab_plan(int num_levels, const int* ny, int world, int min_rows, int halo, int* first_sharded,
+                       int* w0, int* w1);
 /* std::mt19937(seed) + uniform_real_distribution<double>(-1,1), the reference test
  * recipe (tests/oracles.hpp:252-258). */
 void gmg_host_random_vector(long long n, unsigned seed, double* out);

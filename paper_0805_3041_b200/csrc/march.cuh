@@ -280,7 +280,9 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
     }
 
     double a = 0.0, b = 0.0, c = 0.0;  // x0 rows J-2, J-1, J in own column
-    const int Jbeg = j0 - 1;
+    // d is exact from row Jbeg+1 on; a coarse row centred on an odd first row
+    // (a row-slab window may start there) needs d one row above the window
+    const int Jbeg = j0 - 2;
     const int Jend = j1 + 1;
     typename Src::Raw q[PF];
     double gq[PF];

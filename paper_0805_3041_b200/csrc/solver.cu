@@ -140,6 +140,7 @@ struct DistCtx {
     void* comm = nullptr;  // ncclComm_t (multi-process mode)
     std::vector<gmg_problem*> slabs;  // local mode: slab r = rank r (slab 0 owns the others)
     std::vector<std::vector<int>> w0, w1;  // [level-1][rank]
+    ~DistCtx();
 };
 
 }  // namespace
@@ -177,6 +178,7 @@ struct gmg_problem {
     double* linebuf = nullptr;  // k_gstri scratch: 2 x max(nx, ny)
     // row-slab mode: rank of this slab and the shared context (null: single GPU)
     int rank = 0;
+    bool owns_stream = true;
     std::shared_ptr<DistCtx> dist;
     double* dscr = nullptr;  // [0,8): approx totals + nz; [8,16): rank prefix; [16,24): start; [32,..): gathered
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -922,9 +924,11 @@ template <class MakeTG>
 void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int out_off, int mode, bool with_nz) {
     using TG = decltype(make(S[0]).first);
     constexpr int NS = TG::NS;
-    if (!D) {
-        auto tn = make(S[0]);
-        seqsum(S[0], tn.first, tn.second, S[0]->sums + out_off, mode);
+    if (!D) {  // a replicated level: every slab sums its own (identical) copy
+        for (auto* q : S) {
+            auto tn = make(q);
+            seqsum(q, tn.first, tn.second, q->sums + out_off, mode);
+        }
         return;
     }
     cudaStream_t st = S[0]->st;
@@ -1175,6 +1179,18 @@ struct Driver {
             final_resid(e, -1, xout, false);
         }
         norm_d(L, DCAS, 2);
+    }
+
+    // r0 = b - A x0 -> DCAS[L] (x0 in X[0], complete on every slab), and for the
+    // F-cycle its restriction, the first defect cascade seed
+    void initial_resid() {
+        const int L = p()->L;
+        const bool restr = sp.cycle == GMG_CYCLE_F && L >= 2;
+        for (auto* q : S) {
+            Lev& F = q->lev(L);
+            launch_resid(q, F, q->X[0], nullptr, q->B, F.buf[DCAS], nullptr, restr ? q->lev(L - 1).buf[DCAS] : nullptr);
+        }
+        if (restr) gather_threshold(L, DCAS);
     }
 
     // visit of the finest level with rhs b (V/W cycles, single level)
@@ -1429,21 +1445,30 @@ const SmSetup* find_smoother(gmg_problem* p, const gmg_cycle_desc& sp) {
     return ensure_smoother(p, sp.smoother_kind, sp.smoother_omega);
 }
 
+// Row slabs: every slab's rows of the finest x to every slab (then slab 0 holds x).
+void collect_x(gmg_problem* p, int par) {
+    if (!p->dist || p->dist->Ls > p->L) return;
+    DistCtx& D = *p->dist;
+    dist_gather(driver_slabs(p), D, p->L, par == 0 ? B_X0 : B_X1, D.w0[p->L - 1], D.w1[p->L - 1]);
+}
+
 // gmg::solve (cycle.cpp:146-194). b, x in device layout already (B, X[0]).
 void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep, int* final_par) {
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     check_smoother(sp);
-    ensure_smoother(p, sp.smoother_kind, sp.smoother_omega);
+    if (p->dist && sp.smoother_kind != GMG_SMOOTHER_JACOBI)
+        throw GmgError{GMG_ERR_UNSUPPORTED, "row slabs: only the jacobi smoother is sharded"};
+    const SmSetup* sm = ensure_smoother(p, sp.smoother_kind, sp.smoother_omega);
     const int L = p->L;
-    Lev& F = p->lev(L);
-    CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+    const std::vector<gmg_problem*> S = driver_slabs(p);
+    for (auto* q : S) CK(cudaMemsetAsync(q->status, 0, sizeof(int), q->st));
     // r0 = ||b - A x||, and the F-cycle's first defect cascade seed
-    launch_resid(p, F, p->X[0], nullptr, p->B, F.buf[DCAS], nullptr,
-                 (sp.cycle == GMG_CYCLE_F && L >= 2) ? p->lev(L - 1).buf[DCAS] : nullptr);
-    norm_sum(p, F, F.buf[DCAS], p->sums + 2, sp.reduction);
+    Driver d0{S, sp, sm};
+    d0.initial_resid();
+    d0.norm_d(L, DCAS, 2);
     const double r0 = std::sqrt(fetch_scalar(p, p->sums + 2));
-    norm_sum(p, F, p->B, p->sums + 3, sp.reduction);
+    d0.norm_d(L, B_B, 3);
     const double bnorm = std::sqrt(fetch_scalar(p, p->sums + 3));
     int hl = 0;
     rep->residual_history[hl++] = r0;
@@ -1489,6 +1514,13 @@ void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep,
 void free_problem(gmg_problem* p) {
     if (!p) return;
     cudaSetDevice(p->device);
+    if (p->dist && p->dist->local && p->rank == 0) {
+        auto D = p->dist;  // keep the context alive while the other slabs go
+        for (auto* q : D->slabs)
+            if (q != p) free_problem(q);
+        D->slabs.clear();
+    }
+    cudaFree(p->dscr);
     for (auto& kv : p->graphs)
         for (auto g : kv.second)
             if (g) cudaGraphExecDestroy(g);
@@ -1519,7 +1551,7 @@ void free_problem(gmg_problem* p) {
     if (p->hostbuf) cudaFreeHost(p->hostbuf);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
-    if (p->st) cudaStreamDestroy(p->st);
+    if (p->st && p->owns_stream) cudaStreamDestroy(p->st);
     delete p;
 }
 
@@ -1687,10 +1719,78 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
     *out = p.release();
 }
 
+DistCtx::~DistCtx() {
+    if (!local && comm && nccl().commDestroy) nccl().commDestroy(comm);
+}
+
+// Row-slab problem(s): sl->rank < 0 builds all sl->world slabs
+// in this process on one device and one stream (virtual ranks; the handle is
+// slab 0, which owns the others); sl->rank >= 0 builds this process's slab of
+// a multi-process (one GPU per rank) NCCL group.
+void create_slabs(const gmg_problem_desc* d, const gmg_slab_desc* sl, gmg_problem** out) {
+    if (!sl || sl->world < 1) throw std::invalid_argument("slabs: world must be >= 1");
+    const bool local = sl->rank < 0;
+    if (!local && (sl->rank >= sl->world || !sl->nccl_id)) throw std::invalid_argument("slabs: bad rank or id");
+    const int nloc = local ? sl->world : 1;
+    std::vector<gmg_problem*> slabs;
+    auto D = std::make_shared<DistCtx>();
+    try {
+        for (int r = 0; r < nloc; ++r) {
+            gmg_problem* q = nullptr;
+            create_problem(d, &q);
+            slabs.push_back(q);
+        }
+        for (int r = 1; r < nloc; ++r) {
+            CK(cudaStreamDestroy(slabs[r]->st));
+            slabs[r]->st = slabs[0]->st;
+            slabs[r]->owns_stream = false;
+        }
+        std::vector<int> ny;
+        for (int l = 1; l <= d->num_levels; ++l) ny.push_back(d->levels[l - 1].ny);
+        const gmg_host::SlabPlan plan = gmg_host::slab_plan(ny, sl->world, std::max(1, sl->min_rows), D->H);
+        D->world = sl->world;
+        D->Ls = plan.Ls;
+        D->local = local;
+        D->w0 = plan.w0;
+        D->w1 = plan.w1;
+        if (!local) {
+            NcclId id;
+            std::memcpy(id.internal, sl->nccl_id, sizeof id.internal);
+            void* comm = nullptr;
+            NC(nccl().commInitRank(&comm, sl->world, id, sl->rank));
+            D->comm = comm;
+        }
+        for (int r = 0; r < nloc; ++r) {
+            gmg_problem* q = slabs[r];
+            q->rank = local ? r : sl->rank;
+            q->dist = D;
+            for (int l = 1; l <= q->L; ++l) {
+                q->lev(l).w0 = plan.w0[l - 1][q->rank];
+                q->lev(l).w1 = plan.w1[l - 1][q->rank];
+            }
+            CK(cudaMalloc(&q->dscr, (32 + 8 * (size_t)sl->world) * sizeof(double)));
+            CK(cudaMemset(q->dscr, 0, (32 + 8 * (size_t)sl->world) * sizeof(double)));
+        }
+        CK(cudaDeviceSynchronize());
+        D->slabs = local ? slabs : std::vector<gmg_problem*>{slabs[0]};
+    } catch (...) {
+        for (auto* q : slabs) {
+            q->dist.reset();
+            free_problem(q);
+        }
+        throw;
+    }
+    *out = slabs[0];
+}
+
 gmg_problem* checked(gmg_problem* p) {
     if (!p) throw std::logic_error("null problem handle");
     CK(cudaSetDevice(p->device));
     return p;
+}
+
+void single(const gmg_problem* p, const char* what) {
+    if (p->dist) throw std::logic_error(std::string(what) + ": not available on a row-slab handle");
 }
 
 void check_level(const gmg_problem* p, int level, const char* what) {
@@ -1717,6 +1817,35 @@ int gmg_dev_problem_destroy(gmg_problem* p) {
     return GMG_OK;
 }
 
+int gmg_dev_problem_create_slabs(const gmg_problem_desc* desc, const gmg_slab_desc* slabs, gmg_problem** out) {
+    return guarded([&] { create_slabs(desc, slabs, out); });
+}
+
+int gmg_dist_unique_id(unsigned char* id128) {
+    return guarded([&] {
+        NcclId id;
+        NC(nccl().getUniqueId(&id));
+        std::memcpy(id128, id.internal, sizeof id.internal);
+    });
+}
+
+int gmg_dev_dist_info(const gmg_problem* p, int* rank, int* world, int* first_sharded_level) {
+    return guarded([&] {
+        if (!p) throw std::logic_error("null problem handle");
+        *rank = p->rank;
+        *world = p->dist ? p->dist->world : 1;
+        *first_sharded_level = p->dist ? p->dist->Ls : p->L + 1;
+    });
+}
+
+int gmg_dev_level_window(const gmg_problem* p, int level, int* w0, int* w1) {
+    return guarded([&] {
+        check_level(p, level, "level_window");
+        *w0 = p->lv[level - 1].w0;
+        *w1 = p->lv[level - 1].w1;
+    });
+}
+
 int gmg_dev_num_levels(const gmg_problem* p) { return p ? p->L : 0; }
 
 int gmg_dev_level_shape(const gmg_problem* p, int level, int* nx, int* ny) {
@@ -1738,13 +1867,16 @@ int gmg_dev_solve(gmg_problem* p, const gmg_cycle_desc* spec, const double* b, d
         checked(p);
         std::lock_guard<std::mutex> lk(p->mu);
         Lev& F = p->lev(p->L);
-        upload(p, F, p->B, b, cudaMemcpyHostToDevice);
-        upload(p, F, p->X[0], x, cudaMemcpyHostToDevice);
+        for (auto* q : driver_slabs(p)) {
+            upload(q, F, q->B, b, cudaMemcpyHostToDevice);
+            upload(q, F, q->X[0], x, cudaMemcpyHostToDevice);
+        }
         int par = 0;
         try {
             solve_core(p, *spec, rep, &par);
         } catch (const GmgError& e) {
             if (e.code == GMG_DIVERGED) {
+                collect_x(p, par);
                 download(p, F, x, p->X[par], cudaMemcpyDeviceToHost);
                 CK(cudaStreamSynchronize(p->st));
                 std::snprintf(rep->message, sizeof rep->message, "%s", e.msg.c_str());
@@ -1752,10 +1884,12 @@ int gmg_dev_solve(gmg_problem* p, const gmg_cycle_desc* spec, const double* b, d
             throw;
         } catch (const std::runtime_error&) {
             // x keeps the last completed iterate, as the reference's in-place x does
+            collect_x(p, par);
             download(p, F, x, p->X[par], cudaMemcpyDeviceToHost);
             CK(cudaStreamSynchronize(p->st));
             throw;
         }
+        collect_x(p, par);
         download(p, F, x, p->X[par], cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
     });
@@ -1767,10 +1901,13 @@ int gmg_dev_solve_devptr(gmg_problem* p, const gmg_cycle_desc* spec, const doubl
         checked(p);
         std::lock_guard<std::mutex> lk(p->mu);
         Lev& F = p->lev(p->L);
-        upload(p, F, p->B, b_dev, cudaMemcpyDeviceToDevice);
-        upload(p, F, p->X[0], x_dev, cudaMemcpyDeviceToDevice);
+        for (auto* q : driver_slabs(p)) {
+            upload(q, F, q->B, b_dev, cudaMemcpyDeviceToDevice);
+            upload(q, F, q->X[0], x_dev, cudaMemcpyDeviceToDevice);
+        }
         int par = 0;
         solve_core(p, *spec, rep, &par);
+        collect_x(p, par);
         download(p, F, x_dev, p->X[par], cudaMemcpyDeviceToDevice);
         CK(cudaStreamSynchronize(p->st));
     });
@@ -1780,6 +1917,7 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
                      const double* g, double* u) {
     return guarded([&] {
         checked(p);
+        single(p, "mg_cycle");
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "mg_cycle");
         check_smoother(*spec);
@@ -1807,6 +1945,7 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
 int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y) {
     return guarded([&] {
         checked(p);
+        single(p, "apply");
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "apply");
         Lev& L = p->lev(level);
@@ -1824,6 +1963,7 @@ int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y) {
 int gmg_dev_residual(gmg_problem* p, int level, const double* x, const double* b, double* r) {
     return guarded([&] {
         checked(p);
+        single(p, "residual");
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "residual");
         Lev& L = p->lev(level);
@@ -1839,6 +1979,7 @@ int gmg_dev_smooth_step(gmg_problem* p, int level, int kind, double somega, doub
                         const double* x, const double* b, double* out) {
     return guarded([&] {
         checked(p);
+        single(p, "smooth_step");
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "smooth_step");
         gmg_cycle_desc sp{};
@@ -1867,6 +2008,7 @@ int gmg_dev_smooth_step(gmg_problem* p, int level, int kind, double somega, doub
 int gmg_dev_restriction(gmg_problem* p, int fine_level, const double* fine, double* coarse) {
     return guarded([&] {
         checked(p);
+        single(p, "restriction");
         std::lock_guard<std::mutex> lk(p->mu);
         if (fine_level < 2 || fine_level > p->L) throw std::logic_error("restriction: levels are not parent and child");
         Lev& F = p->lev(fine_level);
@@ -1881,6 +2023,7 @@ int gmg_dev_restriction(gmg_problem* p, int fine_level, const double* fine, doub
 int gmg_dev_prolongation(gmg_problem* p, int coarse_level, const double* coarse, double* fine) {
     return guarded([&] {
         checked(p);
+        single(p, "prolongation");
         std::lock_guard<std::mutex> lk(p->mu);
         if (coarse_level < 1 || coarse_level >= p->L)
             throw std::logic_error("prolongation: levels are not parent and child");
@@ -1898,6 +2041,7 @@ int gmg_dev_prolongation(gmg_problem* p, int coarse_level, const double* coarse,
 int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* d, const double* corr, double* omega) {
     return guarded([&] {
         checked(p);
+        single(p, "adaptive_omega");
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "adaptive_omega");
         Lev& L = p->lev(level);
@@ -1929,6 +2073,7 @@ int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* d, const dou
 int gmg_dev_coarse_solve(gmg_problem* p, const double* b, double* x) {
     return guarded([&] {
         checked(p);
+        single(p, "coarse_solve");
         std::lock_guard<std::mutex> lk(p->mu);
         Lev& L = p->lev(1);
         upload(p, L, L.buf[GRHS], b, cudaMemcpyHostToDevice);
@@ -1966,6 +2111,7 @@ static void flat_sum(gmg_problem* p, long long n, const double* a, const double*
 int gmg_dev_norm_l2(gmg_problem* p, long long n, const double* v, int mode, double* out) {
     return guarded([&] {
         checked(p);
+        single(p, "norm_l2");
         std::lock_guard<std::mutex> lk(p->mu);
         double s = 0.0;
         flat_sum(p, n, v, nullptr, mode, &s);
@@ -1976,6 +2122,7 @@ int gmg_dev_norm_l2(gmg_problem* p, long long n, const double* v, int mode, doub
 int gmg_dev_dot(gmg_problem* p, long long n, const double* a, const double* b, int mode, double* out) {
     return guarded([&] {
         checked(p);
+        single(p, "dot");
         std::lock_guard<std::mutex> lk(p->mu);
         flat_sum(p, n, a, b, mode, out);
     });
@@ -1984,6 +2131,7 @@ int gmg_dev_dot(gmg_problem* p, long long n, const double* a, const double* b, i
 int gmg_dev_axpy(gmg_problem* p, long long n, double alpha, const double* x, double* y) {
     return guarded([&] {
         checked(p);
+        single(p, "axpy");
         std::lock_guard<std::mutex> lk(p->mu);
         if (n <= 0) return;
         double *dx = nullptr, *dy = nullptr;
@@ -2004,6 +2152,7 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
                           double* bytes) {
     return guarded([&] {
         checked(p);
+        single(p, "time_smoother");
         std::lock_guard<std::mutex> lk(p->mu);
         if (p->L < 2) throw std::logic_error("time_smoother: needs >= 2 levels");
         const int L = p->L;
@@ -2090,6 +2239,36 @@ int gmg_host_problem_create(int num_levels, int cnx, int cny, double gx, double 
         }
         gmg_problem_desc pd{num_levels, d.data(), device};
         create_problem(&pd, out);
+    });
+}
+
+int gmg_host_problem_create_slabs(int num_levels, int cnx, int cny, double gx, double gy, int coords, double alpha,
+                                  double beta, int device, const gmg_slab_desc* slabs, gmg_problem** out) {
+    return guarded([&] {
+        std::vector<gmg_host::Level> lv = gmg_host::build_problem(num_levels, cnx, cny, gx, gy, coords, alpha, beta);
+        std::vector<gmg_level_desc> d(lv.size());
+        for (size_t q = 0; q < lv.size(); ++q) {
+            d[q] = gmg_level_desc{lv[q].level, lv[q].nx, lv[q].ny, lv[q].x.data(), lv[q].y.data(),
+                                  lv[q].c.data(), lv[q].n.data(), lv[q].s.data(), lv[q].e.data(),
+                                  lv[q].w.data()};
+        }
+        gmg_problem_desc pd{num_levels, d.data(), device};
+        create_slabs(&pd, slabs, out);
+    });
+}
+
+int gmg_host_slab_plan(int num_levels, const int* ny, int world, int min_rows, int halo, int* first_sharded, int* w0,
+                       int* w1) {
+    return guarded([&] {
+        if (num_levels < 1 || world < 1) throw std::invalid_argument("slab_plan: bad sizes");
+        const gmg_host::SlabPlan sp =
+            gmg_host::slab_plan(std::vector<int>(ny, ny + num_levels), world, min_rows, halo);
+        *first_sharded = sp.Ls;
+        for (int l = 0; l < num_levels; ++l)
+            for (int r = 0; r < world; ++r) {
+                w0[l * world + r] = sp.w0[l][r];
+                w1[l * world + r] = sp.w1[l][r];
+            }
     });
 }
 

@@ -51,7 +51,8 @@ EXPORTS = [
     "gmg_dev_smooth_step", "gmg_dev_restriction", "gmg_dev_prolongation", "gmg_dev_adaptive_omega",
     "gmg_dev_coarse_solve", "gmg_dev_norm_l2", "gmg_dev_dot", "gmg_dev_axpy",
     "gmg_dev_time_smoother", "gmg_dev_cycle_kernel_count", "gmg_dev_seqsum_stats", "gmg_host_problem_create",
-    "gmg_host_random_vector", "gmg_host_seqsum_emulate",
+    "gmg_host_random_vector", "gmg_host_seqsum_emulate", "gmg_dev_problem_create_slabs", "gmg_dist_unique_id",
+    "gmg_dev_dist_info", "gmg_dev_level_window", "gmg_host_problem_create_slabs", "gmg_host_slab_plan",
 ]
 
 
@@ -101,6 +102,10 @@ class _LevelDesc(C.Structure):
 
 class _ProblemDesc(C.Structure):
     _fields_ = [("num_levels", C.c_int), ("levels", C.POINTER(_LevelDesc)), ("device", C.c_int)]
+
+
+class _SlabDesc(C.Structure):
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("min_rows", C.c_int), ("nccl_id", C.c_void_p)]
 
 
 class _CycleDesc(C.Structure):
@@ -156,6 +161,16 @@ def lib() -> C.CDLL:
                                               C.c_int, C.c_double, C.c_double, C.c_int,
                                               C.POINTER(C.c_void_p)]
         L.gmg_host_random_vector.argtypes = [C.c_longlong, C.c_uint, _dp]
+        L.gmg_dev_problem_create_slabs.argtypes = [C.POINTER(_ProblemDesc), C.POINTER(_SlabDesc),
+                                                   C.POINTER(C.c_void_p)]
+        L.gmg_dist_unique_id.argtypes = [C.c_char_p]
+        L.gmg_dev_dist_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.gmg_dev_level_window.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.gmg_host_problem_create_slabs.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                                    C.c_int, C.c_double, C.c_double, C.c_int,
+                                                    C.POINTER(_SlabDesc), C.POINTER(C.c_void_p)]
+        L.gmg_host_slab_plan.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.gmg_host_seqsum_emulate.argtypes = [C.c_longlong, _dp, C.c_int, C.c_int, _dp,
                                               C.POINTER(C.c_longlong)]
         _lib = L
@@ -177,6 +192,42 @@ def _arr(a, n=None) -> np.ndarray:
 
 def _p(a: np.ndarray):
     return a.ctypes.data_as(_dp)
+
+
+@dataclass
+class Slabs:
+    """Row-slab distribution of a problem (gmg_slab_desc): rank=None puts all `world`
+    slabs in this process on one GPU (virtual ranks); rank>=0 is this process's slab
+    of an NCCL group whose id (bytes from unique_id() on rank 0) is shared by the caller."""
+    world: int
+    rank: Optional[int] = None
+    min_rows: int = 255
+    nccl_id: Optional[bytes] = None
+
+    def _c(self):
+        buf = C.create_string_buffer(self.nccl_id, 128) if self.nccl_id is not None else None
+        sd = _SlabDesc(self.world, -1 if self.rank is None else self.rank, self.min_rows,
+                       C.cast(buf, C.c_void_p) if buf is not None else None)
+        return sd, buf
+
+
+def unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 of a row-slab group)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().gmg_dist_unique_id(buf))
+    return buf.raw
+
+
+def slab_plan(ny, world: int, min_rows: int = 255, halo: int = 4):
+    """The row-slab partition (host only): (first sharded level, w0[level][rank], w1[level][rank])."""
+    L = len(ny)
+    nya = (C.c_int * L)(*ny)
+    w0 = (C.c_int * (L * world))()
+    w1 = (C.c_int * (L * world))()
+    first = C.c_int()
+    _check(lib().gmg_host_slab_plan(L, nya, world, min_rows, halo, C.byref(first), w0, w1))
+    return (first.value, [[w0[l * world + r] for r in range(world)] for l in range(L)],
+            [[w1[l * world + r] for r in range(world)] for l in range(L)])
 
 
 @dataclass
@@ -221,13 +272,18 @@ class MultilevelProblem:
     """Device-resident operators of every level plus the level-1 factorization."""
 
     def __init__(self, levels: int, coarse_nx: int = 1, coarse_ny: int = 1, grading=(1.0, 1.0),
-                 coords: str = "cartesian", alpha: float = 1.0, beta: float = 1.0, device: int = 0):
+                 coords: str = "cartesian", alpha: float = 1.0, beta: float = 1.0, device: int = 0,
+                 slabs: Optional["Slabs"] = None):
         h = C.c_void_p()
         if coords not in COORDS:
             raise InvalidArgument(f"coords: unknown coordinate system '{coords}'")
-        _check(lib().gmg_host_problem_create(levels, coarse_nx, coarse_ny, float(grading[0]),
-                                             float(grading[1]), COORDS[coords], float(alpha),
-                                             float(beta), device, C.byref(h)))
+        args = (levels, coarse_nx, coarse_ny, float(grading[0]), float(grading[1]), COORDS[coords], float(alpha),
+                float(beta), device)
+        if slabs is None:
+            _check(lib().gmg_host_problem_create(*args, C.byref(h)))
+        else:
+            sd, _keep = slabs._c()
+            _check(lib().gmg_host_problem_create_slabs(*args, C.byref(sd), C.byref(h)))
         self._init(h)
 
     @classmethod
@@ -258,6 +314,17 @@ class MultilevelProblem:
     def n(self, level: int) -> int:
         nx, ny = self.shapes[level]
         return nx * ny
+
+    def dist_info(self):
+        """(rank, world, first sharded level) of a row-slab handle; (0, 1, L+1) otherwise."""
+        r, w, f = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().gmg_dev_dist_info(self._h, C.byref(r), C.byref(w), C.byref(f)))
+        return r.value, w.value, f.value
+
+    def level_window(self, level: int):
+        a, b = C.c_int(), C.c_int()
+        _check(lib().gmg_dev_level_window(self._h, level, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def coef_kind(self, level: int) -> str:
         return {0: "const", 1: "rowx", 2: "field"}.get(lib().gmg_dev_level_coef_kind(self._h, level), "?")
