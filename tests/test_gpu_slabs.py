@@ -90,3 +90,20 @@ def test_slab_handle_rejects_unsharded_ops(gpu):
         gmg.apply(slab, 6, np.zeros(n))
     with pytest.raises(gmg.Unsupported, match="jacobi"):
         gmg.solve(slab, np.ones(n), gmg.CycleSpec(smoother="gauss_seidel"), np.zeros(n))
+
+
+def test_nccl_group_of_one(gpu):
+    # the multi-process entry point end to end on one GPU: NCCL loaded and a
+    # one-rank communicator created (nothing is sharded with one rank)
+    uid = gmg.unique_id()
+    assert len(uid) == 128
+    args = (7, 1, 1, (1.0, 1.0), "cartesian", 1.0, 1.0)
+    p1 = gmg.MultilevelProblem(*args, slabs=gmg.Slabs(world=1, rank=0, min_rows=15, nccl_id=uid))
+    assert p1.dist_info() == (0, 1, 8)
+    single = gmg.MultilevelProblem(*args)
+    n = single.n(7)
+    b = gmg.random_vector(n, 1)
+    spec = gmg.CycleSpec(smoother="jacobi", tolerance=1e-10)
+    x1, x2 = np.zeros(n), np.zeros(n)
+    r1, r2 = gmg.solve(p1, b, spec, x1), gmg.solve(single, b, spec, x2)
+    assert r1.residual_history == r2.residual_history and bits_equal(x1, x2)
