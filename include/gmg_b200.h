@@ -195,7 +195,8 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
  * [0] sums, [1] records, [2] chain SM cycles, [3] of which re-walks,
  * [4] break adds, [5] re-walked ranges, [6] terms re-walked, [7] chunks,
  * [8..12] walk-kernel SM cycles per phase (load, prefix look-back, thread walk,
- * block merge, run/offset look-back), [13] walk CTAs. out16 holds 16 values. */
+ * block merge, run/offset look-back), [13] walk CTAs, [14] literal (dense-break)
+ * chunks among [5], [15] their cycles. out16 holds 16 values. */
 int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out16);
 /* Number of kernels one solver cycle launches (from the captured graph). */
 int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* count);

@@ -447,38 +447,43 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 // walk is not bound by one memory round trip per batch.
 constexpr int kSsRing = 8;
 
-// Literal left-to-right adds over terms [k0, k1) of sum s, by one warp: lane 0's
-// order of adds on shuffled terms (every lane computes the same chain).
+// Literal left-to-right adds over terms [k0, k1) of sum s, by one warp. The
+// adds are one dependent fp64 chain (8 cycles each on B200), so nothing else may
+// sit on it: the warp stages kSsLitTile terms in shared memory (coalesced;
+// the next tile's loads are in flight in registers meanwhile) and every lane
+// runs the same chain from broadcast shared-memory reads.
+constexpr int kSsLitTile = 1024;
 template <class TG>
-__device__ double literal_sum(const TG& tg, int s, double a, long long k0, long long k1) {
+__device__ double literal_sum(const TG& tg, int s, double a, long long k0, long long k1, double* tile) {
     const int lane = threadIdx.x & 31;
-    double ring[kSsRing];
+    constexpr int PER = kSsLitTile / 32;
+    double r[PER];
+    auto load = [&](long long k) {
 #pragma unroll
-    for (int r = 0; r < kSsRing; ++r) {
-        const long long k = k0 + r * 32 + lane;
-        ring[r] = k < k1 ? tg.term(s, k) : 0.0;
-    }
-    for (long long k = k0; k < k1; k += 32 * kSsRing) {
-#pragma unroll
-        for (int r = 0; r < kSsRing; ++r) {
-            const long long kb = k + r * 32;
-            if (kb >= k1) break;
-            const double cur = ring[r];
-            const long long kn = kb + 32 * kSsRing + lane;
-            ring[r] = kn < k1 ? tg.term(s, kn) : 0.0;
-            const int m = (int)min(32LL, k1 - kb);
-            if (m == 32) {
-                double v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __shfl_sync(0xffffffffu, cur, j);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) a = a + v[j];
-            } else {
-                for (int j = 0; j < m; ++j) a = a + __shfl_sync(0xffffffffu, cur, j);
-            }
+        for (int j = 0; j < PER; ++j) {
+            const long long kk = k + j * 32 + lane;
+            r[j] = kk < k1 ? tg.term(s, kk) : 0.0;
         }
+    };
+    load(k0);
+    for (long long k = k0; k < k1; k += kSsLitTile) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) tile[j * 32 + lane] = r[j];
+        __syncwarp();
+        if (k + kSsLitTile < k1) load(k + kSsLitTile);
+        const int m = (int)min((long long)kSsLitTile, k1 - k);
+        int j = 0;
+        for (; j + 8 <= m; j += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = tile[j + q];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a = a + v[q];
+        }
+        for (; j < m; ++j) a = a + tile[j];
+        __syncwarp();
     }
-    return __shfl_sync(0xffffffffu, a, 0);
+    return a;
 }
 
 // Exact sum of terms [k0, k1) added to sv, by one warp with the integer model:
@@ -557,6 +562,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
     gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
     __shared__ longlong2 cD[32];  // per record of the current group: signed run steps (parity 0, 1)
     __shared__ double2 cPB[32];   // break term (-0.0 if none), tie flag
+    __shared__ double ltile[kSsLitTile];  // literal re-sum staging
     const int s = blockIdx.x;
     const SsState& S = sts.s[s];
     const int t = threadIdx.x;
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
     // and the integer state is M = s * 2^(1075-E), also exact.
     double sv = start ? start[s] : 0.0;  // exact state entering this range (earlier row slabs)
     long long prev = -1;  // global index of the last element consumed
-    unsigned long long n_brk = 0, n_lit = 0, n_litterms = 0, cyc_lit = 0;
+    unsigned long long n_brk = 0, n_lit = 0, n_litterms = 0, cyc_lit = 0, n_dense = 0, cyc_dense = 0;
     const long long cyc0 = clock64();
     for (int b = 0; b < nb; ++b) {
         const gmg_ss::Rec* A = buf + (b & 1) * kSsBatch;
@@ -656,10 +662,14 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
                 // binades often, and there the literal chain (~6 cycles/term) beats the
                 // warp's integer walk, which restarts at every break
                 (void)lit_f;
-                const double s1 = literal_sum(tg, s, sv, pf + 1, k1);
+                const double s1 = literal_sum(tg, s, sv, pf + 1, k1, ltile);
                 cyc_lit += clock64() - c0;
                 ++n_lit;
                 n_litterms += k1 - (pf + 1);
+                if (lit_f) {
+                    ++n_dense;
+                    cyc_dense += clock64() - c0;
+                }
                 sv = brk_f ? s1 + rf.pb : s1;
                 prev = kb_f;
                 q0 += f + 1;
@@ -682,6 +692,8 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
             atomicAdd(S.stats + 4, n_brk);
             atomicAdd(S.stats + 5, n_lit);
             atomicAdd(S.stats + 6, n_litterms);
+            atomicAdd(S.stats + 14, n_dense);
+            atomicAdd(S.stats + 15, cyc_dense);
             atomicAdd(S.stats + 7, (unsigned long long)((n + kSsC - 1) / kSsC));
         }
     }

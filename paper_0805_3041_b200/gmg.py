@@ -499,5 +499,5 @@ def seqsum_stats(prob: MultilevelProblem, reset: bool = True) -> dict:
     _check(lib().gmg_dev_seqsum_stats(prob._h, int(reset), a))
     keys = ["sums", "records", "chain_cycles", "rewalk_cycles", "break_adds", "rewalks",
             "rewalk_terms", "chunks", "walk_load", "walk_prefix_lookback", "walk_thread_walk",
-            "walk_block_merge", "walk_run_lookback", "walk_ctas"]
+            "walk_block_merge", "walk_run_lookback", "walk_ctas", "dense_chunks", "dense_cycles"]
     return dict(zip(keys, list(a)))
