@@ -1,0 +1,259 @@
+// k_smooth4: the fused M-step Jacobi smoother for large levels, built to cut
+// instructions per point (the row-streaming kernels before it were issue-bound
+// at ~60 instructions per point update).
+//
+//   * Every warp is an independent column strip of 128 columns (4 per lane),
+//     H = M rounded up to even halo columns on each side; horizontal neighbours
+//     come from the adjacent lanes by shuffles, so there is no block barrier
+//     and no shared-memory exchange in the row loop.
+//   * Inputs (u, g, and the two coarse rows a prolongation needs) stream
+//     through per-warp shared-memory rings filled by cp.async (zero-fill
+//     outside the interior), 3 rows ahead.
+//   * The row loop is unrolled by 3 so the per-level 3-row register windows
+//     rotate by renaming instead of moves.
+//   * Domain masks only where a warp strip or a row touches the boundary
+//     (warp-uniform branches).
+// Arithmetic per point is jacobi_point (march.cuh) on the same operands as the
+// reference, so results are bit-identical to the other smoother kernels.
+#pragma once
+
+#include "march.cuh"
+#include "march2.cuh"
+
+namespace gmg_dev {
+
+constexpr int kS4W = 4;  // warps per CTA (independent strips)
+
+template <int SK>
+struct Smooth4Smem {
+    static constexpr bool HAS_U = SK == K3_U || SK == K3_CORRECT;
+    static constexpr bool HAS_C = SK == K3_PROLONG || SK == K3_CORRECT;
+    static constexpr int D = 4;
+    // [slot][half][lane]: lane's columns 4l..4l+1 in half 0, 4l+2..4l+3 in half 1
+    // (16-B lane stride: conflict-free 128-bit accesses)
+    double2 g[D][2][32];
+    double2 u[HAS_U ? D : 1][2][32];
+    double c[HAS_C ? D : 1][68];  // coarse rows, slot = coarse row & (D-1)
+};
+
+template <int M, int SK, class Coef>
+__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
+    k_smooth4(Grid fg, Coef A, const double* __restrict__ u, Prolong P, OmegaSrc om, const double* __restrict__ g,
+              double* __restrict__ out, double omega_damp, int seg) {
+    using SM = Smooth4Smem<SK>;
+    constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C;
+    constexpr int D = SM::D;
+    constexpr int H = (M + 1) & ~1;  // halo columns, even: 16-B aligned strips
+    constexpr int OW = 128 - 2 * H;  // columns each strip produces
+    constexpr int ML = M > 0 ? M : 1;
+    extern __shared__ __align__(16) unsigned char sm4raw[];
+    SM& S = reinterpret_cast<SM*>(sm4raw)[threadIdx.x >> 5];
+
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * kS4W + (threadIdx.x >> 5);
+    const int i0 = strip * OW - H;
+    if (i0 + H >= fg.nx) return;  // warp-uniform; the kernel has no block barriers
+    const int i = i0 + 4 * lane;
+    const int nx = fg.nx, ny = fg.ny;
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
+    const bool edge = i0 < 0 || i0 + 128 > nx;
+    bool cin[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cin[k] = i + k >= 0 && i + k < nx;
+    const int m0 = i0 / 2 - 1;  // first coarse column staged (i0 even)
+    const double tX0 = (HAS_C && cin[0]) ? __ldg(P.tx + i) : 0.0;
+    const double tX2 = (HAS_C && cin[2]) ? __ldg(P.tx + i + 2) : 0.0;
+    double omega = 0.0;
+    if constexpr (SK == K3_CORRECT) omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0);
+
+    const int Jbeg = j0 - M;
+    const int Jend = j1 - 1 + M;
+    auto slot_of = [](int J) { return (J + 8) & (D - 1); };
+    auto chunk_bytes = [&](int c) { return (c >= 0 && c < nx) ? (c + 1 < nx ? 16 : 8) : 0; };
+    auto stage_crow = [&](int q) {
+        double* dst = S.c[(q + 8) & (D - 1)];
+        stage_coarse(dst + 2 * lane, P.uc, P.cg, m0 + 2 * lane, q);
+        stage_coarse(dst + 2 * lane + 1, P.uc, P.cg, m0 + 2 * lane + 1, q);
+        if (lane == 0) stage_coarse(dst + 64, P.uc, P.cg, m0 + 64, q);
+    };
+    auto stage = [&](int J) {
+        const int sl = slot_of(J);
+        const bool row_in = J >= 0 && J < ny;
+        const long long rb = (long long)J * fg.pitch;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = i + 2 * h;
+            const int bytes = row_in ? chunk_bytes(c) : 0;
+            cpa16(&S.g[sl][h][lane], bytes ? g + rb + c : g, bytes);
+            if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], bytes ? u + rb + c : u, bytes);
+        }
+        if constexpr (HAS_C) {
+            // fine row J needs coarse rows floor(J/2)-1 (J even only) and floor(J/2):
+            // a new coarse row every other fine row, staged once
+            if (((J + 8) & 1) == 0) stage_crow((J + 8) / 2 - 4);
+        }
+        cpa_commit();
+    };
+    // the source value of row J for this lane's 4 columns (zero outside the interior)
+    auto source = [&](int J, int sl, double (&nv)[4]) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nv[k] = 0.0;
+        if (J < 0 || J >= ny) return;
+        if constexpr (SK == K3_U) {
+            const double2 a = S.u[sl][0][lane];
+            const double2 b = S.u[sl][1][lane];
+            nv[0] = a.x;
+            nv[1] = a.y;
+            nv[2] = b.x;
+            nv[3] = b.y;
+        }
+        if constexpr (HAS_C) {
+            const int qf = (J + 8) / 2 - 4;  // floor(J/2)
+            const bool even = ((J + 8) & 1) == 0;
+            const double* ca = &S.c[((even ? qf - 1 : qf) + 8) & (D - 1)][2 * lane];
+            const double* cb = &S.c[(qf + 8) & (D - 1)][2 * lane];
+            Pair2Raw r;
+            r.ty = ((J + 1) & 1) ? __ldg(P.ty + J) : 0.0;
+            r.a = ca[0];
+            r.b = ca[1];
+            r.c = cb[0];
+            r.d = cb[1];
+            const double2 p0 = prolong2_make(r, i, J, nx, tX0);
+            r.a = ca[1];
+            r.b = ca[2];
+            r.c = cb[1];
+            r.d = cb[2];
+            const double2 p1 = prolong2_make(r, i + 2, J, nx, tX2);
+            if constexpr (SK == K3_PROLONG) {
+                nv[0] = p0.x;
+                nv[1] = p0.y;
+                nv[2] = p1.x;
+                nv[3] = p1.y;
+            } else {
+                const double2 a = S.u[sl][0][lane];
+                const double2 b = S.u[sl][1][lane];
+                nv[0] = a.x + omega * p0.x;
+                nv[1] = a.y + omega * p0.y;
+                nv[2] = b.x + omega * p1.x;
+                nv[3] = b.y + omega * p1.y;
+            }
+        }
+        if (edge) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (!cin[k]) nv[k] = 0.0;
+        }
+    };
+    auto store = [&](int R, const double (&v)[4]) {
+        double* o = out + (long long)R * fg.pitch + i;
+        if (!edge && lane > 0 && lane < 31) {  // all four columns are produced here
+            *reinterpret_cast<double2*>(o) = make_double2(v[0], v[1]);
+            *reinterpret_cast<double2*>(o + 2) = make_double2(v[2], v[3]);
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int c = 4 * lane + k;
+            if (c >= H && c < 128 - H && cin[k]) o[k] = v[k];
+        }
+    };
+
+    if constexpr (HAS_C) {
+        // coarse rows of fine rows Jbeg .. Jbeg+D-2 that stage() itself will not fetch
+        // Jbeg even: floor(Jbeg/2)-1 (its pair partner comes with stage(Jbeg));
+        // Jbeg odd: floor(Jbeg/2)
+        const int qf = (Jbeg + 8) / 2 - 4;
+        stage_crow(((Jbeg + 8) & 1) ? qf : qf - 1);
+    }
+#pragma unroll
+    for (int p = 0; p < D - 1; ++p) stage(Jbeg + p);
+    cpa_wait<D - 2>();
+    __syncwarp();
+
+    double w[ML][3][4];
+    double gr[ML][4];
+#pragma unroll
+    for (int l = 0; l < ML; ++l)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w[l][0][k] = w[l][1][k] = w[l][2][k] = 0.0;
+            gr[l][k] = 0.0;
+        }
+
+    // one row J; PH = (J - Jbeg) mod 3 names the window slots statically
+    auto row = [&](int J, auto ph) {
+        constexpr int PH = decltype(ph)::value;
+        stage(J + D - 1);  // into the slot of row J-1, read last iteration
+        const int sl = slot_of(J);
+        double nv[4];
+        source(J, sl, nv);
+        if constexpr (M == 0) {
+            if (J >= j0 && J < j1) store(J, nv);
+        } else {
+            double gn[4];
+            {
+                const double2 a = S.g[sl][0][lane];
+                const double2 b = S.g[sl][1][lane];
+                gn[0] = a.x;
+                gn[1] = a.y;
+                gn[2] = b.x;
+                gn[3] = b.y;
+            }
+#pragma unroll
+            for (int l = 0; l < M; ++l) {
+                const int sn = (PH - l + 30) % 3;      // newest row J-l
+                const int sc = (PH - l - 1 + 30) % 3;  // centre row J-l-1
+                const int sd = (PH - l - 2 + 30) % 3;  // row J-l-2
+#pragma unroll
+                for (int k = 0; k < 4; ++k) w[l][sn][k] = nv[k];
+                const int R = J - l - 1;
+                const double xl = __shfl_up_sync(0xffffffffu, w[l][sc][3], 1);
+                const double xr = __shfl_down_sync(0xffffffffu, w[l][sc][0], 1);
+                double y[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double xw = k == 0 ? xl : w[l][sc][k - 1];
+                    const double xe = k == 3 ? xr : w[l][sc][k + 1];
+                    y[k] = jacobi_point(A, i + k, R, w[l][sc][k], xw, xe, w[l][sd][k], w[l][sn][k], gr[l][k],
+                                        omega_damp);
+                }
+                if (R < 0 || R >= ny) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) y[k] = 0.0;
+                } else if (edge) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (!cin[k]) y[k] = 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nv[k] = y[k];
+            }
+            const int RM = J - M;
+            if (RM >= j0 && RM < j1) store(RM, nv);
+#pragma unroll
+            for (int l = ML - 1; l > 0; --l)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) gr[l][k] = gr[l - 1][k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gr[0][k] = gn[k];
+        }
+        cpa_wait<D - 2>();  // row J+1 has landed (for this lane)
+        __syncwarp();       // ... for every lane; slot of row J is free again
+    };
+    for (int J = Jbeg; J <= Jend; J += 3) {
+        row(J, std::integral_constant<int, 0>{});
+        if (J + 1 > Jend) break;
+        row(J + 1, std::integral_constant<int, 1>{});
+        if (J + 2 > Jend) break;
+        row(J + 2, std::integral_constant<int, 2>{});
+    }
+    cpa_wait<0>();
+}
+
+template <int SK>
+constexpr size_t smooth4_smem() {
+    return sizeof(Smooth4Smem<SK>) * kS4W;
+}
+
+}  // namespace gmg_dev

@@ -32,6 +32,7 @@
 #include "linesm.cuh"
 #include "march.cuh"
 #include "march2.cuh"
+#include "march4.cuh"
 #include "seqsum.cuh"
 
 using namespace gmg_dev;
@@ -463,12 +464,42 @@ void launch_smooth3_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     CK(cudaGetLastError());
 }
 
-// levels at least this wide stream their inputs through the cp.async ring (k_smooth3)
+template <int M, int SK, class Coef>
+void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* u, const double* uc,
+                      OmegaSrc om, const double* g, double* out, double wd) {
+    constexpr int H = (M + 1) & ~1;
+    constexpr int OW = 128 - 2 * H;
+    constexpr size_t smem = smooth4_smem<SK>();
+    static bool attr = false;
+    if (!attr) {
+        set_smem(k_smooth4<M, SK, Coef>, smem);
+        attr = true;
+    }
+    Prolong P{};
+    if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
+    const int seg = seg_rows(L.nx, L.rows());
+    const int strips = (L.nx + OW - 1) / OW;
+    dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
+    k_smooth4<M, SK, Coef><<<grid, kS4W * 32, smem, p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
+    CK(cudaGetLastError());
+}
+
+// levels at least this wide use the strip-per-warp smoother (k_smooth4)
 constexpr int kRingMinNx = 255;
+static int g_smooth_variant = 4;  // 4: k_smooth4, 3: k_smooth3 (GMG_SMOOTH_KERNEL=3 selects it)
 
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
                        double* out, double wd) {
+    if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
+        switch (s.kind) {
+            case S_ZERO: launch_smooth4_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
+            case S_U: launch_smooth4_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
+            case S_PROLONG: launch_smooth4_t<M, K3_PROLONG>(p, L, A, nullptr, s.uc, s.om, g, out, wd); return;
+            case S_CORRECT: launch_smooth4_t<M, K3_CORRECT>(p, L, A, s.u, s.uc, s.om, g, out, wd); return;
+            default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
+        }
+    }
     if (L.nx >= kRingMinNx) {
         switch (s.kind) {
             case S_ZERO: launch_smooth3_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
