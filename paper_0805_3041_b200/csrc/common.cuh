@@ -62,6 +62,12 @@ struct CoefConst {
     }
 };
 
+// CoefConst whose c is a power of two: the division is the exact multiplication
+// unconditionally (chosen on the host, so kernels carry no per-point branch).
+struct CoefConstP2 : CoefConst {
+    __device__ __forceinline__ double div_by_c(double r, int, int) const { return r * inv_c; }
+};
+
 struct CoefRowX {
     const double *c, *w, *e, *s, *n;  // length nx each
     __device__ __forceinline__ void load(int i, int, double& C, double& W, double& E, double& S,

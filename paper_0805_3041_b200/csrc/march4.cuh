@@ -71,6 +71,11 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
     const int Jend = j1 - 1 + M;
     auto slot_of = [](int J) { return (J + 8) & (D - 1); };
     auto chunk_bytes = [&](int c) { return (c >= 0 && c < nx) ? (c + 1 < nx ? 16 : 8) : 0; };
+    const int cb0 = chunk_bytes(i), cb1 = chunk_bytes(i + 2);
+    // running pointers of the next row to stage / the next row to store
+    const long long pitch = fg.pitch;
+    long long soff = (long long)Jbeg * pitch + i;
+    long long roff = soff;
     auto stage_crow = [&](int q) {
         double* dst = S.c[(q + 8) & (D - 1)];
         stage_coarse(dst + 2 * lane, P.uc, P.cg, m0 + 2 * lane, q);
@@ -80,14 +85,14 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
     auto stage = [&](int J) {
         const int sl = slot_of(J);
         const bool row_in = J >= 0 && J < ny;
-        const long long rb = (long long)J * fg.pitch;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int c = i + 2 * h;
-            const int bytes = row_in ? chunk_bytes(c) : 0;
-            cpa16(&S.g[sl][h][lane], bytes ? g + rb + c : g, bytes);
-            if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], bytes ? u + rb + c : u, bytes);
+            const int bytes = row_in ? (h ? cb1 : cb0) : 0;
+            const long long o = bytes ? soff + 2 * h : 0;
+            cpa16(&S.g[sl][h][lane], g + o, bytes);
+            if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], u + o, bytes);
         }
+        soff += pitch;
         if constexpr (HAS_C) {
             // fine row J needs coarse rows floor(J/2)-1 (J even only) and floor(J/2):
             // a new coarse row every other fine row, staged once
@@ -145,8 +150,8 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                 if (!cin[k]) nv[k] = 0.0;
         }
     };
-    auto store = [&](int R, const double (&v)[4]) {
-        double* o = out + (long long)R * fg.pitch + i;
+    auto store = [&](long long off, const double (&v)[4]) {
+        double* o = out + off;
         if (!edge && lane > 0 && lane < 31) {  // all four columns are produced here
             *reinterpret_cast<double2*>(o) = make_double2(v[0], v[1]);
             *reinterpret_cast<double2*>(o + 2) = make_double2(v[2], v[3]);
@@ -186,10 +191,12 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
         constexpr int PH = decltype(ph)::value;
         stage(J + D - 1);  // into the slot of row J-1, read last iteration
         const int sl = slot_of(J);
+        const long long rJ = roff;  // offset of row J in this lane's columns
+        roff += pitch;
         double nv[4];
         source(J, sl, nv);
         if constexpr (M == 0) {
-            if (J >= j0 && J < j1) store(J, nv);
+            if (J >= j0 && J < j1) store(rJ, nv);
         } else {
             double gn[4];
             {
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                 for (int k = 0; k < 4; ++k) nv[k] = y[k];
             }
             const int RM = J - M;
-            if (RM >= j0 && RM < j1) store(RM, nv);
+            if (RM >= j0 && RM < j1) store(rJ - M * pitch, nv);
 #pragma unroll
             for (int l = ML - 1; l > 0; --l)
 #pragma unroll

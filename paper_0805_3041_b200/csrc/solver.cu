@@ -491,6 +491,15 @@ static int g_smooth_variant = 4;  // 4: k_smooth4, 3: k_smooth3 (GMG_SMOOTH_KERN
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
                        double* out, double wd) {
+    if constexpr (std::is_same<Coef, CoefConstP2>::value) {
+        switch (s.kind) {
+            case S_ZERO: launch_smooth4_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
+            case S_U: launch_smooth4_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
+            case S_PROLONG: launch_smooth4_t<M, K3_PROLONG>(p, L, A, nullptr, s.uc, s.om, g, out, wd); return;
+            case S_CORRECT: launch_smooth4_t<M, K3_CORRECT>(p, L, A, s.u, s.uc, s.om, g, out, wd); return;
+            default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
+        }
+    } else {
     if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
         switch (s.kind) {
             case S_ZERO: launch_smooth4_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
@@ -529,11 +538,24 @@ void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const Smooth
         default:
             throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
     }
+    }
 }
 
 // One launch of M <= 4 Jacobi steps.
 void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, const double* g, double* out,
                    double wd) {
+    if (L.kind == 0 && L.cconst.c_pow2 && L.nx >= kRingMinNx && g_smooth_variant == 4) {
+        CoefConstP2 A;
+        static_cast<CoefConst&>(A) = L.cconst;
+        switch (M) {
+            case 0: launch_smooth_src<0>(p, L, A, s, g, out, wd); return;
+            case 1: launch_smooth_src<1>(p, L, A, s, g, out, wd); return;
+            case 2: launch_smooth_src<2>(p, L, A, s, g, out, wd); return;
+            case 3: launch_smooth_src<3>(p, L, A, s, g, out, wd); return;
+            case 4: launch_smooth_src<4>(p, L, A, s, g, out, wd); return;
+            default: throw GmgError{GMG_ERR_LOGIC, "smooth: M > 4"};
+        }
+    }
     with_coef(L, [&](const auto& A) {
         switch (M) {
             case 0: launch_smooth_src<0>(p, L, A, s, g, out, wd); break;
