@@ -258,6 +258,202 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
     cpa_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// k_resid4: residual d = g - A x0 (stencil.cpp:148-153) of x0 = x or x + e
+// (fcycle_pass's x + 1.0*e, cycle.cpp:139-140), optionally storing d and x0,
+// and optionally the full-weighting restriction of d into the coarse right-hand
+// side (transfer.cpp:72-101) — one pass, the warp-strip layout of k_smooth4.
+// ---------------------------------------------------------------------------
+template <bool SUM>
+struct Resid4Smem {
+    static constexpr int D = 4;
+    double2 x[D][2][32];
+    double2 e[SUM ? D : 1][2][32];
+    double2 g[D][2][32];
+};
+
+template <bool SUM, class Coef>
+__global__ void __launch_bounds__(kS4W * 32, 4)
+    k_resid4(Grid fg, Coef A, const double* __restrict__ x, const double* __restrict__ e,
+             const double* __restrict__ g, double* __restrict__ dout, double* __restrict__ x0out, Grid cg,
+             RestrictW rw, double* __restrict__ gc, int seg) {
+    using SM = Resid4Smem<SUM>;
+    constexpr int D = SM::D;
+    constexpr int H = 2;
+    constexpr int OW = 128 - 2 * H;
+    extern __shared__ __align__(16) unsigned char r4raw[];
+    SM& S = reinterpret_cast<SM*>(r4raw)[threadIdx.x >> 5];
+    const bool STORE_D = dout != nullptr, STORE_X0 = x0out != nullptr, RESTRICT = gc != nullptr;
+
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * kS4W + (threadIdx.x >> 5);
+    const int i0 = strip * OW - H;
+    if (i0 + H >= fg.nx) return;  // warp-uniform; no block barriers below
+    const int i = i0 + 4 * lane;
+    const int nx = fg.nx, ny = fg.ny;
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
+    const bool edge = i0 < 0 || i0 + 128 > nx;
+    bool cin[4], cout_[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cin[k] = i + k >= 0 && i + k < nx;
+        const int c = 4 * lane + k;
+        cout_[k] = cin[k] && c >= H && c < 128 - H;
+    }
+    auto chunk_bytes = [&](int c) { return (c >= 0 && c < nx) ? (c + 1 < nx ? 16 : 8) : 0; };
+    const int cb0 = chunk_bytes(i), cb1 = chunk_bytes(i + 2);
+    const long long pitch = fg.pitch;
+    // d is exact from row Jbeg+1 on; the restriction needs it from row j0-1
+    const int Jbeg = j0 - 2;
+    const int Jend = j1 + 1;
+    long long soff = (long long)Jbeg * pitch + i;
+    long long roff = soff;
+    auto slot_of = [](int J) { return (J + 8) & (D - 1); };
+    auto stage = [&](int J) {
+        const int sl = slot_of(J);
+        const bool row_in = J >= 0 && J < ny;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int bytes = row_in ? (h ? cb1 : cb0) : 0;
+            const long long o = bytes ? soff + 2 * h : 0;
+            cpa16(&S.x[sl][h][lane], x + o, bytes);
+            if constexpr (SUM) cpa16(&S.e[sl][h][lane], e + o, bytes);
+            cpa16(&S.g[sl][h][lane], g + o, bytes);
+        }
+        soff += pitch;
+        cpa_commit();
+    };
+    auto store4 = [&](double* base, long long off, const double (&v)[4]) {
+        double* o = base + off;
+        if (!edge && lane > 0 && lane < 31) {
+            *reinterpret_cast<double2*>(o) = make_double2(v[0], v[1]);
+            *reinterpret_cast<double2*>(o + 2) = make_double2(v[2], v[3]);
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (cout_[k]) o[k] = v[k];
+    };
+    // coarse columns of this lane's two odd (centre) fine columns i+1, i+3
+    const int P0 = i / 2, P1 = i / 2 + 1;  // (i even)
+    const bool p0ok = RESTRICT && lane > 0 && i + 1 < nx && P0 >= 0 && P0 < cg.nx;
+    const bool p1ok = RESTRICT && lane < 31 && i + 3 < nx && P1 >= 0 && P1 < cg.nx;
+
+    stage(Jbeg);
+    stage(Jbeg + 1);
+    cpa_wait<1>();
+    __syncwarp();
+
+    double xw[3][4], dw[3][4];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) xw[r][k] = dw[r][k] = 0.0;
+
+    auto row = [&](int J, auto ph) {
+        constexpr int PH = decltype(ph)::value;
+        constexpr int sJ = PH % 3, sJ1 = (PH + 2) % 3, sJ2 = (PH + 1) % 3;  // rows J, J-1, J-2
+        stage(J + 2);  // slot of row J-2: no longer read
+        const int sl = slot_of(J), sl1 = slot_of(J - 1);
+        const long long rJ = roff;
+        roff += pitch;
+        // x0 of row J
+        {
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            if (J >= 0 && J < ny) {
+                const double2 a = S.x[sl][0][lane], b = S.x[sl][1][lane];
+                v[0] = a.x;
+                v[1] = a.y;
+                v[2] = b.x;
+                v[3] = b.y;
+                if constexpr (SUM) {
+                    const double2 c = S.e[sl][0][lane], f = S.e[sl][1][lane];
+                    v[0] = v[0] + 1.0 * c.x;
+                    v[1] = v[1] + 1.0 * c.y;
+                    v[2] = v[2] + 1.0 * f.x;
+                    v[3] = v[3] + 1.0 * f.y;
+                }
+                if (edge) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (!cin[k]) v[k] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) xw[sJ][k] = v[k];
+            if (STORE_X0 && J >= j0 && J < j1) store4(x0out, rJ, v);
+        }
+        // d of row R = J-1
+        const int R = J - 1;
+        {
+            double d[4] = {0.0, 0.0, 0.0, 0.0};
+            if (R >= 0 && R < ny) {
+                const double2 ga = S.g[sl1][0][lane], gb = S.g[sl1][1][lane];
+                const double gv[4] = {ga.x, ga.y, gb.x, gb.y};
+                const double xl = __shfl_up_sync(0xffffffffu, xw[sJ1][3], 1);
+                const double xr = __shfl_down_sync(0xffffffffu, xw[sJ1][0], 1);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const double xe_ = k == 3 ? xr : xw[sJ1][k + 1];
+                    const double xwv = k == 0 ? xl : xw[sJ1][k - 1];
+                    const double ax = stencil_apply(A, i + k, R, xw[sJ1][k], xwv, xe_, xw[sJ2][k], xw[sJ][k]);
+                    d[k] = gv[k] - ax;
+                }
+                if (edge) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (!cin[k]) d[k] = 0.0;
+                }
+            } else {
+                // keep the shuffles warp-uniform: nothing to exchange on rows outside
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dw[sJ1][k] = d[k];
+            if (STORE_D && R >= j0 && R < j1) store4(dout, rJ - pitch, d);
+        }
+        // coarse row Q whose centre fine row 2Q+1 = R-1 lies in the segment
+        if (RESTRICT && ((R & 1) == 0) && R >= 2 && R - 1 >= j0 && R - 1 < j1) {
+            const int Q = R / 2 - 1;
+            // rows dj = -1, 0, +1 are R-2, R-1, R = slots sJ, sJ2, sJ1 of dw
+            const double n0 = __shfl_down_sync(0xffffffffu, dw[sJ][0], 1);
+            const double n1 = __shfl_down_sync(0xffffffffu, dw[sJ2][0], 1);
+            const double n2 = __shfl_down_sync(0xffffffffu, dw[sJ1][0], 1);
+            if (Q < cg.ny) {
+                double* crow = gc + (long long)Q * cg.pitch;
+                if (p0ok) {
+                    crow[P0] = restrict_at(rw, P0, Q, [&](int di, int dj) {
+                        const double* rowv = dj < 0 ? dw[sJ] : (dj == 0 ? dw[sJ2] : dw[sJ1]);
+                        return rowv[1 + di];
+                    });
+                }
+                if (p1ok) {
+                    crow[P1] = restrict_at(rw, P1, Q, [&](int di, int dj) {
+                        const double* rowv = dj < 0 ? dw[sJ] : (dj == 0 ? dw[sJ2] : dw[sJ1]);
+                        if (di < 1) return rowv[3 + di];
+                        return dj < 0 ? n0 : (dj == 0 ? n1 : n2);
+                    });
+                }
+            }
+        }
+        cpa_wait<1>();  // row J+1 has landed
+        __syncwarp();
+    };
+    for (int J = Jbeg; J <= Jend; J += 3) {
+        row(J, std::integral_constant<int, 0>{});
+        if (J + 1 > Jend) break;
+        row(J + 1, std::integral_constant<int, 1>{});
+        if (J + 2 > Jend) break;
+        row(J + 2, std::integral_constant<int, 2>{});
+    }
+    cpa_wait<0>();
+}
+
+template <bool SUM>
+constexpr size_t resid4_smem() {
+    return sizeof(Resid4Smem<SUM>) * kS4W;
+}
+
 template <int SK>
 constexpr size_t smooth4_smem() {
     return sizeof(Smooth4Smem<SK>) * kS4W;

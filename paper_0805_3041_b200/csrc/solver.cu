@@ -609,9 +609,41 @@ void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src,
     CK(cudaGetLastError());
 }
 
+template <bool SUM, class Coef>
+void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* u, const double* e, const double* g,
+                     double* dout, double* x0out, double* gc) {
+    constexpr size_t smem = resid4_smem<SUM>();
+    static bool attr = false;
+    if (!attr) {
+        set_smem(k_resid4<SUM, Coef>, smem);
+        attr = true;
+    }
+    Grid cg{0, 0, 0};
+    RestrictW rw{};
+    if (gc) {
+        const Lev& C = p->lev(L.l - 1);
+        cg = C.grid();
+        rw = C.rw;
+    }
+    const int seg = seg_rows(L.nx, L.rows());
+    const int strips = (L.nx + 123) / 124;
+    dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
+    k_resid4<SUM, Coef><<<grid, kS4W * 32, smem, p->st>>>(L.grid(), A, u, e, g, dout, x0out, cg, rw, gc, seg);
+    CK(cudaGetLastError());
+}
+
 // residual of (u, or x+e when e != null) against g; optional outputs.
 void launch_resid(gmg_problem* p, const Lev& L, const double* u, const double* e, const double* g,
                   double* dout, double* x0out, double* gc) {
+    if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
+        with_coef(L, [&](const auto& A) {
+            if (e)
+                launch_resid4_t<true>(p, L, A, u, e, g, dout, x0out, gc);
+            else
+                launch_resid4_t<false>(p, L, A, u, nullptr, g, dout, x0out, gc);
+        });
+        return;
+    }
     with_coef(L, [&](const auto& A) {
         if (e)
             launch_resid_t(p, L, A, SrcSum{u, e, L.grid()}, g, dout, x0out, gc);
