@@ -449,6 +449,179 @@ __global__ void __launch_bounds__(kS4W * 32, 4)
     cpa_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// k_omega4: the adaptive-omega terms (cycle.cpp:40-51) for corr = P uc:
+// T0_k = (A corr)_k * corr_k and T1_k = d_k * corr_k written densely in the
+// reference's k order, and whether some corr_k^2 != 0 — warp-strip layout,
+// coarse rows staged once per two fine rows as in k_smooth4.
+// ---------------------------------------------------------------------------
+struct Omega4Smem {
+    static constexpr int D = 4;
+    double2 d[D][2][32];
+    double c[D][68];
+    double t[2][128];  // one row of T0, T1 for coalesced stores
+};
+
+template <class Coef>
+__global__ void __launch_bounds__(kS4W * 32, 4)
+    k_omega4(Grid fg, Coef A, Prolong P, const double* __restrict__ dd, double* __restrict__ T0,
+             double* __restrict__ T1, int* __restrict__ nz, int seg) {
+    using SM = Omega4Smem;
+    constexpr int D = SM::D;
+    constexpr int H = 2;
+    constexpr int OW = 128 - 2 * H;
+    extern __shared__ __align__(16) unsigned char o4raw[];
+    SM& S = reinterpret_cast<SM*>(o4raw)[threadIdx.x >> 5];
+
+    const int lane = threadIdx.x & 31;
+    const int strip = blockIdx.x * kS4W + (threadIdx.x >> 5);
+    const int i0 = strip * OW - H;
+    if (i0 + H >= fg.nx) return;
+    const int i = i0 + 4 * lane;
+    const int nx = fg.nx, ny = fg.ny;
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
+    const bool edge = i0 < 0 || i0 + 128 > nx;
+    bool cin[4], cout_[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        cin[k] = i + k >= 0 && i + k < nx;
+        const int c = 4 * lane + k;
+        cout_[k] = cin[k] && c >= H && c < 128 - H;
+    }
+    const int m0 = i0 / 2 - 1;
+    const double tX0 = cin[0] ? __ldg(P.tx + i) : 0.0;
+    const double tX2 = cin[2] ? __ldg(P.tx + i + 2) : 0.0;
+    auto chunk_bytes = [&](int c) { return (c >= 0 && c < nx) ? (c + 1 < nx ? 16 : 8) : 0; };
+    const int cb0 = chunk_bytes(i), cb1 = chunk_bytes(i + 2);
+    const long long pitch = fg.pitch;
+    const int Jbeg = j0 - 1;  // corr rows j0-1 .. j1 give A corr on rows j0 .. j1-1
+    const int Jend = j1;
+    long long soff = (long long)Jbeg * pitch + i;
+    auto slot_of = [](int J) { return (J + 8) & (D - 1); };
+    auto stage_crow = [&](int q) {
+        double* dst = S.c[(q + 8) & (D - 1)];
+        stage_coarse(dst + 2 * lane, P.uc, P.cg, m0 + 2 * lane, q);
+        stage_coarse(dst + 2 * lane + 1, P.uc, P.cg, m0 + 2 * lane + 1, q);
+        if (lane == 0) stage_coarse(dst + 64, P.uc, P.cg, m0 + 64, q);
+    };
+    // fine row J: d of row J (used as d_R one iteration later) + the coarse row it adds
+    auto stage = [&](int J) {
+        const int sl = slot_of(J);
+        const bool row_in = J >= 0 && J < ny;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int bytes = row_in ? (h ? cb1 : cb0) : 0;
+            cpa16(&S.d[sl][h][lane], dd + (bytes ? soff + 2 * h : 0), bytes);
+        }
+        soff += pitch;
+        if (((J + 8) & 1) == 0) stage_crow((J + 8) / 2 - 4);
+        cpa_commit();
+    };
+    {
+        const int qf = (Jbeg + 8) / 2 - 4;
+        stage_crow(((Jbeg + 8) & 1) ? qf : qf - 1);
+    }
+    stage(Jbeg);
+    stage(Jbeg + 1);
+    cpa_wait<1>();
+    __syncwarp();
+
+    double cw[3][4];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cw[r][k] = 0.0;
+    int any = 0;
+
+    auto row = [&](int J, auto ph) {
+        constexpr int PH = decltype(ph)::value;
+        constexpr int sJ = PH % 3, sJ1 = (PH + 2) % 3, sJ2 = (PH + 1) % 3;  // rows J, J-1, J-2
+        stage(J + 2);
+        const int sl1 = slot_of(J - 1);
+        // corr of row J
+        {
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            if (J >= 0 && J < ny) {
+                const int qf = (J + 8) / 2 - 4;
+                const bool even = ((J + 8) & 1) == 0;
+                const double* ca = &S.c[((even ? qf - 1 : qf) + 8) & (D - 1)][2 * lane];
+                const double* cb = &S.c[(qf + 8) & (D - 1)][2 * lane];
+                Pair2Raw r;
+                r.ty = ((J + 1) & 1) ? __ldg(P.ty + J) : 0.0;
+                r.a = ca[0];
+                r.b = ca[1];
+                r.c = cb[0];
+                r.d = cb[1];
+                const double2 p0 = prolong2_make(r, i, J, nx, tX0);
+                r.a = ca[1];
+                r.b = ca[2];
+                r.c = cb[1];
+                r.d = cb[2];
+                const double2 p1 = prolong2_make(r, i + 2, J, nx, tX2);
+                v[0] = p0.x;
+                v[1] = p0.y;
+                v[2] = p1.x;
+                v[3] = p1.y;
+                if (edge) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (!cin[k]) v[k] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cw[sJ][k] = v[k];
+        }
+        const int R = J - 1;
+        if (R >= j0 && R < j1) {
+            const double xl = __shfl_up_sync(0xffffffffu, cw[sJ1][3], 1);
+            const double xr = __shfl_down_sync(0xffffffffu, cw[sJ1][0], 1);
+            const double2 da = S.d[sl1][0][lane], db = S.d[sl1][1][lane];
+            const double dv[4] = {da.x, da.y, db.x, db.y};
+            double t0[4], t1[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double b = cw[sJ1][k];
+                const double xwv = k == 0 ? xl : cw[sJ1][k - 1];
+                const double xev = k == 3 ? xr : cw[sJ1][k + 1];
+                const double ac = stencil_apply(A, i + k, R, b, xwv, xev, cw[sJ2][k], cw[sJ][k]);
+                t0[k] = ac * b;
+                t1[k] = dv[k] * b;
+                if (cout_[k]) any |= (b * b) != 0.0;
+            }
+            // through shared memory so that consecutive lanes store consecutive k
+            *reinterpret_cast<double2*>(&S.t[0][4 * lane]) = make_double2(t0[0], t0[1]);
+            *reinterpret_cast<double2*>(&S.t[0][4 * lane + 2]) = make_double2(t0[2], t0[3]);
+            *reinterpret_cast<double2*>(&S.t[1][4 * lane]) = make_double2(t1[0], t1[1]);
+            *reinterpret_cast<double2*>(&S.t[1][4 * lane + 2]) = make_double2(t1[2], t1[3]);
+            __syncwarp();
+            const long long kr = (long long)R * nx + i0;  // k of the strip's first column
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int c = lane + 32 * m;
+                if (c >= H && c < 128 - H && i0 + c < nx) {
+                    T0[kr + c] = S.t[0][c];
+                    T1[kr + c] = S.t[1][c];
+                }
+            }
+            __syncwarp();
+        }
+        cpa_wait<1>();
+        __syncwarp();
+    };
+    for (int J = Jbeg; J <= Jend; J += 3) {
+        row(J, std::integral_constant<int, 0>{});
+        if (J + 1 > Jend) break;
+        row(J + 1, std::integral_constant<int, 1>{});
+        if (J + 2 > Jend) break;
+        row(J + 2, std::integral_constant<int, 2>{});
+    }
+    cpa_wait<0>();
+    if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(nz, 1);
+}
+
+constexpr size_t omega4_smem() { return sizeof(Omega4Smem) * kS4W; }
+
 template <bool SUM>
 constexpr size_t resid4_smem() {
     return sizeof(Resid4Smem<SUM>) * kS4W;

@@ -16,6 +16,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -486,7 +487,12 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
 
 // levels at least this wide use the strip-per-warp smoother (k_smooth4)
 constexpr int kRingMinNx = 255;
-static int g_smooth_variant = 4;  // 4: k_smooth4, 3: k_smooth3 (GMG_SMOOTH_KERNEL=3 selects it)
+// 4: the warp-strip kernels (k_smooth4, k_resid4, k_omega4); 3: the earlier
+// row-streaming kernels (GMG_STREAM_KERNELS=3, for A/B timing)
+static int g_smooth_variant = [] {
+    const char* e = std::getenv("GMG_STREAM_KERNELS");
+    return (e && e[0] == '3') ? 3 : 4;
+}();
 
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
@@ -544,7 +550,7 @@ void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const Smooth
 // One launch of M <= 4 Jacobi steps.
 void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, const double* g, double* out,
                    double wd) {
-    if (L.kind == 0 && L.cconst.c_pow2 && L.nx >= kRingMinNx && g_smooth_variant == 4) {
+    if (L.kind == 0 && L.cconst.c_pow2 && L.nx >= kRingMinNx && g_smooth_variant == 4) {  // k_smooth4
         CoefConstP2 A;
         static_cast<CoefConst&>(A) = L.cconst;
         switch (M) {
@@ -1193,7 +1199,20 @@ struct Driver {
             double* T1 = q->T + q->lev(q->L).n();
             with_coef(L, [&](const auto& A) {
                 using C = std::decay_t<decltype(A)>;
-                k_omega_terms<kTW, 2, C><<<grid, kTW, 0, q->st>>>(L.grid(), A, src, L.buf[DD], T0, T1, q->nz, seg);
+                if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
+                    static bool attr = false;
+                    if (!attr) {
+                        set_smem(k_omega4<C>, omega4_smem());
+                        attr = true;
+                    }
+                    const int strips = (L.nx + 123) / 124;
+                    dim3 g4((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
+                    k_omega4<C><<<g4, kS4W * 32, omega4_smem(), q->st>>>(L.grid(), A, src.P, L.buf[DD], T0, T1,
+                                                                          q->nz, seg);
+                } else {
+                    k_omega_terms<kTW, 2, C><<<grid, kTW, 0, q->st>>>(L.grid(), A, src, L.buf[DD], T0, T1, q->nz,
+                                                                       seg);
+                }
             });
             CK(cudaGetLastError());
         }
