@@ -32,6 +32,7 @@ namespace gmg_dev {
 constexpr int kSsT = 256;             // threads per chunk
 constexpr int kSsEPT = 32;            // terms per thread
 constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk
+constexpr uint32_t kRecOpen = 1u << 16;  // Rec.meta: the carried-in run is still to be prepended
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
 constexpr int kSsRMax = 256;          // records a chunk may store; more -> exact re-walk
@@ -47,7 +48,8 @@ struct SsState {
     double* incl;    // [nch]
     unsigned char* cagg;   // [nch] ChunkAgg
     unsigned char* cincl;  // [nch] ChunkAgg
-    gmg_ss::Rec* recs;
+    gmg_ss::Rec* recs;   // [nch * kSsRMax] per-chunk record slots written by the walk
+    gmg_ss::Rec* recs2;  // compacted records in order (k_ss_compact), read by the chain
     unsigned long long* stats;  // [16] calls, records, chain cycles, re-walk cycles, break adds, re-walks,
                                 //      re-walked terms, chunks; walk phase cycles [8..13]
 };
@@ -284,7 +286,6 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     __shared__ SegF sws[8];
     __shared__ int s_chunk;
     __shared__ double s_pre;
-    __shared__ SegF s_carry;
 
     const int s = blockIdx.y;
     const SsState& S = sts.s[s];
@@ -376,51 +377,32 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     const int R = tot.cnt + (close ? 1 : 0);
     const bool literal = R > kSsRMax;
 
-    // (5) run carry + record offset by look-back over chunks (aggregate
-    //     published first, so no chunk waits on a predecessor's look-back)
+    // (5) the chunk's aggregate for k_ss_scan (the run it carries on, the
+    //     records it stores). No look-back: the cross-chunk segmented scan runs
+    //     as one small kernel after all walks, and the chunk's first record is
+    //     stored "open" (kRecOpen) for k_ss_compact to prepend the run carried in.
     SegF mine = tot;
     mine.cnt = literal ? 1 : R;
     if (literal || close) {
         mine.f = 1;
         mine.g = gmg_ss::seg_empty();
     }
-    if (t == 0) {
-        if (c == 0) {
-            agg_store(S.cincl, 0, mine);
-            st_flag(S.cflag, 2);
-        } else {
-            agg_store(S.cagg, c, mine);
-            st_flag(S.cflag + c, 1);
-        }
-    }
-    if (t < 32) {
-        const SegF ex = c == 0 ? segf_id() : lookback_seg(c, S.cflag, S.cagg, S.cincl);
-        if (t == 0) {
-            if (c > 0) {
-                agg_store(S.cincl, c, segf_combine(ex, mine));
-                st_flag(S.cflag + c, 2);
-            }
-            if (last) *S.total = ex.cnt + mine.cnt;
-            s_carry = ex;
-        }
-    }
-    __syncthreads();
+    if (t == 0) agg_store(S.cagg, c, mine);
     ph[5] = clock64();
     if (t == 0 && S.stats) {
         for (int q = 0; q < 5; ++q) atomicAdd(S.stats + 8 + q, (unsigned long long)(ph[q + 1] - ph[q]));
         atomicAdd(S.stats + 13, 1ull);
     }
-    const SegF cin = s_carry;  // run since the last break before this chunk; cnt = offset
-    gmg_ss::Rec* out = S.recs + cin.cnt;
+    gmg_ss::Rec* out = S.recs + (long long)c * kSsRMax;
     if (literal) {
         if (t == 0) out[0] = gmg_ss::rec_literal((uint32_t)(base + clen - 1));
         return;
     }
     if (r > 0) {
-        // pass 2: emit this thread's records; the first absorbs the run carried in
+        // pass 2: emit this thread's records; the first absorbs the run since the
+        // last break inside the chunk (and, when there is none, the run carried in)
         const int pos = carry.cnt;
-        gmg_ss::Seg first = carry.g;
-        if (!carry.f) first = gmg_ss::seg_merge(cin.g, first);
+        const gmg_ss::Seg first = carry.g;
         gmg_ss::walker_init(wk, pred);
         int k = 0;
         for (int m = 0; m < ne; ++m) {
@@ -428,7 +410,9 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
             if (!gmg_ss::walker_try(wk, p)) {
                 const gmg_ss::Seg sg = gmg_ss::walker_seg(wk);
                 const gmg_ss::Seg g = k == 0 ? gmg_ss::seg_merge(first, sg) : sg;
-                out[pos + k] = gmg_ss::rec_make(g, true, p, (uint32_t)(base + e0 + m));
+                gmg_ss::Rec rec = gmg_ss::rec_make(g, true, p, (uint32_t)(base + e0 + m));
+                if (k == 0 && !carry.f) rec.meta |= kRecOpen;
+                out[pos + k] = rec;
                 ++k;
                 gmg_ss::walker_open(wk);
                 gmg_ss::walker_real_add(wk, p);
@@ -436,8 +420,67 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
         }
     }
     if (close && t == kSsT - 1) {
-        const gmg_ss::Seg g = tot.f ? tot.g : gmg_ss::seg_merge(cin.g, tot.g);
-        out[R - 1] = gmg_ss::rec_make(g, false, 0.0, (uint32_t)(base + clen - 1));
+        gmg_ss::Rec rec = gmg_ss::rec_make(tot.g, false, 0.0, (uint32_t)(base + clen - 1));
+        if (!tot.f) rec.meta |= kRecOpen;
+        out[R - 1] = rec;
+    }
+}
+
+// ---- cross-chunk scan and record compaction --------------------------------
+// grid (NS); 1024 threads. Exclusive ordered segmented scan of the chunk
+// aggregates: cincl[c] = the run carried into chunk c (cnt = its first record's
+// position); *total = records of the sum.
+constexpr int kSsScanT = 1024;
+__global__ void __launch_bounds__(kSsScanT) k_ss_scan(SsPair sts, int nch) {
+    __shared__ SegF sw[kSsScanT / 32];
+    const SsState& S = sts.s[blockIdx.x];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int per = (nch + kSsScanT - 1) / kSsScanT;
+    const int c0 = min(t * per, nch), c1 = min(c0 + per, nch);
+    SegF a = segf_id();
+    for (int c = c0; c < c1; ++c) a = segf_combine(a, agg_load(S.cagg, c));
+    // block exclusive scan of the thread aggregates
+    SegF inc = a;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const SegF y = segf_shfl(inc, 0, true, o);
+        if (lane >= o) inc = segf_combine(y, inc);
+    }
+    const SegF ex_w = segf_shfl(inc, 0, true, 1);
+    if (lane == 31) sw[w] = inc;
+    __syncthreads();
+    SegF base = segf_id(), tot = segf_id();
+    for (int q = 0; q < kSsScanT / 32; ++q) {
+        if (q < w) base = segf_combine(base, sw[q]);
+        tot = segf_combine(tot, sw[q]);
+    }
+    SegF ex = lane == 0 ? base : segf_combine(base, ex_w);
+    for (int c = c0; c < c1; ++c) {
+        agg_store(S.cincl, c, ex);
+        ex = segf_combine(ex, agg_load(S.cagg, c));
+    }
+    if (t == 0) *S.total = tot.cnt;
+}
+
+// grid (ceil(nch/8), NS); 256 threads, a warp per chunk: copies the chunk's
+// records to their place in the ordered list, prepending the carried-in run to
+// an open record (seg_merge is associative, so this equals merging in order).
+__global__ void __launch_bounds__(256) k_ss_compact(SsPair sts, int nch) {
+    const SsState& S = sts.s[blockIdx.y];
+    const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (c >= nch) return;
+    const int cnt = __ldcg(&reinterpret_cast<const ChunkAgg*>(S.cagg)[c].cnt);
+    if (cnt == 0) return;
+    const SegF cin = agg_load(S.cincl, c);
+    const gmg_ss::Rec* src = S.recs + (long long)c * kSsRMax;
+    gmg_ss::Rec* dst = S.recs2 + cin.cnt;
+    for (int j = lane; j < cnt; j += 32) {
+        gmg_ss::Rec r = src[j];
+        if (r.meta & kRecOpen) {
+            const bool brk = (r.meta >> 12) & 1u;
+            r = gmg_ss::rec_make(gmg_ss::seg_merge(cin.g, gmg_ss::rec_seg(r)), brk, r.pb, r.kb);
+        }
+        dst[j] = r;
     }
 }
 
@@ -569,7 +612,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
     const int total = *S.total;
     const int nb = (total + kSsBatch - 1) / kSsBatch;
 
-    for (int q = t; q < min(total, kSsBatch); q += kSsT) buf[q] = S.recs[q];
+    for (int q = t; q < min(total, kSsBatch); q += kSsT) buf[q] = S.recs2[q];
     __syncthreads();
 
     // Exact running sum kept as a double. While a record's run validates, the
@@ -677,7 +720,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
         } else if (b + 1 < nb) {
             gmg_ss::Rec* B = buf + ((b + 1) & 1) * kSsBatch;
             const int cn = min(kSsBatch, total - (b + 1) * kSsBatch);
-            const gmg_ss::Rec* src = S.recs + (long long)(b + 1) * kSsBatch;
+            const gmg_ss::Rec* src = S.recs2 + (long long)(b + 1) * kSsBatch;
             for (int q = t - 32; q < cn; q += kSsT - 32) B[q] = src[q];
         }
         __syncthreads();

@@ -165,7 +165,8 @@ struct gmg_problem {
     double* lb = nullptr;            // look-back values: per sum agg, incl [nch] each
     unsigned char* lbs = nullptr;    // per sum: cagg, cincl [nch] ChunkAgg each
     int* flags = nullptr;            // per sum: ticket, total, flag[nch], cflag[nch]
-    gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records
+    gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records (per-chunk slots)
+    gmg_ss::Rec* recs2 = nullptr;    // per sum: rec_cap records (compacted, in order)
     int rec_cap = 0;
     unsigned long long* ss_stats = nullptr;  // [16] exact-sum engine counters (seqsum.cuh)
     double* gs_edge = nullptr;               // Gauss-Seidel wavefront warp-edge rows
@@ -322,6 +323,7 @@ SsPair ss_state(gmg_problem* p, int nch) {
         S.cagg = p->lbs + (size_t)s * 2 * p->nch_max * sizeof(ChunkAgg);
         S.cincl = S.cagg + (size_t)p->nch_max * sizeof(ChunkAgg);
         S.recs = p->recs + (size_t)s * p->rec_cap;
+        S.recs2 = p->recs2 + (size_t)s * p->rec_cap;
         S.stats = p->ss_stats;
     }
     return sp;
@@ -354,6 +356,8 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) 
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
     k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp, pre0);
+    k_ss_scan<<<NS, kSsScanT, 0, p->st>>>(sp, nch);
+    k_ss_compact<<<dim3((nch + 7) / 8, NS), 256, 0, p->st>>>(sp, nch);
     CK(cudaGetLastError());
 }
 
@@ -1646,6 +1650,7 @@ void free_problem(gmg_problem* p) {
     cudaFree(p->lbs);
     cudaFree(p->flags);
     cudaFree(p->recs);
+    cudaFree(p->recs2);
     cudaFree(p->ss_stats);
     cudaFree(p->gs_edge);
     cudaFree(p->gs_prog);
@@ -1802,6 +1807,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
         p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
         CK(cudaMalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
+        CK(cudaMalloc(&p->recs2, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
         CK(cudaMalloc(&p->ss_stats, 16 * sizeof(unsigned long long)));
         int maxny = 0, maxnx = 0;
         for (const Lev& Lq : p->lv) {
