@@ -65,6 +65,10 @@ int main() {
                gmg::SmootherKind::gauss_seidel, 1e-8, 2);
     bad += run("spherical rect jacobi", 6, 2, 3, gmg::CoordinateSystem::spherical, 1.0, 0.5,
                gmg::SmootherKind::jacobi, 1e-9, 2);
+    bad += run("aniso adi random start", 7, 1, 1, gmg::CoordinateSystem::cartesian, 0.01, 1.0,
+               gmg::SmootherKind::adi, 1e-8, 2);
+    bad += run("cylindrical ilu0", 7, 1, 1, gmg::CoordinateSystem::cylindrical, 1.0, 1.0,
+               gmg::SmootherKind::ilu0, 1e-8, 0);
     // error mapping: an invalid smoother omega must surface as std::invalid_argument
     try {
         const gmg::GridHierarchy h = gmg::build_hierarchy(3, 1, 1, {}, gmg::CoordinateSystem::cartesian);

@@ -252,7 +252,7 @@ __device__ __forceinline__ double block_excl_sum_d(double x, double* sw /* [8] *
 }
 
 // Block exclusive segmented scan (256 threads); returns the block inclusive total too.
-__device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [8] */, SegF* total) {
+__device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [9] */, SegF* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     SegF inc = x;
 #pragma unroll
@@ -263,13 +263,21 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [8
     const SegF ex = segf_shfl(inc, 0, true, 1);
     if (lane == 31) sw[w] = inc;
     __syncthreads();
-    SegF base = segf_id(), tot = segf_id();
-    for (int q = 0; q < 8; ++q) {
-        if (q < w) base = segf_combine(base, sw[q]);
-        tot = segf_combine(tot, sw[q]);
+    // one thread turns the 8 warp totals into exclusive bases (in place, the
+    // block total in sw[8]); every thread then reads its warp's base
+    if (threadIdx.x == 0) {
+        SegF acc = segf_id();
+        for (int q = 0; q < 8; ++q) {
+            const SegF v = sw[q];
+            sw[q] = acc;
+            acc = segf_combine(acc, v);
+        }
+        sw[8] = acc;
     }
     __syncthreads();
-    *total = tot;
+    const SegF base = sw[w];
+    *total = sw[8];
+    __syncthreads();
     if (lane == 0) return base;
     return segf_combine(base, ex);
 }
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
                                                        const double* __restrict__ pre0) {
     extern __shared__ double tm[];
     __shared__ double swd[8];
-    __shared__ SegF sws[8];
+    __shared__ SegF sws[9];
     __shared__ int s_chunk;
     __shared__ double s_pre;
 

@@ -18,7 +18,7 @@ DEMO = os.path.join(ROOT, "oracle", "_ref", "shim_demo")
 def test_reference_solve_vs_b200_shim(gpu):
     r = subprocess.run([DEMO], capture_output=True, text=True, timeout=600)
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 5, r.stdout + r.stderr
+    assert len(lines) == 7, r.stdout + r.stderr
     for case in lines:
         assert case["identical"], case
     assert r.returncode == 0, r.stdout + r.stderr
