@@ -440,10 +440,11 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 // position); *total = records of the sum.
 constexpr int kSsScanT = 1024;
 __global__ void __launch_bounds__(kSsScanT) k_ss_scan(SsPair sts, int nch) {
-    __shared__ SegF sw[kSsScanT / 32];
+    __shared__ SegF sw[kSsScanT / 32 + 1];
     const SsState& S = sts.s[blockIdx.x];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int per = (nch + kSsScanT - 1) / kSsScanT;
+    const int nt = blockDim.x, nw = nt >> 5;
+    const int per = (nch + nt - 1) / nt;
     const int c0 = min(t * per, nch), c1 = min(c0 + per, nch);
     SegF a = segf_id();
     for (int c = c0; c < c1; ++c) a = segf_combine(a, agg_load(S.cagg, c));
@@ -457,11 +458,17 @@ __global__ void __launch_bounds__(kSsScanT) k_ss_scan(SsPair sts, int nch) {
     const SegF ex_w = segf_shfl(inc, 0, true, 1);
     if (lane == 31) sw[w] = inc;
     __syncthreads();
-    SegF base = segf_id(), tot = segf_id();
-    for (int q = 0; q < kSsScanT / 32; ++q) {
-        if (q < w) base = segf_combine(base, sw[q]);
-        tot = segf_combine(tot, sw[q]);
+    if (t == 0) {  // exclusive bases of the warp totals, block total in sw[nw]
+        SegF acc = segf_id();
+        for (int q = 0; q < nw; ++q) {
+            const SegF v = sw[q];
+            sw[q] = acc;
+            acc = segf_combine(acc, v);
+        }
+        sw[nw] = acc;
     }
+    __syncthreads();
+    const SegF base = sw[w], tot = sw[nw];
     SegF ex = lane == 0 ? base : segf_combine(base, ex_w);
     for (int c = c0; c < c1; ++c) {
         agg_store(S.cincl, c, ex);

@@ -356,7 +356,7 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) 
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
     k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp, pre0);
-    k_ss_scan<<<NS, kSsScanT, 0, p->st>>>(sp, nch);
+    k_ss_scan<<<NS, std::min(kSsScanT, (nch + 31) / 32 * 32), 0, p->st>>>(sp, nch);
     k_ss_compact<<<dim3((nch + 7) / 8, NS), 256, 0, p->st>>>(sp, nch);
     CK(cudaGetLastError());
 }
