@@ -35,6 +35,7 @@
 #include "march2.cuh"
 #include "march4.cuh"
 #include "seqsum.cuh"
+#include "vsmall.cuh"
 
 using namespace gmg_dev;
 
@@ -1149,8 +1150,69 @@ struct Driver {
         return dst;
     }
 
+    // levels <= kVTop in one CTA (k_vsmall): Jacobi V recursion from a zero or
+    // prolongated start, every slab replicated (none of these levels is sharded)
+    bool fused_small(int l, const SrcId& s) const {
+        if (l > kVTop || sp.smoother_kind != GMG_SMOOTHER_JACOBI || sp.cycle == GMG_CYCLE_W) return false;
+        if (s.kind != S_ZERO && s.kind != S_PROLONG) return false;
+        if (sharded(l)) return false;
+        return vsmall_smem(l) <= kVSmemMax;
+    }
+    size_t vsmall_smem(int l) const {
+        size_t nd = 0;
+        for (int q = 1; q <= l; ++q) nd += 3 * (size_t)p()->lev(q).n();
+        nd += 2 * (size_t)p()->lev(l).n();
+        return nd * sizeof(double);
+    }
+    void launch_vsmall(gmg_problem* q, int l, const SrcId& s, int g) {
+        VParams V{};
+        int off = 0;
+        for (int k = 1; k <= l; ++k) {
+            const Lev& L = q->lev(k);
+            VLev& v = V.lv[k];
+            v.nx = L.nx;
+            v.ny = L.ny;
+            v.pitch = L.pitch;
+            v.kind = L.kind;
+            v.cc = L.cconst;
+            v.cr = L.crow;
+            v.cf = L.cfield;
+            v.tx = L.tx;
+            v.ty = L.ty;
+            v.rw = L.rw;
+            v.off = off;
+            off += 3 * L.nx * L.ny;
+        }
+        V.toff = off;
+        V.top = l;
+        V.pre = sp.pre_steps;
+        V.post = sp.post_steps;
+        V.adaptive = sp.adaptive_correction != 0;
+        V.direct = (unsigned long long)q->lev(1).n() <= sp.coarse_direct_max_neq;
+        V.cn = q->cn;
+        V.cbw = q->cbw;
+        V.damp = sp.smoothing_omega;
+        V.corr_omega = sp.correction_omega;
+        V.band = q->band;
+        V.g_top = bufptr(q, l, g);
+        V.uc = s.kind == S_PROLONG ? bufptr(q, l - 1, s.uc) : nullptr;
+        V.out = q->lev(l).buf[U0];
+        V.status = q->status;
+        static bool attr = false;
+        if (!attr) {
+            set_smem(k_vsmall, kVSmemMax);
+            attr = true;
+        }
+        k_vsmall<<<1, kVThreads, vsmall_smem(l), q->st>>>(V);
+        CK(cudaGetLastError());
+    }
+
     // gmg::mg_cycle (cycle.cpp:69-100) on level l from start s with rhs g.
     int visit(int l, SrcId s, int g) {
+        if (fused_small(l, s)) {
+            for (auto* q : S) launch_vsmall(q, l, s, g);
+            return U0;
+        }
         const int u_in = s.kind == S_U ? s.u : -1;
         const int a = (u_in == U0) ? U1 : U0;
         const int b = (a == U0) ? U1 : U0;
