@@ -356,13 +356,47 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     gmg_ss::walker_init(wk, pred);
     gmg_ss::Seg lead = gmg_ss::seg_empty();
     int r = 0;
-    for (int m = 0; m < ne; ++m) {
-        const double p = tm[ss_pad(e0 + m)];
-        if (!gmg_ss::walker_try(wk, p)) {
-            if (r == 0) lead = gmg_ss::walker_seg(wk);
-            ++r;
-            gmg_ss::walker_open(wk);
-            gmg_ss::walker_real_add(wk, p);
+    // Fast path: all kSsEPT terms stay in the binade without ties. The increments
+    // q_m = RN(p_m/u) are independent, only their prefix sums are a chain; the
+    // range test on the prefix extremes equals the walker's per-step tests (the
+    // sign cannot change: |q| < 2^52 <= |M|). Same state and segment as
+    // walker_try would leave; otherwise the element-wise walk below.
+    bool fast = false;
+    if (ne == kSsEPT && wk.E != 0) {
+        double P = 0.0, mn = 0.0, mx = 0.0;
+        bool ok = true;
+#pragma unroll
+        for (int m = 0; m < kSsEPT; ++m) {
+            const double x = tm[ss_pad(e0 + m)] * wk.inv_u;  // exact power-of-two scaling
+            const double q = rint(x);
+            ok = ok && (x < gmg_ss::kTwo52 && x > -gmg_ss::kTwo52) && fabs(x - q) != 0.5;
+            P = P + q;
+            mn = m == 0 ? P : fmin(mn, P);
+            mx = m == 0 ? P : fmax(mx, P);
+        }
+        const double M = wk.M;
+        const double lo = static_cast<double>(gmg_ss::kLo), hi = static_cast<double>(gmg_ss::kHi);
+        ok = ok && (M >= 0.0 ? (M + mn >= lo && M + mx <= hi) : (M + mx <= -lo && M + mn >= -hi));
+        if (ok) {
+            wk.segE = wk.E;
+            wk.segneg = M < 0.0;
+            wk.Q[0] = P;
+            wk.mn[0] = mn;
+            wk.mx[0] = mx;
+            wk.len = kSsEPT;
+            wk.M = M + P;
+            fast = true;
+        }
+    }
+    if (!fast) {
+        for (int m = 0; m < ne; ++m) {
+            const double p = tm[ss_pad(e0 + m)];
+            if (!gmg_ss::walker_try(wk, p)) {
+                if (r == 0) lead = gmg_ss::walker_seg(wk);
+                ++r;
+                gmg_ss::walker_open(wk);
+                gmg_ss::walker_real_add(wk, p);
+            }
         }
     }
     const gmg_ss::Seg cur = gmg_ss::walker_seg(wk);
