@@ -35,7 +35,7 @@ constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk
 constexpr uint32_t kRecOpen = 1u << 16;  // Rec.meta: the carried-in run is still to be prepended
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
-constexpr int kSsRMax = 256;          // records a chunk may store; more -> exact re-walk
+constexpr int kSsRMax = 1024;          // records a chunk may store; more -> exact re-walk
 constexpr int kSsRunCap = 16;         // a merged run never spans more than this many chunks
 
 // Per-sum look-back state (flags, ticket and total zeroed before each walk).
@@ -320,8 +320,15 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     __syncthreads();
     const int e0 = t * kSsEPT;
     const int ne = max(0, min(kSsEPT, clen - e0));
-    double ts = 0.0;
-    for (int m = 0; m < ne; ++m) ts += tm[ss_pad(e0 + m)];
+    double ts = 0.0;  // approximate (tree-order) sum of this thread's terms
+    if (ne == kSsEPT) {
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < kSsEPT; ++m) a4[m & 3] += tm[ss_pad(e0 + m)];
+        ts = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    } else {
+        for (int m = 0; m < ne; ++m) ts += tm[ss_pad(e0 + m)];
+    }
     ph[1] = clock64();
 
     // (2) approximate prefix by look-back
