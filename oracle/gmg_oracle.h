@@ -11,7 +11,7 @@
  *
  * Parity pin: tests/test_oracle_pin.py checks this restatement bit-for-bit
  * against the reference itself (oracle/_ref, built from the reference sources)
- * and against the committed golden fixtures tests/golden/*.json.
+ * and against the committed golden fixtures tests/golden/ (*.json).
  */
 #ifndef GMG_ORACLE_H
 #define GMG_ORACLE_H

@@ -17,7 +17,7 @@ gmg = pytest.importorskip("paper_0805_3041_b200.gmg")
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "gmg_b200.h")).read()
-    return sorted(set(re.findall(r"\b(gmg_(?:dev|host)_\w+|gmg_last_error|gmg_version)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(gmg_(?:dev|host|dist)_\w+|gmg_last_error|gmg_version)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
