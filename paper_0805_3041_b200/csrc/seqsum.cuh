@@ -235,7 +235,8 @@ __device__ __forceinline__ double block_sum_d(double x, double* sw /* [8] */) {
     return t;
 }
 
-__device__ __forceinline__ double block_excl_sum_d(double x, double* sw /* [8] */) {
+// Block exclusive sum (256 threads) and the block total, one barrier pair.
+__device__ __forceinline__ double block_excl_sum_tot_d(double x, double* sw /* [8] */, double* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double inc = x;
 #pragma unroll
@@ -245,10 +246,60 @@ __device__ __forceinline__ double block_excl_sum_d(double x, double* sw /* [8] *
     }
     if (lane == 31) sw[w] = inc;
     __syncthreads();
-    double base = 0.0;
-    for (int q = 0; q < w; ++q) base += sw[q];
+    double base = 0.0, t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (q == w) base = t;
+        t += sw[q];
+    }
     __syncthreads();
+    *total = t;
     return base + inc - x;
+}
+
+// One segment per thread, all in the same binade and sign (uniform chunk):
+// the merged segment's total (returned) and its prefix extremes. P, mn, mx are
+// the thread's exact integer total and prefix extremes as doubles.
+__device__ __forceinline__ long long block_seg_i64(double Pd, double mnd, double mxd, long long (*sw)[8],
+                                                   long long* lo, long long* hi) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long P = (long long)Pd;
+    long long inc = P;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sw[0][w] = inc;
+    __syncthreads();
+    long long base = 0, t = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (q == w) base = t;
+        t += sw[0][q];
+    }
+    const long long ex = base + inc - P;
+    long long a = ex + (long long)mnd, b = ex + (long long)mxd;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if (lane == 0) {
+        sw[1][w] = a;
+        sw[2][w] = b;
+    }
+    __syncthreads();
+    a = sw[1][0];
+    b = sw[2][0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) {
+        a = min(a, sw[1][q]);
+        b = max(b, sw[2][q]);
+    }
+    *lo = a;
+    *hi = b;
+    return t;
 }
 
 // Block exclusive segmented scan (256 threads); returns the block inclusive total too.
@@ -292,8 +343,9 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     extern __shared__ double tm[];
     __shared__ double swd[8];
     __shared__ SegF sws[9];
-    __shared__ int s_chunk;
+    __shared__ int s_chunk, s_key;
     __shared__ double s_pre;
+    __shared__ long long s_i64[3][8];
 
     const int s = blockIdx.y;
     const SsState& S = sts.s[s];
@@ -309,11 +361,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     // (1) terms: striped (coalesced) loads, all in flight before the smem stores
     {
         double v[kSsEPT];
-#pragma unroll
-        for (int m = 0; m < kSsEPT; ++m) {
-            const int kl = m * kSsT + t;
-            v[m] = kl < clen ? tg.term(s, base + kl) : 0.0;
-        }
+        tg.striped(s, base + t, clen, v);
 #pragma unroll
         for (int m = 0; m < kSsEPT; ++m) tm[ss_pad(m * kSsT + t)] = v[m];
     }
@@ -332,7 +380,8 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     ph[1] = clock64();
 
     // (2) approximate prefix by look-back
-    const double tot_approx = block_sum_d(ts, swd);
+    double tot_approx;
+    const double ex_approx = block_excl_sum_tot_d(ts, swd, &tot_approx);
     // pre0: approximate sum of the terms before this range (earlier row slabs)
     const double base_pre = pre0 ? pre0[s] : 0.0;
     if (t == 0) {
@@ -355,7 +404,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
         }
     }
     __syncthreads();
-    const double pred = s_pre + block_excl_sum_d(ts, swd);
+    const double pred = s_pre + ex_approx;
     ph[2] = clock64();
 
     // (3) thread walk, pass 1: leading segment, trailing segment, break count
@@ -406,18 +455,36 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
             }
         }
     }
-    const gmg_ss::Seg cur = gmg_ss::walker_seg(wk);
-    if (r == 0) lead = cur;
+    // Uniform chunk: every thread took the fast path in the same binade and sign
+    // (the common case). The chunk is then one segment, and merging the threads'
+    // segments is an int64 exclusive scan of their totals plus a min/max of
+    // (prefix + extreme) — no segmented scan, no records unless the run closes.
+    if (t == 0) s_key = fast ? wk.segE * 2 + wk.segneg : -1;
     __syncthreads();
+    const bool uni = __syncthreads_and(fast && wk.segE * 2 + wk.segneg == s_key);
     ph[3] = clock64();
 
     // (4) merge runs across threads; records = breaks (+ the final record)
-    SegF x = segf_id();
-    x.f = r > 0;
-    x.g = r > 0 ? cur : lead;
-    x.cnt = r;
-    SegF tot;
-    const SegF carry = block_excl_segscan(x, sws, &tot);
+    SegF tot, carry;
+    if (uni) {
+        tot = segf_id();
+        long long lo, hi;
+        tot.g.Q[0] = tot.g.Q[1] = block_seg_i64(wk.Q[0], wk.mn[0], wk.mx[0], s_i64, &lo, &hi);
+        tot.g.mn[0] = tot.g.mn[1] = lo;
+        tot.g.mx[0] = tot.g.mx[1] = hi;
+        tot.g.E = wk.segE;
+        tot.g.neg = wk.segneg;
+        tot.g.len = clen;
+        carry = segf_id();
+    } else {
+        const gmg_ss::Seg cur = gmg_ss::walker_seg(wk);
+        if (r == 0) lead = cur;
+        SegF x = segf_id();
+        x.f = r > 0;
+        x.g = r > 0 ? cur : lead;
+        x.cnt = r;
+        carry = block_excl_segscan(x, sws, &tot);
+    }
     ph[4] = clock64();
     const bool last = c == nch - 1;
     // every kSsRunCap-th chunk closes its run with a no-break record, so a
@@ -853,6 +920,17 @@ __device__ __forceinline__ int row_of(long long k, int nx, double inv_nx) {
     return j;
 }
 
+// Each generator also loads a chunk's terms for one thread of the walk:
+// `striped(s, k0, clen, v)` fills v[m] = term k0 + m*kSsT (0 past the chunk),
+// where k0 = chunk base + threadIdx.x and clen = terms in the chunk.
+#define GMG_SS_STRIPED_DEFAULT                                                              \
+    __device__ __forceinline__ void striped(int s, long long k0, int clen, double (&v)[kSsEPT]) const { \
+        _Pragma("unroll") for (int m = 0; m < kSsEPT; ++m) {                                \
+            const int kl = m * kSsT + (int)threadIdx.x;                                      \
+            v[m] = kl < clen ? term(s, k0 + m * kSsT) : 0.0;                                 \
+        }                                                                                    \
+    }
+
 struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid function
     static constexpr int NS = 1;
     const double* r;
@@ -863,12 +941,29 @@ struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid f
         const double v = __ldg(r + g.at(i, j));
         return v * v;
     }
+    // row/column of the first term once, then stepped by kSsT (no per-term division)
+    __device__ __forceinline__ void striped(int, long long k0, int clen, double (&v)[kSsEPT]) const {
+        int j = row_of(k0, g.nx, inv_nx), i = (int)(k0 - (long long)j * g.nx);
+#pragma unroll
+        for (int m = 0; m < kSsEPT; ++m) {
+            const int kl = m * kSsT + (int)threadIdx.x;
+            double x = 0.0;
+            if (kl < clen) x = __ldg(r + g.at(i, j));
+            v[m] = x * x;
+            i += kSsT;
+            while (i >= g.nx) {
+                i -= g.nx;
+                ++j;
+            }
+        }
+    }
 };
 
 struct DotTerms {  // a_k * b_k (dot, stencil.cpp:21-26) on flat arrays
     static constexpr int NS = 1;
     const double *a, *b;
     __device__ __forceinline__ double term(int, long long k) const { return __ldg(a + k) * __ldg(b + k); }
+    GMG_SS_STRIPED_DEFAULT
 };
 
 struct FlatNormTerms {  // v_k * v_k on a flat array
@@ -878,6 +973,7 @@ struct FlatNormTerms {  // v_k * v_k on a flat array
         const double v = __ldg(a + k);
         return v * v;
     }
+    GMG_SS_STRIPED_DEFAULT
 };
 
 struct ArrTerms {  // materialised terms: sum s reads t[s][k]
@@ -885,6 +981,7 @@ struct ArrTerms {  // materialised terms: sum s reads t[s][k]
     const double* t0;
     const double* t1;
     __device__ __forceinline__ double term(int s, long long k) const { return __ldg((s ? t1 : t0) + k); }
+    GMG_SS_STRIPED_DEFAULT
 };
 
 }  // namespace gmg_dev
