@@ -607,6 +607,75 @@ __global__ void __launch_bounds__(256) k_ss_compact(SsPair sts, int nch) {
     }
 }
 
+// Single-pass replacement for k_ss_scan + k_ss_compact. grid (ceil(nch/256), NS);
+// 256 threads, a thread per chunk. Block exclusive segmented scan of the chunk
+// aggregates, then a decoupled look-back over the CTA aggregates (CTA order
+// from the ticket the walk left at nch, so every predecessor is running),
+// giving the run carried into each chunk and its first record's position; the
+// warps then copy each chunk's records into the ordered list, prepending the
+// carried-in run to an open record (seg_merge is associative, so this equals
+// merging in order). CTA aggregates live in cincl[0, nb), inclusive prefixes in
+// cincl[nb, 2nb) (cincl is otherwise unused); flags in cflag.
+constexpr int kSsScanB = 256;
+__global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) {
+    __shared__ SegF sws[9];
+    __shared__ SegF s_cin[kSsScanB];
+    __shared__ int s_cnt[kSsScanB];
+    __shared__ int s_b;
+    const SsState& S = sts.s[blockIdx.y];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) s_b = atomicAdd(S.ticket, 1) - nch;
+    __syncthreads();
+    const int b = s_b, nb = (nch + kSsScanB - 1) / kSsScanB;
+    const int c = b * kSsScanB + t;
+    const SegF a = c < nch ? agg_load(S.cagg, c) : segf_id();
+    SegF tot;
+    const SegF ex = block_excl_segscan(a, sws, &tot);
+    unsigned char* bagg = S.cincl;
+    unsigned char* bincl = S.cincl + (size_t)nb * sizeof(ChunkAgg);
+    if (t == 0) {
+        if (b == 0) {
+            agg_store(bincl, 0, tot);
+            st_flag(S.cflag, 2);
+        } else {
+            agg_store(bagg, b, tot);
+            st_flag(S.cflag + b, 1);
+        }
+    }
+    if (w == 0) {
+        const SegF pre = b > 0 ? lookback_seg(b, S.cflag, bagg, bincl) : segf_id();
+        if (t == 0) {
+            const SegF inc = segf_combine(pre, tot);
+            if (b > 0) {
+                agg_store(bincl, b, inc);
+                st_flag(S.cflag + b, 2);
+            }
+            if (b == nb - 1) *S.total = inc.cnt;
+            sws[8] = pre;
+        }
+    }
+    __syncthreads();
+    s_cin[t] = segf_combine(sws[8], ex);
+    s_cnt[t] = c < nch ? a.cnt : 0;
+    __syncthreads();
+    // compaction: warp w takes chunks w, w+8, ...; lanes copy a chunk's records
+    for (int q = w; q < kSsScanB; q += 8) {
+        const int cnt = s_cnt[q];
+        if (cnt == 0) continue;
+        const SegF& cin = s_cin[q];
+        const gmg_ss::Rec* src = S.recs + (long long)(b * kSsScanB + q) * kSsRMax;
+        gmg_ss::Rec* dst = S.recs2 + cin.cnt;
+        for (int j = lane; j < cnt; j += 32) {
+            gmg_ss::Rec r = src[j];
+            if (r.meta & kRecOpen) {
+                const bool brk = (r.meta >> 12) & 1u;
+                r = gmg_ss::rec_make(gmg_ss::seg_merge(cin.g, gmg_ss::rec_seg(r)), brk, r.pb, r.kb);
+            }
+            dst[j] = r;
+        }
+    }
+}
+
 // ---- chain --------------------------------------------------------------------
 // Both re-sum paths read terms through a register ring of kSsRing batches of 32
 // (lane = term within a batch), so ~kSsRing*256 B per warp are in flight and the

@@ -357,8 +357,7 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) 
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
     k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp, pre0);
-    k_ss_scan<<<NS, std::min(kSsScanT, (nch + 31) / 32 * 32), 0, p->st>>>(sp, nch);
-    k_ss_compact<<<dim3((nch + 7) / 8, NS), 256, 0, p->st>>>(sp, nch);
+    k_ss_scan2<<<dim3((nch + kSsScanB - 1) / kSsScanB, NS), kSsScanB, 0, p->st>>>(sp, nch);
     CK(cudaGetLastError());
 }
 
@@ -1859,7 +1858,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         p->X[1] = p->xmem + F.elems + F.off0;
         p->B = p->xmem + 2 * F.elems + F.off0;
         const long long n = F.n();
-        p->nch_max = (int)((n + kSsC - 1) / kSsC);
+        p->nch_max = (int)std::max<long long>(2, (n + kSsC - 1) / kSsC);  // >= 2: k_ss_scan2 keeps 2 CTA slots in cincl
         const size_t nm = p->nch_max;
         CK(cudaMalloc(&p->csum, 2 * nm * sizeof(double)));
         CK(cudaMalloc(&p->T, 2 * (size_t)n * sizeof(double)));
