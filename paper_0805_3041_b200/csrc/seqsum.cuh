@@ -44,8 +44,8 @@ struct SsState {
     int* cflag;      // [nch] run/count look-back flags
     int* ticket;     // [1]
     int* total;      // [1] records stored
-    double* agg;     // [nch]
-    double* incl;    // [nch]
+    longlong2* lbw;  // [nch] approximate-sum look-back words {value bits, status 0/1/2};
+                     //       zeroed at allocation and, after each walk, by k_ss_scan2
     unsigned char* cagg;   // [nch] ChunkAgg
     unsigned char* cincl;  // [nch] ChunkAgg
     gmg_ss::Rec* recs;   // [nch * kSsRMax] per-chunk record slots written by the walk
@@ -160,25 +160,42 @@ __device__ __forceinline__ SegF agg_load(const unsigned char* base, int c) {
     return v;
 }
 
+// Approximate-prefix look-back words: value and status in one 16-byte word
+// (one relaxed vector store / load, no fences). The prefix only seeds the
+// speculative walk — the chain validates every segment from the exact state —
+// so nothing here can change a result, only the number of re-walks.
+__device__ __forceinline__ void lbw_store(longlong2* p, double v, long long status) {
+    asm volatile("st.relaxed.gpu.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(__double_as_longlong(v)),
+                 "l"(status)
+                 : "memory");
+}
+__device__ __forceinline__ longlong2 lbw_load(const longlong2* p) {
+    longlong2 r;
+    asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+    return r;
+}
+
 // Decoupled look-back (one warp) for chunk c: approximate double prefix.
-__device__ double lookback_d(int c, const int* flag, const double* agg, const double* incl) {
+__device__ double lookback_d(int c, const longlong2* lbw) {
     const int lane = threadIdx.x & 31;
     double acc = 0.0;
     int p = c - 1;
     while (p >= 0) {
         const int idx = p - lane;
-        int f = 2;
-        if (idx >= 0) {
-            while ((f = ld_flag(flag + idx)) == 0) __nanosleep(64);
-        }
-        __threadfence();
-        const unsigned m2 = __ballot_sync(0xffffffffu, f == 2);
-        const int stop = m2 ? __ffs(m2) - 1 : 32;
+        long long st = 2;
         double v = 0.0;
         if (idx >= 0) {
-            if (lane < stop) v = __ldcg(agg + idx);
-            else if (lane == stop) v = __ldcg(incl + idx);
+            longlong2 wd = lbw_load(lbw + idx);
+            while (wd.y == 0) {
+                __nanosleep(32);
+                wd = lbw_load(lbw + idx);
+            }
+            st = wd.y;
+            v = __longlong_as_double(wd.x);
         }
+        const unsigned m2 = __ballot_sync(0xffffffffu, st == 2);
+        const int stop = m2 ? __ffs(m2) - 1 : 32;
+        if (lane > stop) v = 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         acc += v;
@@ -385,22 +402,14 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     // pre0: approximate sum of the terms before this range (earlier row slabs)
     const double base_pre = pre0 ? pre0[s] : 0.0;
     if (t == 0) {
-        if (c == 0) {
-            S.incl[0] = base_pre + tot_approx;
-            st_flag(S.flag, 2);
-        } else {
-            S.agg[c] = tot_approx;
-            st_flag(S.flag + c, 1);
-        }
+        if (c == 0) lbw_store(S.lbw, base_pre + tot_approx, 2);
+        else lbw_store(S.lbw + c, tot_approx, 1);
     }
     if (t < 32) {
-        const double pre = c == 0 ? base_pre : lookback_d(c, S.flag, S.agg, S.incl);
+        const double pre = c == 0 ? base_pre : lookback_d(c, S.lbw);
         if (t == 0) {
             s_pre = pre;
-            if (c > 0) {
-                S.incl[c] = pre + tot_approx;
-                st_flag(S.flag + c, 2);
-            }
+            if (c > 0) lbw_store(S.lbw + c, pre + tot_approx, 2);
         }
     }
     __syncthreads();
@@ -657,6 +666,7 @@ __global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) {
     __syncthreads();
     s_cin[t] = segf_combine(sws[8], ex);
     s_cnt[t] = c < nch ? a.cnt : 0;
+    if (c < nch) lbw_store(S.lbw + c, 0.0, 0);  // reset the walk's look-back word for the next sum
     __syncthreads();
     // compaction: warp w takes chunks w, w+8, ...; lanes copy a chunk's records
     for (int q = w; q < kSsScanB; q += 8) {

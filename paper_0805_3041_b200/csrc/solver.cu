@@ -319,8 +319,7 @@ SsPair ss_state(gmg_problem* p, int nch) {
         S.total = f + 1;
         S.flag = f + 2;
         S.cflag = f + 2 + nch;
-        S.agg = p->lb + (size_t)s * 2 * p->nch_max;
-        S.incl = S.agg + p->nch_max;
+        S.lbw = reinterpret_cast<longlong2*>(p->lb + (size_t)s * 2 * p->nch_max);
         S.cagg = p->lbs + (size_t)s * 2 * p->nch_max * sizeof(ChunkAgg);
         S.cincl = S.cagg + (size_t)p->nch_max * sizeof(ChunkAgg);
         S.recs = p->recs + (size_t)s * p->rec_cap;
@@ -1863,6 +1862,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         CK(cudaMalloc(&p->csum, 2 * nm * sizeof(double)));
         CK(cudaMalloc(&p->T, 2 * (size_t)n * sizeof(double)));
         CK(cudaMalloc(&p->lb, 2 * 2 * nm * sizeof(double)));
+        CK(cudaMemset(p->lb, 0, 2 * 2 * nm * sizeof(double)));  // look-back words start empty
         CK(cudaMalloc(&p->lbs, 2 * 2 * nm * sizeof(ChunkAgg)));
         CK(cudaMalloc(&p->flags, 2 * (2 + 2 * nm) * sizeof(int)));
         // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
