@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if force or _newer(o, [s, *deps]):
             if verbose:
                 print("nvcc", src, flush=True)
-            _run([NVCC, *NVFLAGS, "-c", s, "-o", o], o + ".log")
+            extra = os.environ.get("GMG_EXTRA_NVFLAGS", "").split()  # e.g. -DGMG_KDEBUG (debug builds)
+            _run([NVCC, *NVFLAGS, *extra, "-c", s, "-o", o], o + ".log")
         objs.append(o)
     for src in SOURCES_CPP:
         s = os.path.join(CSRC, src)

@@ -31,7 +31,10 @@ namespace gmg_dev {
 
 constexpr int kSsT = 256;             // threads per chunk
 constexpr int kSsEPT = 32;            // terms per thread
-constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk
+constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk (large sums)
+constexpr int kSsEPTs = 8;            // terms per thread for small sums
+constexpr int kSsCs = kSsT * kSsEPTs; // terms per chunk (small sums)
+constexpr long long kSsSmallMax = 0;  // sums up to this length use small chunks (off: GMG_SS_SMALL_MAX)
 constexpr uint32_t kRecOpen = 1u << 16;  // Rec.meta: the carried-in run is still to be prepended
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
@@ -353,8 +356,9 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [9
 __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 
 // ---- walk ---------------------------------------------------------------------
-// grid (nch, NS); block kSsT; dynamic smem (kSsC + kSsC/32) doubles.
-template <class TG>
+// grid (nch, NS); block kSsT; dynamic smem (C + C/32) doubles, C = kSsT * EPT terms
+// per chunk (EPT = 32, or 8 for small sums: 4x shorter serial thread walks).
+template <class TG, int EPT>
 __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
                                                        const double* __restrict__ pre0) {
     extern __shared__ double tm[];
@@ -372,24 +376,25 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     if (t == 0) s_chunk = atomicAdd(S.ticket, 1);
     __syncthreads();
     const int c = s_chunk;
-    const long long base = (long long)c * kSsC;
-    const int clen = (int)min((long long)kSsC, n - base);
+    constexpr int kC = kSsT * EPT;
+    const long long base = (long long)c * kC;
+    const int clen = (int)min((long long)kC, n - base);
 
     // (1) terms: striped (coalesced) loads, all in flight before the smem stores
     {
-        double v[kSsEPT];
-        tg.striped(s, base + t, clen, v);
+        double v[EPT];
+        tg.template striped<EPT>(s, base + t, clen, v);
 #pragma unroll
-        for (int m = 0; m < kSsEPT; ++m) tm[ss_pad(m * kSsT + t)] = v[m];
+        for (int m = 0; m < EPT; ++m) tm[ss_pad(m * kSsT + t)] = v[m];
     }
     __syncthreads();
-    const int e0 = t * kSsEPT;
-    const int ne = max(0, min(kSsEPT, clen - e0));
+    const int e0 = t * EPT;
+    const int ne = max(0, min(EPT, clen - e0));
     double ts = 0.0;  // approximate (tree-order) sum of this thread's terms
-    if (ne == kSsEPT) {
+    if (ne == EPT) {
         double a4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int m = 0; m < kSsEPT; ++m) a4[m & 3] += tm[ss_pad(e0 + m)];
+        for (int m = 0; m < EPT; ++m) a4[m & 3] += tm[ss_pad(e0 + m)];
         ts = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     } else {
         for (int m = 0; m < ne; ++m) ts += tm[ss_pad(e0 + m)];
@@ -421,17 +426,17 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     gmg_ss::walker_init(wk, pred);
     gmg_ss::Seg lead = gmg_ss::seg_empty();
     int r = 0;
-    // Fast path: all kSsEPT terms stay in the binade without ties. The increments
+    // Fast path: all EPT terms stay in the binade without ties. The increments
     // q_m = RN(p_m/u) are independent, only their prefix sums are a chain; the
     // range test on the prefix extremes equals the walker's per-step tests (the
     // sign cannot change: |q| < 2^52 <= |M|). Same state and segment as
     // walker_try would leave; otherwise the element-wise walk below.
     bool fast = false;
-    if (ne == kSsEPT && wk.E != 0) {
+    if (ne == EPT && wk.E != 0) {
         double P = 0.0, mn = 0.0, mx = 0.0;
         bool ok = true;
 #pragma unroll
-        for (int m = 0; m < kSsEPT; ++m) {
+        for (int m = 0; m < EPT; ++m) {
             const double x = tm[ss_pad(e0 + m)] * wk.inv_u;  // exact power-of-two scaling
             const double q = rint(x);
             ok = ok && (x < gmg_ss::kTwo52 && x > -gmg_ss::kTwo52) && fabs(x - q) != 0.5;
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
             wk.Q[0] = P;
             wk.mn[0] = mn;
             wk.mx[0] = mx;
-            wk.len = kSsEPT;
+            wk.len = EPT;
             wk.M = M + P;
             fast = true;
         }
@@ -987,7 +992,8 @@ __global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double*
     if (threadIdx.x == 0) csum[(long long)s * nch + blockIdx.x] = acc;
 }
 
-constexpr size_t ss_walk_smem() { return sizeof(double) * (kSsC + kSsC / 32); }
+template <int EPT>
+constexpr size_t ss_walk_smem() { return sizeof(double) * (kSsT * EPT + kSsT * EPT / 32); }
 constexpr size_t ss_chain_smem() { return sizeof(gmg_ss::Rec) * 2 * kSsBatch; }
 
 // ---- term generators ----------------------------------------------------------
@@ -1003,8 +1009,9 @@ __device__ __forceinline__ int row_of(long long k, int nx, double inv_nx) {
 // `striped(s, k0, clen, v)` fills v[m] = term k0 + m*kSsT (0 past the chunk),
 // where k0 = chunk base + threadIdx.x and clen = terms in the chunk.
 #define GMG_SS_STRIPED_DEFAULT                                                              \
-    __device__ __forceinline__ void striped(int s, long long k0, int clen, double (&v)[kSsEPT]) const { \
-        _Pragma("unroll") for (int m = 0; m < kSsEPT; ++m) {                                \
+    template <int EPT>                                                                       \
+    __device__ __forceinline__ void striped(int s, long long k0, int clen, double (&v)[EPT]) const { \
+        _Pragma("unroll") for (int m = 0; m < EPT; ++m) {                                   \
             const int kl = m * kSsT + (int)threadIdx.x;                                      \
             v[m] = kl < clen ? term(s, k0 + m * kSsT) : 0.0;                                 \
         }                                                                                    \
@@ -1021,10 +1028,11 @@ struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid f
         return v * v;
     }
     // row/column of the first term once, then stepped by kSsT (no per-term division)
-    __device__ __forceinline__ void striped(int, long long k0, int clen, double (&v)[kSsEPT]) const {
+    template <int EPT>
+    __device__ __forceinline__ void striped(int, long long k0, int clen, double (&v)[EPT]) const {
         int j = row_of(k0, g.nx, inv_nx), i = (int)(k0 - (long long)j * g.nx);
 #pragma unroll
-        for (int m = 0; m < kSsEPT; ++m) {
+        for (int m = 0; m < EPT; ++m) {
             const int kl = m * kSsT + (int)threadIdx.x;
             double x = 0.0;
             if (kl < clen) x = __ldg(r + g.at(i, j));

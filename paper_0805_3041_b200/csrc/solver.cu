@@ -29,6 +29,7 @@
 #include "../../include/gmg_b200.h"
 #include "common.cuh"
 #include "host_setup.h"
+#include "dalloc.h"
 #include "gs.cuh"
 #include "linesm.cuh"
 #include "march.cuh"
@@ -52,7 +53,22 @@ struct GmgError {
     do {                                                                                       \
         cudaError_t e_ = (x);                                                                  \
         if (e_ != cudaSuccess)                                                                 \
-            throw GmgError{GMG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};     \
+            throw GmgError{GMG_ERR_CUDA, std::string(#x) + " (solver.cu:" + std::to_string(__LINE__) + \
+                                             "): " + cudaGetErrorString(e_)};                 \
+    } while (0)
+
+// after a launch: the launch error, and with GMG_DEBUG_SYNC the kernel's own
+// completion status (debugging: pinpoints a faulting launch by line)
+static const bool g_debug_sync = getenv("GMG_DEBUG_SYNC") != nullptr;
+inline void dbg_sync(int line) {
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+        throw GmgError{GMG_ERR_CUDA, "debug sync after solver.cu:" + std::to_string(line) + ": " + cudaGetErrorString(e)};
+}
+#define KCHECK()                                        \
+    do {                                                \
+        CK(cudaGetLastError());                         \
+        if (g_debug_sync) dbg_sync(__LINE__);           \
     } while (0)
 
 template <class F>
@@ -310,6 +326,15 @@ void set_smem(T* fn, size_t bytes) {
                             (int)bytes));
 }
 
+// sums up to this length walk in small chunks (GMG_SS_SMALL_MAX overrides, for A/B timing)
+long long ss_small_max() {
+    static const long long v = [] {
+        const char* e = getenv("GMG_SS_SMALL_MAX");
+        return e ? atoll(e) : kSsSmallMax;
+    }();
+    return v;
+}
+
 SsPair ss_state(gmg_problem* p, int nch) {
     SsPair sp{};
     for (int s = 0; s < kSsMaxSums; ++s) {
@@ -325,6 +350,7 @@ SsPair ss_state(gmg_problem* p, int nch) {
         S.recs = p->recs + (size_t)s * p->rec_cap;
         S.recs2 = p->recs2 + (size_t)s * p->rec_cap;
         S.stats = p->ss_stats;
+
     }
     return sp;
 }
@@ -333,10 +359,29 @@ template <class TG>
 void seqsum_attrs() {
     static bool attr_done = false;
     if (!attr_done) {
-        set_smem(k_ss_walk<TG>, ss_walk_smem());
+        set_smem(k_ss_walk<TG, kSsEPT>, ss_walk_smem<kSsEPT>());
+        set_smem(k_ss_walk<TG, kSsEPTs>, ss_walk_smem<kSsEPTs>());
         set_smem(k_ss_chain<TG>, ss_chain_smem());
         attr_done = true;
     }
+}
+
+// Loads (lazy module loading) and configures every exact-sum kernel before any
+// graph capture, so no kernel is first touched while a stream is capturing.
+void preload_seqsum_kernels() {
+    static bool done = false;
+    if (done) return;
+    seqsum_attrs<NormTerms>();
+    seqsum_attrs<ArrTerms>();
+    seqsum_attrs<DotTerms>();
+    seqsum_attrs<FlatNormTerms>();
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, k_ss_scan2));
+    CK(cudaFuncGetAttributes(&fa, k_ss_direct<NormTerms>));
+    CK(cudaFuncGetAttributes(&fa, k_ss_direct<ArrTerms>));
+    CK(cudaFuncGetAttributes(&fa, k_ss_direct<DotTerms>));
+    CK(cudaFuncGetAttributes(&fa, k_ss_direct<FlatNormTerms>));
+    done = true;
 }
 
 // Sums of TG's NS term sequences, each bit-identical to the reference's
@@ -348,16 +393,21 @@ void seqsum_attrs() {
 template <class TG>
 void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) {
     constexpr int NS = TG::NS;
-    const int nch = (int)((n + kSsC - 1) / kSsC);
+    const bool small = n <= ss_small_max();
+    const int cs = small ? kSsCs : kSsC;
+    const int nch = (int)((n + cs - 1) / cs);
     if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
     seqsum_attrs<TG>();
     if (n <= kSsDirect) return;  // the direct kernel needs no walk
     const SsPair sp = ss_state(p, nch);
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
-    k_ss_walk<TG><<<dim3(nch, NS), kSsT, ss_walk_smem(), p->st>>>(tg, n, nch, sp, pre0);
+    if (small)
+        k_ss_walk<TG, kSsEPTs><<<dim3(nch, NS), kSsT, ss_walk_smem<kSsEPTs>(), p->st>>>(tg, n, nch, sp, pre0);
+    else
+        k_ss_walk<TG, kSsEPT><<<dim3(nch, NS), kSsT, ss_walk_smem<kSsEPT>(), p->st>>>(tg, n, nch, sp, pre0);
     k_ss_scan2<<<dim3((nch + kSsScanB - 1) / kSsScanB, NS), kSsScanB, 0, p->st>>>(sp, nch);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <class TG>
@@ -368,17 +418,18 @@ void seqsum_chain(gmg_problem* p, const TG& tg, long long n, double* out, const 
             CK(cudaMemcpyAsync(out, start, NS * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
         else
             CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
+            if (g_debug_sync) dbg_sync(__LINE__);
         return;
     }
     if (n <= kSsDirect) {
         k_ss_direct<TG><<<NS, 256, n * sizeof(double), p->st>>>(tg, (int)n, out, start);
-        CK(cudaGetLastError());
+        KCHECK();
         return;
     }
     const int nch = (int)((n + kSsC - 1) / kSsC);
     const SsPair sp = ss_state(p, nch);
     k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, sp, out, start);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 // tree-order partial sums of the NS sequences into out (fast mode; also the
@@ -393,11 +444,12 @@ void seqsum_fast(gmg_problem* p, const TG& tg, long long n, double* out, const d
             CK(cudaMemcpyAsync(out, start, NS * sizeof(double), cudaMemcpyDeviceToDevice, p->st));
         else
             CK(cudaMemsetAsync(out, 0, NS * sizeof(double), p->st));
+            if (g_debug_sync) dbg_sync(__LINE__);
         return;
     }
     k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
     k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out, start);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <class TG>
@@ -433,7 +485,7 @@ void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.rows() + seg - 1) / seg);
     k_smooth<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <int M, class Coef, class Src>
@@ -445,7 +497,7 @@ void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& sr
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
     k_smooth2<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <int M, int SK, class Coef>
@@ -465,7 +517,7 @@ void launch_smooth3_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
     k_smooth3<M, kTW, D, SK, Coef><<<grid, kTW, sizeof(SM), p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <int M, int SK, class Coef>
@@ -485,7 +537,7 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     const int strips = (L.nx + OW - 1) / OW;
     dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
     k_smooth4<M, SK, Coef><<<grid, kS4W * 32, smem, p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 // levels at least this wide use the strip-per-warp smoother (k_smooth4)
@@ -615,7 +667,7 @@ void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src,
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
     k_resid<kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg, neg,
                                                           om);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <bool SUM, class Coef>
@@ -638,7 +690,7 @@ void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* 
     const int strips = (L.nx + 123) / 124;
     dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
     k_resid4<SUM, Coef><<<grid, kS4W * 32, smem, p->st>>>(L.grid(), A, u, e, g, dout, x0out, cg, rw, gc, seg);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 // residual of (u, or x+e when e != null) against g; optional outputs.
@@ -695,6 +747,7 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
     const int blocks = (warps + kGsWarps - 1) / kGsWarps;
     if (blocks > 148) throw GmgError{GMG_ERR_UNSUPPORTED, "gs: more rows than one co-resident wavefront"};
     CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
     static bool attr = false;
     if (!attr) {
         set_smem(k_gs_wave<Pol>, gs_smem());
@@ -702,7 +755,7 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
     }
     k_gs_wave<Pol><<<blocks, kGsWarps * 32, gs_smem(), p->st>>>(L.grid(), pol, d, x, xo, damp, p->gs_edge,
                                                                  p->gs_prog);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 // One lexicographic Gauss-Seidel/SOR smooth_step: x' = x - damp * (D + om L)^{-1} (A x - g).
@@ -726,7 +779,7 @@ void launch_line(gmg_problem* p, const Lev& L, const LineFactors& f, const doubl
                  const double* x, const double* z1, double* out, double damp) {
     const int nl = DIR == 0 ? L.ny : L.nx;
     k_line<DIR, MODE><<<(nl + kLineT - 1) / kLineT, kLineT, 0, p->st>>>(L.grid(), f, rhs, ybuf, x, z1, out, damp);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 template <int DIR, int MODE>
@@ -738,7 +791,7 @@ void launch_gstri(gmg_problem* p, const Lev& L, double om, const LineFactors& f,
         k_gstri<DIR, MODE, C><<<1, 32, 0, p->st>>>(L.grid(), A, om, f, rhs, x, z1, out, p->linebuf,
                                                    p->linebuf + nmax, damp);
     });
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 // One smooth_step (smoother.cpp:389-399) of a non-Jacobi kind, given the
@@ -755,7 +808,7 @@ void pc_apply(gmg_problem* p, const Lev& L, const gmg_cycle_desc& sp, const SmLe
         case GMG_SMOOTHER_RICHARDSON: {
             dim3 gr((L.nx + 127) / 128, L.ny);
             k_rich_update<<<gr, 128, 0, p->st>>>(L.grid(), d, x, out, m->rich, damp);
-            CK(cudaGetLastError());
+            KCHECK();
             return;
         }
         case GMG_SMOOTHER_ILU0:
@@ -839,13 +892,13 @@ void launch_restrict(gmg_problem* p, int fine_level, const double* f, double* c)
     const Lev& C = p->lev(fine_level - 1);
     dim3 b(32, 8), gr((C.nx + 31) / 32, (C.ny + 7) / 8);
     k_restrict_simple<<<gr, b, 0, p->st>>>(F.grid(), f, C.grid(), C.rw, c);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 void launch_coarse(gmg_problem* p, const double* g, double* x) {
     const Lev& L = p->lev(1);
     k_coarse_chol<<<1, 32, 0, p->st>>>(p->band, p->cn, p->cbw, L.grid(), g, x, p->cscr);
-    CK(cudaGetLastError());
+    KCHECK();
 }
 
 void norm_sum(gmg_problem* p, const Lev& L, const double* v, double* out, int mode) {
@@ -855,6 +908,7 @@ void norm_sum(gmg_problem* p, const Lev& L, const double* v, double* out, int mo
 // adaptive_omega sums for corr = P uc: terms materialised by k_omega_terms.
 void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc, int mode) {
     CK(cudaMemsetAsync(p->nz, 0, sizeof(int), p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.rows() + seg - 1) / seg);
     SrcProlong src{prolong_from(p, L.l - 1, uc), L.nx, L.ny, 0.0};
@@ -864,7 +918,7 @@ void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc,
         using C = std::decay_t<decltype(A)>;
         k_omega_terms<kTW, 2, C><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, d, T0, T1, p->nz, seg);
     });
-    CK(cudaGetLastError());
+    KCHECK();
     seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, mode);
 }
 
@@ -929,8 +983,10 @@ void dist_halo(const std::vector<gmg_problem*>& S, DistCtx& D, int l, int id, in
             const int e = w1[r];  // == w0[r + 1]
             const RowSpan up = rows_of(S[r], l, id, e - rows, e), upd = rows_of(S[r + 1], l, id, e - rows, e);
             CK(cudaMemcpyAsync(upd.p, up.p, up.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            if (g_debug_sync) dbg_sync(__LINE__);
             const RowSpan dn = rows_of(S[r + 1], l, id, e, e + rows), dnd = rows_of(S[r], l, id, e, e + rows);
             CK(cudaMemcpyAsync(dnd.p, dn.p, dn.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            if (g_debug_sync) dbg_sync(__LINE__);
         }
         return;
     }
@@ -962,6 +1018,7 @@ void dist_gather(const std::vector<gmg_problem*>& S, DistCtx& D, int l, int id, 
                     const RowSpan src = rows_of(S[r], l, id, a[r], b[r]), dst = rows_of(S[t], l, id, a[r], b[r]);
                     if (src.count)
                         CK(cudaMemcpyAsync(dst.p, src.p, src.count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                    if (g_debug_sync) dbg_sync(__LINE__);
                 }
         return;
     }
@@ -1032,7 +1089,7 @@ void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int o
         seqsum_fast(q, tn.first, tn.second, q->dscr, nullptr);
         if (with_nz) k_nz_to_d<<<1, 1, 0, st>>>(q->nz, q->dscr + NS);
     }
-    CK(cudaGetLastError());
+    KCHECK();
     if (D->local) {
         for (auto* q : S)
             for (auto* t : S)
@@ -1044,7 +1101,7 @@ void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int o
     for (auto* q : S)
         k_dist_prefix<<<1, 32, 0, st>>>(q->dscr + 32, q->rank, D->world, NS, with_nz ? 1 : 0, q->dscr + 8, q->nz,
                                         mode == GMG_REDUCE_FAST ? q->sums + out_off : nullptr);
-    CK(cudaGetLastError());
+    KCHECK();
     if (mode == GMG_REDUCE_FAST) return;
     // 2. walks (independent), 3. chains in rank order, 4. broadcast of the total
     for (auto* q : S) {
@@ -1202,7 +1259,7 @@ struct Driver {
             attr = true;
         }
         k_vsmall<<<1, kVThreads, vsmall_smem(l), q->st>>>(V);
-        CK(cudaGetLastError());
+        KCHECK();
     }
 
     // gmg::mg_cycle (cycle.cpp:69-100) on level l from start s with rhs g.
@@ -1256,6 +1313,7 @@ struct Driver {
         for (auto* q : S) {
             Lev& L = q->lev(l);
             CK(cudaMemsetAsync(q->nz, 0, sizeof(int), q->st));
+            if (g_debug_sync) dbg_sync(__LINE__);
             const int seg = seg_rows(L.nx, L.rows());
             dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.rows() + seg - 1) / seg);
             SrcProlong src{prolong_from(q, l - 1, q->lev(l - 1).buf[uc]), L.nx, L.ny, 0.0};
@@ -1278,7 +1336,7 @@ struct Driver {
                                                                        seg);
                 }
             });
-            CK(cudaGetLastError());
+            KCHECK();
         }
         dist_sum(S, sharded(l) ? D() : nullptr, [&](gmg_problem* q) {
             const Lev& L = q->lev(l);
@@ -1444,14 +1502,17 @@ void check_cycle(const gmg_problem* p, const gmg_cycle_desc& sp) {
 void upload(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
     CK(cudaMemcpy2DAsync(dst, L.pitch * sizeof(double), src, L.nx * sizeof(double), L.nx * sizeof(double),
                          L.ny, kind, p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
 }
 void download(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
     CK(cudaMemcpy2DAsync(dst, L.nx * sizeof(double), src, L.pitch * sizeof(double), L.nx * sizeof(double),
                          L.ny, kind, p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
 }
 
 double fetch_scalar(gmg_problem* p, const double* dev) {
     CK(cudaMemcpyAsync(p->hostbuf, dev, sizeof(double), cudaMemcpyDeviceToHost, p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
     CK(cudaStreamSynchronize(p->st));
     return p->hostbuf[0];
 }
@@ -1459,6 +1520,7 @@ double fetch_scalar(gmg_problem* p, const double* dev) {
 int fetch_status(gmg_problem* p) {
     int s = 0;
     CK(cudaMemcpyAsync(&s, p->status, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
     CK(cudaStreamSynchronize(p->st));
     return s;
 }
@@ -1498,8 +1560,9 @@ void host_coefs(gmg_problem* p, const Lev& L, std::vector<double> (&a)[5]) {
 
 void ensure_scratch(gmg_problem* p, Lev& L) {
     if (L.scrmem) return;
-    CK(cudaMalloc(&L.scrmem, 2 * L.elems * sizeof(double)));
+    CK(dmalloc(&L.scrmem, 2 * L.elems * sizeof(double)));
     CK(cudaMemsetAsync(L.scrmem, 0, 2 * L.elems * sizeof(double), p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
     L.scr[0] = L.scrmem + L.off0;
     L.scr[1] = L.scrmem + L.elems + L.off0;
 }
@@ -1520,12 +1583,12 @@ double richardson_omega(gmg_problem* p, Lev& L, double omega) {
             dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
             k_apply_simple<<<gr, b, 0, p->st>>>(L.grid(), A, xa, ya);
         });
-        CK(cudaGetLastError());
+        KCHECK();
         norm_sum(p, L, ya, p->sums + 3, GMG_REDUCE_EXACT);
         lambda = std::sqrt(fetch_scalar(p, p->sums + 3));
         if (lambda == 0.0) break;
         k_div_scalar<<<dim3((L.nx + 127) / 128, L.ny), 128, 0, p->st>>>(L.grid(), ya, lambda);
-        CK(cudaGetLastError());
+        KCHECK();
         std::swap(xa, ya);
     }
     if (lambda > 0.0 && omega > 1.0 / lambda) return 0.9 / lambda;
@@ -1563,8 +1626,9 @@ const SmSetup* ensure_smoother(gmg_problem* p, int kind, double omega) {
                 std::vector<double> lw(N), ls(N), dp(N);
                 gmg_host::factor_ilu0(L.nx, L.ny, a[0].data(), a[1].data(), a[2].data(), a[3].data(), a[4].data(),
                                       lw.data(), ls.data(), dp.data());
-                CK(cudaMalloc(&m.mem, 3 * L.elems * sizeof(double)));
+                CK(dmalloc(&m.mem, 3 * L.elems * sizeof(double)));
                 CK(cudaMemsetAsync(m.mem, 0, 3 * L.elems * sizeof(double), p->st));
+                if (g_debug_sync) dbg_sync(__LINE__);
                 double* q[3] = {m.mem + L.off0, m.mem + L.elems + L.off0, m.mem + 2 * L.elems + L.off0};
                 upload(p, L, q[0], lw.data(), cudaMemcpyHostToDevice);
                 upload(p, L, q[1], ls.data(), cudaMemcpyHostToDevice);
@@ -1577,9 +1641,11 @@ const SmSetup* ensure_smoother(gmg_problem* p, int kind, double omega) {
             } else {
                 const bool fx = uses_x_lines(kind), fy = uses_y_lines(kind);
                 const int nset = (int)fx + (int)fy;
-                CK(cudaMalloc(&m.mem, 3 * nset * L.elems * sizeof(double)));
+                CK(dmalloc(&m.mem, 3 * nset * L.elems * sizeof(double)));
                 CK(cudaMemsetAsync(m.mem, 0, 3 * nset * L.elems * sizeof(double), p->st));
+                if (g_debug_sync) dbg_sync(__LINE__);
                 CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+                if (g_debug_sync) dbg_sync(__LINE__);
                 double* base = m.mem + L.off0;
                 with_coef(L, [&](const auto& A) {
                     if (fx) {
@@ -1594,16 +1660,17 @@ const SmSetup* ensure_smoother(gmg_problem* p, int kind, double omega) {
                             L.grid(), A, omega, base, base + L.elems, base + 2 * L.elems, p->status);
                     }
                 });
-                CK(cudaGetLastError());
+                KCHECK();
                 if (fetch_status(p) == 4) {
                     CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+                    if (g_debug_sync) dbg_sync(__LINE__);
                     throw std::runtime_error("tri factorization: zero pivot");
                 }
                 if (kind == GMG_SMOOTHER_ADI || kind == GMG_SMOOTHER_GSADI) ensure_scratch(p, L);
             }
         }
     } catch (...) {
-        for (auto& m : S.lev) cudaFree(m.mem);
+        for (auto& m : S.lev) dfree(m.mem);
         throw;
     }
     return &p->smsetups.emplace(key, std::move(S)).first->second;
@@ -1651,10 +1718,18 @@ void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep,
         return;
     }
     check_cycle(p, sp);
-    auto& ex = get_graphs(p, sp);
+    // GMG_NO_GRAPH=1 runs the cycle's launches directly (debugging with CUDA_LAUNCH_BLOCKING)
+    static const bool no_graph = getenv("GMG_NO_GRAPH") != nullptr;
+    auto& ex = no_graph ? p->graphs[""] : get_graphs(p, sp);
     int par = 0;
     for (int k = 1; k <= sp.max_cycles; ++k) {
-        CK(cudaGraphLaunch(ex[par], p->st));
+        if (no_graph) {
+            Driver d{driver_slabs(p), sp, find_smoother(p, sp)};
+            d.cycle(par == 0 ? B_X0 : B_X1, par == 0 ? B_X1 : B_X0);
+            CK(cudaStreamSynchronize(p->st));
+        } else {
+            CK(cudaGraphLaunch(ex[par], p->st));
+        }
         par = 1 - par;
         const double rk = std::sqrt(fetch_scalar(p, p->sums + 2));
         if (sp.adaptive_correction && fetch_status(p) == 3) {
@@ -1688,35 +1763,35 @@ void free_problem(gmg_problem* p) {
             if (q != p) free_problem(q);
         D->slabs.clear();
     }
-    cudaFree(p->dscr);
+    dfree(p->dscr);
     for (auto& kv : p->graphs)
         for (auto g : kv.second)
             if (g) cudaGraphExecDestroy(g);
     for (auto& kv : p->smsetups)
-        for (auto& m : kv.second.lev) cudaFree(m.mem);
-    cudaFree(p->linebuf);
+        for (auto& m : kv.second.lev) dfree(m.mem);
+    dfree(p->linebuf);
     for (auto& L : p->lv) {
-        cudaFree(L.scrmem);
-        cudaFree(L.mem);
-        cudaFree(L.coefmem);
-        cudaFree(L.wmem);
+        dfree(L.scrmem);
+        dfree(L.mem);
+        dfree(L.coefmem);
+        dfree(L.wmem);
     }
-    cudaFree(p->xmem);
-    cudaFree(p->band);
-    cudaFree(p->cscr);
-    cudaFree(p->csum);
-    cudaFree(p->T);
-    cudaFree(p->lb);
-    cudaFree(p->lbs);
-    cudaFree(p->flags);
-    cudaFree(p->recs);
-    cudaFree(p->recs2);
-    cudaFree(p->ss_stats);
-    cudaFree(p->gs_edge);
-    cudaFree(p->gs_prog);
-    cudaFree(p->sums);
-    cudaFree(p->nz);
-    cudaFree(p->status);
+    dfree(p->xmem);
+    dfree(p->band);
+    dfree(p->cscr);
+    dfree(p->csum);
+    dfree(p->T);
+    dfree(p->lb);
+    dfree(p->lbs);
+    dfree(p->flags);
+    dfree(p->recs);
+    dfree(p->recs2);
+    dfree(p->ss_stats);
+    dfree(p->gs_edge);
+    dfree(p->gs_prog);
+    dfree(p->sums);
+    dfree(p->nz);
+    dfree(p->status);
     if (p->hostbuf) cudaFreeHost(p->hostbuf);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
@@ -1726,7 +1801,7 @@ void free_problem(gmg_problem* p) {
 
 double* alloc_pitched(size_t n_buffers, Lev& L) {
     double* m = nullptr;
-    CK(cudaMalloc(&m, n_buffers * L.elems * sizeof(double)));
+    CK(dmalloc(&m, n_buffers * L.elems * sizeof(double)));
     return m;
 }
 
@@ -1740,6 +1815,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         throw GmgError{GMG_ERR_CUDA, "no CUDA device available"};
     CK(cudaSetDevice(p->device));
     CK(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
+    if (!getenv("GMG_NO_PRELOAD")) preload_seqsum_kernels();
     CK(cudaEventCreate(&p->ev0));
     CK(cudaEventCreate(&p->ev1));
     CK(cudaMallocHost(&p->hostbuf, 4 * sizeof(double)));
@@ -1784,14 +1860,14 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
                 L.cconst.inv_c = std::ldexp(1.0, 1 - ex2);
             }
         } else if (cc.kind == gmg_host::COEF_ROWX) {
-            CK(cudaMalloc(&L.coefmem, 5 * L.nx * sizeof(double)));
+            CK(dmalloc(&L.coefmem, 5 * L.nx * sizeof(double)));
             const std::vector<double>* t[5] = {&cc.rc, &cc.rw, &cc.re, &cc.rs, &cc.rn};
             for (int q = 0; q < 5; ++q)
                 CK(cudaMemcpy(L.coefmem + q * L.nx, t[q]->data(), L.nx * sizeof(double), cudaMemcpyHostToDevice));
             L.crow = CoefRowX{L.coefmem, L.coefmem + L.nx, L.coefmem + 2 * L.nx, L.coefmem + 3 * L.nx,
                               L.coefmem + 4 * L.nx};
         } else {
-            CK(cudaMalloc(&L.coefmem, 5 * L.elems * sizeof(double)));
+            CK(dmalloc(&L.coefmem, 5 * L.elems * sizeof(double)));
             CK(cudaMemset(L.coefmem, 0, 5 * L.elems * sizeof(double)));
             const double* src[5] = {ld.c, ld.w, ld.e, ld.s, ld.n};
             double* dst[5];
@@ -1826,7 +1902,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
             for (auto* v : {&a, &b, &c, &e, &f, &g}) host.insert(host.end(), v->begin(), v->end());
         }
         if (host.empty()) continue;
-        CK(cudaMalloc(&L.wmem, host.size() * sizeof(double)));
+        CK(dmalloc(&L.wmem, host.size() * sizeof(double)));
         CK(cudaMemcpy(L.wmem, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice));
         if (l >= 2) {
             L.tx = L.wmem + o_tx;
@@ -1844,46 +1920,49 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         std::vector<double> band = gmg_host::cholesky_band(ld.c, ld.w, ld.s, ld.nx, ld.ny);
         p->cn = ld.nx * ld.ny;
         p->cbw = ld.nx;
-        CK(cudaMalloc(&p->band, band.size() * sizeof(double)));
+        CK(dmalloc(&p->band, band.size() * sizeof(double)));
         CK(cudaMemcpy(p->band, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&p->cscr, std::max(1, p->cn) * sizeof(double)));
+        CK(dmalloc(&p->cscr, std::max(1, p->cn) * sizeof(double)));
     }
     // finest x (ping-pong) and b
     {
         Lev& F = p->lv.back();
-        CK(cudaMalloc(&p->xmem, 3 * F.elems * sizeof(double)));
+        CK(dmalloc(&p->xmem, 3 * F.elems * sizeof(double)));
         CK(cudaMemset(p->xmem, 0, 3 * F.elems * sizeof(double)));
         p->X[0] = p->xmem + F.off0;
         p->X[1] = p->xmem + F.elems + F.off0;
         p->B = p->xmem + 2 * F.elems + F.off0;
         const long long n = F.n();
-        p->nch_max = (int)std::max<long long>(2, (n + kSsC - 1) / kSsC);  // >= 2: k_ss_scan2 keeps 2 CTA slots in cincl
+        // chunks of the largest sum: large chunks for the finest level, small chunks up to
+        // ss_small_max() terms; >= 2: k_ss_scan2 keeps 2 CTA slots in cincl
+        p->nch_max = (int)std::max<long long>(
+            {2, (n + kSsC - 1) / kSsC, (std::min<long long>(n, ss_small_max()) + kSsCs - 1) / kSsCs});
         const size_t nm = p->nch_max;
-        CK(cudaMalloc(&p->csum, 2 * nm * sizeof(double)));
-        CK(cudaMalloc(&p->T, 2 * (size_t)n * sizeof(double)));
-        CK(cudaMalloc(&p->lb, 2 * 2 * nm * sizeof(double)));
+        CK(dmalloc(&p->csum, 2 * nm * sizeof(double)));
+        CK(dmalloc(&p->T, 2 * (size_t)n * sizeof(double)));
+        CK(dmalloc(&p->lb, 2 * 2 * nm * sizeof(double)));
         CK(cudaMemset(p->lb, 0, 2 * 2 * nm * sizeof(double)));  // look-back words start empty
-        CK(cudaMalloc(&p->lbs, 2 * 2 * nm * sizeof(ChunkAgg)));
-        CK(cudaMalloc(&p->flags, 2 * (2 + 2 * nm) * sizeof(int)));
+        CK(dmalloc(&p->lbs, 2 * 2 * nm * sizeof(ChunkAgg)));
+        CK(dmalloc(&p->flags, 2 * (2 + 2 * nm) * sizeof(int)));
         // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
         p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
-        CK(cudaMalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
-        CK(cudaMalloc(&p->recs2, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
-        CK(cudaMalloc(&p->ss_stats, 16 * sizeof(unsigned long long)));
+        CK(dmalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
+        CK(dmalloc(&p->recs2, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
+        CK(dmalloc(&p->ss_stats, 16 * sizeof(unsigned long long)));
         int maxny = 0, maxnx = 0;
         for (const Lev& Lq : p->lv) {
             maxny = std::max(maxny, Lq.ny);
             maxnx = std::max(maxnx, Lq.nx);
         }
         p->gs_warps = (maxny + 31) / 32;
-        CK(cudaMalloc(&p->gs_edge, (size_t)p->gs_warps * maxnx * sizeof(double)));
-        CK(cudaMalloc(&p->gs_prog, p->gs_warps * sizeof(int)));
-        CK(cudaMalloc(&p->linebuf, 2 * (size_t)std::max(maxnx, maxny) * sizeof(double)));
+        CK(dmalloc(&p->gs_edge, (size_t)p->gs_warps * maxnx * sizeof(double)));
+        CK(dmalloc(&p->gs_prog, p->gs_warps * sizeof(int)));
+        CK(dmalloc(&p->linebuf, 2 * (size_t)std::max(maxnx, maxny) * sizeof(double)));
         CK(cudaMemset(p->ss_stats, 0, 16 * sizeof(unsigned long long)));
-        CK(cudaMalloc(&p->sums, 8 * sizeof(double)));
+        CK(dmalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
-        CK(cudaMalloc(&p->nz, sizeof(int)));
-        CK(cudaMalloc(&p->status, sizeof(int)));
+        CK(dmalloc(&p->nz, sizeof(int)));
+        CK(dmalloc(&p->status, sizeof(int)));
         CK(cudaMemset(p->status, 0, sizeof(int)));
     }
     CK(cudaDeviceSynchronize());
@@ -1939,7 +2018,7 @@ void create_slabs(const gmg_problem_desc* d, const gmg_slab_desc* sl, gmg_proble
                 q->lev(l).w0 = plan.w0[l - 1][q->rank];
                 q->lev(l).w1 = plan.w1[l - 1][q->rank];
             }
-            CK(cudaMalloc(&q->dscr, (32 + 8 * (size_t)sl->world) * sizeof(double)));
+            CK(dmalloc(&q->dscr, (32 + 8 * (size_t)sl->world) * sizeof(double)));
             CK(cudaMemset(q->dscr, 0, (32 + 8 * (size_t)sl->world) * sizeof(double)));
         }
         CK(cudaDeviceSynchronize());
@@ -2099,6 +2178,7 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
         upload(p, L, L.buf[DCAS], u0, cudaMemcpyHostToDevice);
         upload(p, L, L.buf[GRHS], g, cudaMemcpyHostToDevice);
         CK(cudaMemsetAsync(p->status, 0, sizeof(int), p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         Driver d{{p}, *spec, sm};
         SrcId s;
         s.kind = S_U;
@@ -2125,7 +2205,7 @@ int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y) {
             dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
             k_apply_simple<<<gr, b, 0, p->st>>>(L.grid(), A, L.buf[U0], L.buf[U1]);
         });
-        CK(cudaGetLastError());
+        KCHECK();
         download(p, L, y, L.buf[U1], cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
     });
@@ -2203,7 +2283,7 @@ int gmg_dev_prolongation(gmg_problem* p, int coarse_level, const double* coarse,
         upload(p, C, C.buf[U0], coarse, cudaMemcpyHostToDevice);
         dim3 b(32, 8), gr((F.nx + 31) / 32, (F.ny + 7) / 8);
         k_prolong_simple<<<gr, b, 0, p->st>>>(prolong_from(p, coarse_level, C.buf[U0]), F.grid(), F.buf[U1]);
-        CK(cudaGetLastError());
+        KCHECK();
         download(p, F, fine, F.buf[U1], cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
     });
@@ -2219,18 +2299,21 @@ int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* d, const dou
         upload(p, L, L.buf[DD], d, cudaMemcpyHostToDevice);
         upload(p, L, L.buf[U0], corr, cudaMemcpyHostToDevice);
         CK(cudaMemsetAsync(p->nz, 0, sizeof(int), p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         double* T0 = p->T;
         double* T1 = p->T + p->lev(p->L).n();
         with_coef(L, [&](const auto& A) {
             dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
             k_omega_terms_field<<<gr, b, 0, p->st>>>(L.grid(), A, L.buf[DD], L.buf[U0], T0, T1, p->nz);
         });
-        CK(cudaGetLastError());
+        KCHECK();
         seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, GMG_REDUCE_EXACT);
         double h[2];
         int nz = 0;
         CK(cudaMemcpyAsync(h, p->sums, 2 * sizeof(double), cudaMemcpyDeviceToHost, p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         CK(cudaMemcpyAsync(&nz, p->nz, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         CK(cudaStreamSynchronize(p->st));
         if (!nz) {
             *omega = 1.0;
@@ -2260,14 +2343,15 @@ static void flat_sum(gmg_problem* p, long long n, const double* a, const double*
         return;
     }
     double *da = nullptr, *db = nullptr;
-    CK(cudaMalloc(&da, n * sizeof(double)));
-    if (b) CK(cudaMalloc(&db, n * sizeof(double)));
+    CK(dmalloc(&da, n * sizeof(double)));
+    if (b) CK(dmalloc(&db, n * sizeof(double)));
     CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+    if (g_debug_sync) dbg_sync(__LINE__);
     if (b) CK(cudaMemcpyAsync(db, b, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
     // a flat vector viewed as one row; chunks never exceed the workspace (checked)
     if ((n + kSsC - 1) / kSsC > p->nch_max) {
-        cudaFree(da);
-        cudaFree(db);
+        dfree(da);
+        dfree(db);
         throw std::logic_error("norm/dot: vector longer than the finest level");
     }
     if (b)
@@ -2275,8 +2359,8 @@ static void flat_sum(gmg_problem* p, long long n, const double* a, const double*
     else
         seqsum(p, FlatNormTerms{da}, n, p->sums + 4, mode);
     *out = fetch_scalar(p, p->sums + 4);
-    cudaFree(da);
-    cudaFree(db);
+    dfree(da);
+    dfree(db);
 }
 
 int gmg_dev_norm_l2(gmg_problem* p, long long n, const double* v, int mode, double* out) {
@@ -2306,16 +2390,19 @@ int gmg_dev_axpy(gmg_problem* p, long long n, double alpha, const double* x, dou
         std::lock_guard<std::mutex> lk(p->mu);
         if (n <= 0) return;
         double *dx = nullptr, *dy = nullptr;
-        CK(cudaMalloc(&dx, n * sizeof(double)));
-        CK(cudaMalloc(&dy, n * sizeof(double)));
+        CK(dmalloc(&dx, n * sizeof(double)));
+        CK(dmalloc(&dy, n * sizeof(double)));
         CK(cudaMemcpyAsync(dx, x, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         CK(cudaMemcpyAsync(dy, y, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         k_axpy_flat<<<(unsigned)((n + 255) / 256), 256, 0, p->st>>>(n, alpha, dx, dy);
-        CK(cudaGetLastError());
+        KCHECK();
         CK(cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, p->st));
+        if (g_debug_sync) dbg_sync(__LINE__);
         CK(cudaStreamSynchronize(p->st));
-        cudaFree(dx);
-        cudaFree(dy);
+        dfree(dx);
+        dfree(dy);
     });
 }
 
@@ -2366,6 +2453,7 @@ int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out8) { 
         CK(cudaMemcpy(out8, p->ss_stats, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         if (reset) {
             CK(cudaMemsetAsync(p->ss_stats, 0, 16 * sizeof(unsigned long long), p->st));
+            if (g_debug_sync) dbg_sync(__LINE__);
             CK(cudaStreamSynchronize(p->st));
         }
     });
