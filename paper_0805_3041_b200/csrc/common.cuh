@@ -100,6 +100,11 @@ struct CoefField {
     }
 };
 
+// Coefficient index clamp for points a streaming kernel evaluates outside the
+// grid (halo columns/rows whose results are discarded): ROWX/FIELD tables are
+// only read in bounds; for interior points the clamp is the identity.
+__device__ __forceinline__ int cix(int v, int n) { return v < 0 ? 0 : (v >= n ? n - 1 : v); }
+
 // y = (A x)(i,j) in the reference's order c, w, e, s, n (stencil.cpp:133-137).
 template <class Coef>
 __device__ __forceinline__ double stencil_apply(const Coef& A, int i, int j, double xc, double xw,

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(TW) k_smooth(Grid fg, Coef A, Src src, OmegaSr
                     const int R = J - l - 1;
                     const double xl = t > 0 ? sh[pb][l][t - 1] : 0.0;
                     const double xr = t < TW - 1 ? sh[pb][l][t + 1] : 0.0;
-                    const double y = jacobi_point(A, i, R, win[l][1], xl, xr, win[l][0], win[l][2],
+                    const double y = jacobi_point(A, cix(i, fg.nx), cix(R, fg.ny), win[l][1], xl, xr, win[l][0], win[l][2],
                                                   gring[l], omega_damp);
                     nv = (col_in && R >= 0 && R < fg.ny) ? y : 0.0;
                 }
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
             xs[J & 1][t] = x0;
             double d = 0.0;
             if (col_in && R >= 0 && R < fg.ny) {
-                const double ax = stencil_apply(A, i, R, b, xl, xr, a, c);
+                const double ax = stencil_apply(A, cix(i, fg.nx), R, b, xl, xr, a, c);
                 d = neg ? ax - gR : gR - ax;  // smoother defect (Ax - g) or residual (g - Ax)
             }
             if (STORE_D && owner && R >= j0 && R < j1) dout[fg.at(i, R)] = d;
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(TW) k_omega_terms(Grid fg, Coef A, SrcProlong 
             const double xr = t < TW - 1 ? xs[(J - 1) & 1][t + 1] : 0.0;
             xs[J & 1][t] = cj;
             if (owner && R >= j0 && R < j1) {
-                const double ac = stencil_apply(A, i, R, b, xl, xr, a, c);
+                const double ac = stencil_apply(A, cix(i, fg.nx), R, b, xl, xr, a, c);
                 const long long k = (long long)R * fg.nx + i;
                 T0[k] = ac * b;
                 T1[k] = dR * b;

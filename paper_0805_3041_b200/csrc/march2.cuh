@@ -184,8 +184,10 @@ __global__ void __launch_bounds__(TW) k_smooth2(Grid fg, Coef A, Src src, OmegaS
                     const double xl = t > 0 ? sh[pb][l][t - 1].y : 0.0;
                     const double xr = t < TW - 1 ? sh[pb][l][t + 1].x : 0.0;
                     const double2 c = win[l][1], dn = win[l][0], up = win[l][2];
-                    const double y0 = jacobi_point(A, i, R, c.x, xl, c.y, dn.x, up.x, gring[l].x, omega_damp);
-                    const double y1 = jacobi_point(A, i + 1, R, c.y, c.x, xr, dn.y, up.y, gring[l].y, omega_damp);
+                    const int Rc = cix(R, fg.ny);
+                    const double y0 = jacobi_point(A, cix(i, fg.nx), Rc, c.x, xl, c.y, dn.x, up.x, gring[l].x, omega_damp);
+                    const double y1 =
+                        jacobi_point(A, cix(i + 1, fg.nx), Rc, c.y, c.x, xr, dn.y, up.y, gring[l].y, omega_damp);
                     const bool rin = R >= 0 && R < fg.ny;
                     nv = make_double2((rin && in0) ? y0 : 0.0, (rin && in1) ? y1 : 0.0);
                 }
@@ -363,8 +365,10 @@ __global__ void __launch_bounds__(TW) k_smooth3(Grid fg, Coef A, const double* _
                 const double xl = t > 0 ? S.sh[pb][l][t - 1].y : 0.0;
                 const double xr = t < TW - 1 ? S.sh[pb][l][t + 1].x : 0.0;
                 const double2 c = win[l][1], dn = win[l][0], upv = win[l][2];
-                const double y0 = jacobi_point(A, i, R, c.x, xl, c.y, dn.x, upv.x, gring[l].x, omega_damp);
-                const double y1 = jacobi_point(A, i + 1, R, c.y, c.x, xr, dn.y, upv.y, gring[l].y, omega_damp);
+                const int Rc = cix(R, fg.ny);
+                const double y0 = jacobi_point(A, cix(i, fg.nx), Rc, c.x, xl, c.y, dn.x, upv.x, gring[l].x, omega_damp);
+                const double y1 =
+                    jacobi_point(A, cix(i + 1, fg.nx), Rc, c.y, c.x, xr, dn.y, upv.y, gring[l].y, omega_damp);
                 const bool rin = R >= 0 && R < fg.ny;
                 nv = make_double2((rin && in0) ? y0 : 0.0, (rin && in1) ? y1 : 0.0);
             }

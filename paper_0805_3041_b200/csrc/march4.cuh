@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                 for (int k = 0; k < 4; ++k) {
                     const double xw = k == 0 ? xl : w[l][sc][k - 1];
                     const double xe = k == 3 ? xr : w[l][sc][k + 1];
-                    y[k] = jacobi_point(A, i + k, R, w[l][sc][k], xw, xe, w[l][sd][k], w[l][sn][k], gr[l][k],
+                    y[k] = jacobi_point(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe, w[l][sd][k],
+                                        w[l][sn][k], gr[l][k],
                                         omega_damp);
                 }
                 if (R < 0 || R >= ny) {
@@ -397,7 +398,8 @@ __global__ void __launch_bounds__(kS4W * 32, 4)
                 for (int k = 0; k < 4; ++k) {
                     const double xe_ = k == 3 ? xr : xw[sJ1][k + 1];
                     const double xwv = k == 0 ? xl : xw[sJ1][k - 1];
-                    const double ax = stencil_apply(A, i + k, R, xw[sJ1][k], xwv, xe_, xw[sJ2][k], xw[sJ][k]);
+                    const double ax =
+                        stencil_apply(A, cix(i + k, fg.nx), R, xw[sJ1][k], xwv, xe_, xw[sJ2][k], xw[sJ][k]);
                     d[k] = gv[k] - ax;
                 }
                 if (edge) {
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(kS4W * 32, 4)
                 const double b = cw[sJ1][k];
                 const double xwv = k == 0 ? xl : cw[sJ1][k - 1];
                 const double xev = k == 3 ? xr : cw[sJ1][k + 1];
-                const double ac = stencil_apply(A, i + k, R, b, xwv, xev, cw[sJ2][k], cw[sJ][k]);
+                const double ac = stencil_apply(A, cix(i + k, fg.nx), R, b, xwv, xev, cw[sJ2][k], cw[sJ][k]);
                 t0[k] = ac * b;
                 t1[k] = dv[k] * b;
                 if (cout_[k]) any |= (b * b) != 0.0;

@@ -34,7 +34,7 @@ constexpr int kSsEPT = 32;            // terms per thread
 constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk (large sums)
 constexpr int kSsEPTs = 8;            // terms per thread for small sums
 constexpr int kSsCs = kSsT * kSsEPTs; // terms per chunk (small sums)
-constexpr long long kSsSmallMax = 0;  // sums up to this length use small chunks (off: GMG_SS_SMALL_MAX)
+constexpr long long kSsSmallMax = 1ll << 20;  // sums up to this length walk in small chunks (GMG_SS_SMALL_MAX)
 constexpr uint32_t kRecOpen = 1u << 16;  // Rec.meta: the carried-in run is still to be prepended
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
