@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(256) k_ss_compact(SsPair sts, int nch) {
 // merging in order). CTA aggregates live in cincl[0, nb), inclusive prefixes in
 // cincl[nb, 2nb) (cincl is otherwise unused); flags in cflag.
 constexpr int kSsScanB = 256;
-__global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) {
+__device__ __forceinline__ void ss_scan2_body(const SsPair& sts, int nch) {
     __shared__ SegF sws[9];
     __shared__ SegF s_cin[kSsScanB];
     __shared__ int s_cnt[kSsScanB];
@@ -690,6 +690,7 @@ __global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) {
         }
     }
 }
+__global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) { ss_scan2_body(sts, nch); }
 
 // ---- chain --------------------------------------------------------------------
 // Both re-sum paths read terms through a register ring of kSsRing batches of 32
@@ -806,15 +807,13 @@ __device__ double warp_walk(const TG& tg, int s, double sv, long long k0, long l
 // grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays,
 // warps 1.. stage the next batch.
 template <class TG>
-__global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out,
-                                                 const double* __restrict__ start) {
-    extern __shared__ unsigned char smraw[];
+__device__ __forceinline__ void ss_chain_body(const TG& tg, long long n, const SsState& S, int s,
+                                              double* __restrict__ out, const double* __restrict__ start,
+                                              unsigned char* smraw) {
     gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
     __shared__ longlong2 cD[32];  // per record of the current group: signed run steps (parity 0, 1)
     __shared__ double2 cPB[32];   // break term (-0.0 if none), tie flag
     __shared__ double ltile[kSsLitTile];  // literal re-sum staging
-    const int s = blockIdx.x;
-    const SsState& S = sts.s[s];
     const int t = threadIdx.x;
     const int total = *S.total;
     const int nb = (total + kSsBatch - 1) / kSsBatch;
@@ -947,6 +946,35 @@ __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair st
             atomicAdd(S.stats + 7, (unsigned long long)((n + kSsC - 1) / kSsC));
         }
     }
+}
+
+// grid (NS); block kSsT; dynamic smem ss_chain_smem(). One CTA per sum.
+template <class TG>
+__global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out,
+                                                 const double* __restrict__ start) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    ss_chain_body(tg, n, sts.s[blockIdx.x], (int)blockIdx.x, out, start, smraw);
+}
+
+// k_ss_scan2 with the chain fused: the CTA that finishes its sum's compaction
+// last (completion counter, threadfence-reduction pattern) replays the records.
+// Saves a launch per sum; used when no other range has to chain in first.
+template <class TG>
+__global__ void __launch_bounds__(kSsScanB) k_ss_scan_chain(TG tg, long long n, SsPair sts, int nch,
+                                                           double* __restrict__ out,
+                                                           const double* __restrict__ start) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ int s_last;
+    const SsState& S = sts.s[blockIdx.y];
+    ss_scan2_body(sts, nch);
+    __threadfence();
+    __syncthreads();
+    const int nb = (nch + kSsScanB - 1) / kSsScanB;
+    if (threadIdx.x == 0) s_last = atomicAdd(S.flag, 1) == nb - 1;  // flag[0]: completion counter
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    ss_chain_body(tg, n, S, (int)blockIdx.y, out, start, smraw);
 }
 
 // Small sums (n <= kSsDirect): the reference's loop literally. The CTA stages

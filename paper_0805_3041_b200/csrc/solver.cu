@@ -362,6 +362,7 @@ void seqsum_attrs() {
         set_smem(k_ss_walk<TG, kSsEPT>, ss_walk_smem<kSsEPT>());
         set_smem(k_ss_walk<TG, kSsEPTs>, ss_walk_smem<kSsEPTs>());
         set_smem(k_ss_chain<TG>, ss_chain_smem());
+        set_smem(k_ss_scan_chain<TG>, ss_chain_smem());
         attr_done = true;
     }
 }
@@ -390,8 +391,11 @@ void preload_seqsum_kernels() {
 // the sum of the terms before it (earlier row slabs); pre0: an approximation of
 // the same, used only to seed the speculative walk. Split in two phases so
 // that row slabs can run their walks concurrently and chain in rank order.
+// fused_out != null: the chain runs inside the scan kernel (k_ss_scan_chain) and writes the
+// NS sums there, starting from fused_start (may be null).
 template <class TG>
-void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) {
+void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0, double* fused_out = nullptr,
+                 const double* fused_start = nullptr) {
     constexpr int NS = TG::NS;
     const bool small = n <= ss_small_max();
     const int cs = small ? kSsCs : kSsC;
@@ -406,7 +410,11 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0) 
         k_ss_walk<TG, kSsEPTs><<<dim3(nch, NS), kSsT, ss_walk_smem<kSsEPTs>(), p->st>>>(tg, n, nch, sp, pre0);
     else
         k_ss_walk<TG, kSsEPT><<<dim3(nch, NS), kSsT, ss_walk_smem<kSsEPT>(), p->st>>>(tg, n, nch, sp, pre0);
-    k_ss_scan2<<<dim3((nch + kSsScanB - 1) / kSsScanB, NS), kSsScanB, 0, p->st>>>(sp, nch);
+    const dim3 sg((nch + kSsScanB - 1) / kSsScanB, NS);
+    if (fused_out)
+        k_ss_scan_chain<TG><<<sg, kSsScanB, ss_chain_smem(), p->st>>>(tg, n, sp, nch, fused_out, fused_start);
+    else
+        k_ss_scan2<<<sg, kSsScanB, 0, p->st>>>(sp, nch);
     KCHECK();
 }
 
@@ -459,8 +467,17 @@ void seqsum(gmg_problem* p, const TG& tg, long long n, double* out, int mode, co
         seqsum_fast(p, tg, n, out, start);
         return;
     }
-    seqsum_walk(p, tg, n, pre0);
-    seqsum_chain(p, tg, n, out, start);
+    if (n <= kSsDirect) {  // the direct kernel (or the empty sum): no walk
+        seqsum_chain(p, tg, n, out, start);
+        return;
+    }
+    static const bool split = getenv("GMG_SPLIT_CHAIN") != nullptr;  // A/B: separate chain launch
+    if (split) {
+        seqsum_walk(p, tg, n, pre0);
+        seqsum_chain(p, tg, n, out, start);
+        return;
+    }
+    seqsum_walk(p, tg, n, pre0, out, start);
 }
 
 Prolong prolong_from(gmg_problem* p, int coarse_level, const double* uc) {
