@@ -373,7 +373,13 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     const int t = threadIdx.x;
     long long ph[7];
     ph[0] = clock64();
+#ifdef GMG_SS_TICKET
     if (t == 0) s_chunk = atomicAdd(S.ticket, 1);
+#else
+    // chunk = blockIdx.x: CTAs are dispatched in increasing linear block order, so every
+    // look-back predecessor is already resident (no ticket atomic on the critical path)
+    if (t == 0) s_chunk = blockIdx.x;
+#endif
     __syncthreads();
     const int c = s_chunk;
     constexpr int kC = kSsT * EPT;
@@ -638,7 +644,11 @@ __device__ __forceinline__ void ss_scan2_body(const SsPair& sts, int nch) {
     __shared__ int s_b;
     const SsState& S = sts.s[blockIdx.y];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#ifdef GMG_SS_TICKET
     if (t == 0) s_b = atomicAdd(S.ticket, 1) - nch;
+#else
+    if (t == 0) s_b = blockIdx.x;
+#endif
     __syncthreads();
     const int b = s_b, nb = (nch + kSsScanB - 1) / kSsScanB;
     const int c = b * kSsScanB + t;

@@ -31,7 +31,7 @@ from typing import List, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgmg_b200.so")
+LIB_PATH = os.environ.get("GMG_LIB_PATH") or os.path.join(_HERE, "libgmg_b200.so")  # override: A/B of alternative builds
 
 GMG_OK, GMG_ERR_LOGIC, GMG_ERR_INVALID, GMG_ERR_RUNTIME, GMG_DIVERGED, GMG_ERR_CUDA, \
     GMG_ERR_UNSUPPORTED = range(7)
