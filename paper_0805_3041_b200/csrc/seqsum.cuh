@@ -872,14 +872,23 @@ __device__ __forceinline__ void ss_chain_body(const TG& tg, long long n, const S
                 cPB[lane] = make_double2(brk ? r.pb : -0.0, __longlong_as_double(ties ? 1ll : 0ll));
                 __syncwarp();
                 double x = sv, before = sv;
+                if (!__any_sync(0xffffffffu, act && ties)) {
+                    // no tie in the group: one parity variant, the chain is integer add + fp64 add
+#pragma unroll 8
+                    for (int k = 0; k < gn; ++k) {
+                        if (lane == k) before = x;
+                        x = gmg_ss::bitsd(gmg_ss::dbits(x) + (uint64_t)cD[k].x) + cPB[k].x;
+                    }
+                } else {
 #pragma unroll 4
-                for (int k = 0; k < gn; ++k) {
-                    if (lane == k) before = x;
-                    const longlong2 dd = cD[k];
-                    const double2 pt = cPB[k];
-                    const uint64_t bits = gmg_ss::dbits(x);
-                    const long long D = (bits & (uint64_t)__double_as_longlong(pt.y)) ? dd.y : dd.x;
-                    x = gmg_ss::bitsd(bits + (uint64_t)D) + pt.x;
+                    for (int k = 0; k < gn; ++k) {
+                        if (lane == k) before = x;
+                        const longlong2 dd = cD[k];
+                        const double2 pt = cPB[k];
+                        const uint64_t bits = gmg_ss::dbits(x);
+                        const long long D = (bits & (uint64_t)__double_as_longlong(pt.y)) ? dd.y : dd.x;
+                        x = gmg_ss::bitsd(bits + (uint64_t)D) + pt.x;
+                    }
                 }
                 // (3) validation of record lane against `before`
                 bool ok = true;
