@@ -303,13 +303,18 @@ __global__ void k_omega_terms_field(Grid g, Coef A, const double* __restrict__ d
 // ---------------------------------------------------------------------------
 constexpr int kTW = 128;
 
-// Rows per CTA segment: 128 on large levels; on small levels short segments so
+// Rows per CTA segment: halved from 128 until the grid has >= 32*148 warp strips
+// (GMG_SEG_TARGET), i.e. about two full waves at 16 resident warps per SM; short segments so
 // the grid has enough CTAs and each marches few rows (the march is latency-bound
 // per row). Always even (the restriction pairs fine rows).
 int seg_rows(int nx, int ny) {
+    static const long long target = [] {
+        const char* e = getenv("GMG_SEG_TARGET");
+        return e ? atoll(e) : 32LL * 148;  // warps: ~2 full waves of the 16-warp/SM streaming kernels
+    }();
     const int strips = (nx + 123) / 124;
     int seg = 128;
-    while (seg > 8 && (long long)strips * ((ny + seg - 1) / seg) < 2 * 148) seg /= 2;
+    while (seg > 8 && (long long)strips * ((ny + seg - 1) / seg) < target) seg /= 2;
     return seg;
 }
 
