@@ -19,6 +19,20 @@
 
 namespace gmg_dev {
 
+// Programmatic dependent launch (kernels are launched with the PDL attribute,
+// solver.cu launch_k): every kernel first waits until the previous kernel in the
+// stream has completed and its writes are visible. The early trigger that would
+// let the next kernel's CTAs launch into this kernel's last wave is compiled out
+// by default (-DGMG_PDL_TRIGGER enables it): measured on C4 it costs 3% — the
+// waiting CTAs hold registers and shared memory the tail of this kernel could
+// use. Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef GMG_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 constexpr int kWarp = 32;
 
 // Rows [w0, w1) are the rows a kernel produces (the whole grid, or one rank's

@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
                                                            const double* __restrict__ x, double* __restrict__ xo,
                                                            double damp, double* __restrict__ gedge,
                                                            int* __restrict__ gprog) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     extern __shared__ double stg[];
     __shared__ double ring[kGsWarps][kGsRing];
     __shared__ volatile int prog[kGsWarps];  // columns of row 32w+31 available in ring[w]

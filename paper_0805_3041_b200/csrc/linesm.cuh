@@ -52,6 +52,8 @@ __device__ __forceinline__ double line_out(double z, const double* x, const doub
 template <int DIR, class Coef>
 __global__ void k_tri_factor(Grid g, Coef A, double om, double* __restrict__ sub, double* __restrict__ diag,
                              double* __restrict__ sup, int* __restrict__ status) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
     const int nl = DIR == 0 ? g.ny : g.nx, n = DIR == 0 ? g.nx : g.ny;
     if (line >= nl) return;
@@ -86,6 +88,8 @@ template <int DIR, int MODE>
 __global__ void __launch_bounds__(kLineT) k_line(Grid g, LineFactors f, const double* rhs, double* ybuf,
                                                  const double* __restrict__ x, const double* __restrict__ z1,
                                                  double* __restrict__ out, double damp) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int line = blockIdx.x * blockDim.x + threadIdx.x;
     const int nl = DIR == 0 ? g.ny : g.nx, n = DIR == 0 ? g.nx : g.ny;
     if (line >= nl) return;
@@ -172,6 +176,8 @@ __global__ void __launch_bounds__(32) k_gstri(Grid g, Coef A, double om, LineFac
                                               const double* __restrict__ z1, double* __restrict__ out,
                                               double* __restrict__ zline, double* __restrict__ ybuf,
                                               double damp) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int lane = threadIdx.x;
     const unsigned full = 0xffffffffu;
     const int nl = DIR == 0 ? g.ny : g.nx, n = DIR == 0 ? g.nx : g.ny;
@@ -265,6 +271,8 @@ __global__ void __launch_bounds__(32) k_gstri(Grid g, Coef A, double om, LineFac
 // Richardson step (smoother.cpp:284-285 with :389-399): x - damp*(rw*d).
 __global__ void k_rich_update(Grid g, const double* __restrict__ d, const double* __restrict__ x,
                               double* __restrict__ out, double rw, double damp) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
     if (i >= g.nx) return;
@@ -275,6 +283,8 @@ __global__ void k_rich_update(Grid g, const double* __restrict__ d, const double
 
 // power_apply_A's normalisation y_k / lambda (smoother.cpp:223).
 __global__ void k_div_scalar(Grid g, double* __restrict__ y, double lambda) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y;
     if (i >= g.nx) return;

@@ -176,6 +176,8 @@ template <int M, int TW, int PF, class Coef, class Src>
 __global__ void __launch_bounds__(TW) k_smooth(Grid fg, Coef A, Src src, OmegaSrc om,
                                                const double* __restrict__ g,
                                                double* __restrict__ out, double omega_damp, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     constexpr int OUTW = TW - 2 * M;
     constexpr int ML = M > 0 ? M : 1;
     __shared__ double sh[2][ML][TW];
@@ -263,6 +265,8 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
                                               double* __restrict__ dout, double* __restrict__ x0out,
                                               Grid cg, RestrictW rw, double* __restrict__ gc, int seg,
                                               int neg, OmegaSrc om) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const bool STORE_D = dout != nullptr, STORE_X0 = x0out != nullptr, RESTRICT = gc != nullptr;
     constexpr int OUTW = TW - 4;
     __shared__ double xs[2][TW];
@@ -350,6 +354,8 @@ template <int TW, int PF, class Coef>
 __global__ void __launch_bounds__(TW) k_omega_terms(Grid fg, Coef A, SrcProlong src,
                                                     const double* __restrict__ d, double* __restrict__ T0,
                                                     double* __restrict__ T1, int* __restrict__ nz, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     constexpr int OUTW = TW - 2;
     __shared__ double xs[2][TW];
     const int t = threadIdx.x;

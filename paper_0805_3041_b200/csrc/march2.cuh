@@ -116,6 +116,8 @@ struct Src2Correct {  // u + omega * P uc (axpy(wl, corr, u), cycle.cpp:93-96)
 template <int M, int TW, int PF, class Coef, class Src>
 __global__ void __launch_bounds__(TW) k_smooth2(Grid fg, Coef A, Src src, OmegaSrc om, const double* __restrict__ g,
                                                 double* __restrict__ out, double omega_damp, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     constexpr int H = (M + 1) & ~1;
     constexpr int OUTW = 2 * TW - 2 * H;
     constexpr int ML = M > 0 ? M : 1;
@@ -268,6 +270,8 @@ template <int M, int TW, int D, int SK, class Coef>
 __global__ void __launch_bounds__(TW) k_smooth3(Grid fg, Coef A, const double* __restrict__ u, Prolong P,
                                                 OmegaSrc om, const double* __restrict__ g,
                                                 double* __restrict__ out, double omega_damp, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     using SM = Smooth3Smem<M, TW, D, SK, Coef>;
     constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C;
     constexpr int H = (M + 1) & ~1;

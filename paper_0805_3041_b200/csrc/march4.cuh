@@ -40,6 +40,8 @@ template <int M, int SK, class Coef>
 __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
     k_smooth4(Grid fg, Coef A, const double* __restrict__ u, Prolong P, OmegaSrc om, const double* __restrict__ g,
               double* __restrict__ out, double omega_damp, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     using SM = Smooth4Smem<SK>;
     constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C;
     constexpr int D = SM::D;
@@ -278,6 +280,8 @@ __global__ void __launch_bounds__(kS4W * 32, 4)
     k_resid4(Grid fg, Coef A, const double* __restrict__ x, const double* __restrict__ e,
              const double* __restrict__ g, double* __restrict__ dout, double* __restrict__ x0out, Grid cg,
              RestrictW rw, double* __restrict__ gc, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     using SM = Resid4Smem<SUM>;
     constexpr int D = SM::D;
     constexpr int H = 2;
@@ -468,6 +472,8 @@ template <class Coef>
 __global__ void __launch_bounds__(kS4W * 32, 4)
     k_omega4(Grid fg, Coef A, Prolong P, const double* __restrict__ dd, double* __restrict__ T0,
              double* __restrict__ T1, int* __restrict__ nz, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     using SM = Omega4Smem;
     constexpr int D = SM::D;
     constexpr int H = 2;

@@ -361,6 +361,8 @@ __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 template <class TG, int EPT>
 __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
                                                        const double* __restrict__ pre0) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     extern __shared__ double tm[];
     __shared__ double swd[8];
     __shared__ SegF sws[9];
@@ -568,6 +570,8 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 // position); *total = records of the sum.
 constexpr int kSsScanT = 1024;
 __global__ void __launch_bounds__(kSsScanT) k_ss_scan(SsPair sts, int nch) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     __shared__ SegF sw[kSsScanT / 32 + 1];
     const SsState& S = sts.s[blockIdx.x];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -609,6 +613,8 @@ __global__ void __launch_bounds__(kSsScanT) k_ss_scan(SsPair sts, int nch) {
 // records to their place in the ordered list, prepending the carried-in run to
 // an open record (seg_merge is associative, so this equals merging in order).
 __global__ void __launch_bounds__(256) k_ss_compact(SsPair sts, int nch) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const SsState& S = sts.s[blockIdx.y];
     const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (c >= nch) return;
@@ -700,7 +706,9 @@ __device__ __forceinline__ void ss_scan2_body(const SsPair& sts, int nch) {
         }
     }
 }
-__global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) { ss_scan2_body(sts, nch); }
+__global__ void __launch_bounds__(kSsScanB) k_ss_scan2(SsPair sts, int nch) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger(); ss_scan2_body(sts, nch); }
 
 // ---- chain --------------------------------------------------------------------
 // Both re-sum paths read terms through a register ring of kSsRing batches of 32
@@ -971,6 +979,8 @@ __device__ __forceinline__ void ss_chain_body(const TG& tg, long long n, const S
 template <class TG>
 __global__ void __launch_bounds__(kSsT) k_ss_chain(TG tg, long long n, SsPair sts, double* __restrict__ out,
                                                  const double* __restrict__ start) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smraw[];
     ss_chain_body(tg, n, sts.s[blockIdx.x], (int)blockIdx.x, out, start, smraw);
 }
@@ -982,6 +992,8 @@ template <class TG>
 __global__ void __launch_bounds__(kSsScanB) k_ss_scan_chain(TG tg, long long n, SsPair sts, int nch,
                                                            double* __restrict__ out,
                                                            const double* __restrict__ start) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smraw[];
     __shared__ int s_last;
     const SsState& S = sts.s[blockIdx.y];
@@ -1004,6 +1016,8 @@ constexpr int kSsDirect = 4096;
 template <class TG>
 __global__ void __launch_bounds__(256) k_ss_direct(TG tg, int n, double* __restrict__ out,
                                                    const double* __restrict__ start) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     extern __shared__ double tv[];
     const int s = blockIdx.x;
     for (int k = threadIdx.x; k < n; k += blockDim.x) tv[k] = tg.term(s, k);
@@ -1026,6 +1040,8 @@ __global__ void __launch_bounds__(256) k_ss_direct(TG tg, int n, double* __restr
 // Fast mode: tree-order partial sums per chunk, then one CTA finishes.
 template <class TG>
 __global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double* __restrict__ csum, int nch) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     __shared__ double swd[8];
     const int s = blockIdx.y;
     const long long base = (long long)blockIdx.x * kSsC;

@@ -71,6 +71,26 @@ inline void dbg_sync(int line) {
         if (g_debug_sync) dbg_sync(__LINE__);           \
     } while (0)
 
+// Every kernel is launched with the programmatic-dependent-launch attribute (the
+// kernels start with pdl_wait()/pdl_trigger(), common.cuh): captured into the
+// cycle graph as programmatic edges, so each launch overlaps its predecessor's
+// tail. GMG_NO_PDL=1 launches plainly (A/B).
+static const bool g_pdl = getenv("GMG_NO_PDL") == nullptr;
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(std::forward<Args>(args))...));
+}
+
 template <class F>
 int guarded(F&& f) {
     try {
@@ -212,6 +232,8 @@ namespace {
 // ---------------------------------------------------------------------------
 __global__ void k_restrict_simple(Grid fg, const double* __restrict__ f, Grid cg, RestrictW rw,
                                   double* __restrict__ c) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int P = blockIdx.x * blockDim.x + threadIdx.x;
     const int Q = blockIdx.y * blockDim.y + threadIdx.y;
     if (P >= cg.nx || Q >= cg.ny) return;
@@ -221,6 +243,8 @@ __global__ void k_restrict_simple(Grid fg, const double* __restrict__ f, Grid cg
 }
 
 __global__ void k_prolong_simple(Prolong P, Grid fg, double* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     if (i >= fg.nx || j >= fg.ny) return;
@@ -229,6 +253,8 @@ __global__ void k_prolong_simple(Prolong P, Grid fg, double* __restrict__ out) {
 
 template <class Coef>
 __global__ void k_apply_simple(Grid g, Coef A, const double* __restrict__ x, double* __restrict__ y) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     if (i >= g.nx || j >= g.ny) return;
@@ -237,6 +263,8 @@ __global__ void k_apply_simple(Grid g, Coef A, const double* __restrict__ x, dou
 }
 
 __global__ void k_axpy_flat(long long n, double a, const double* __restrict__ x, double* __restrict__ y) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) y[k] = y[k] + a * x[k];
 }
@@ -246,6 +274,8 @@ __global__ void k_axpy_flat(long long n, double a, const double* __restrict__ x,
 __global__ void k_coarse_chol(const double* __restrict__ band, int n, int bw, Grid g,
                               const double* __restrict__ b, double* __restrict__ x,
                               double* __restrict__ xs) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int k = 0; k < n; ++k) {
         double acc = b[g.at(k % g.nx, k / g.nx)];
@@ -265,6 +295,8 @@ __global__ void k_coarse_chol(const double* __restrict__ band, int n, int bw, Gr
 // Fast (tree-order) reduction finisher: sums the chunk partials of S1.
 __global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, double* __restrict__ out,
                              const double* __restrict__ start) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     __shared__ double red[32];
     for (int s = 0; s < ns; ++s) {
         double a = 0.0;
@@ -286,6 +318,8 @@ __global__ void k_fast_final(const double* __restrict__ csum, int nch, int ns, d
 template <class Coef>
 __global__ void k_omega_terms_field(Grid g, Coef A, const double* __restrict__ d, const double* __restrict__ cr,
                                     double* __restrict__ T0, double* __restrict__ T1, int* __restrict__ nz) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     if (i >= g.nx || j >= g.ny) return;
@@ -412,14 +446,14 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0, 
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
     if (small)
-        k_ss_walk<TG, kSsEPTs><<<dim3(nch, NS), kSsT, ss_walk_smem<kSsEPTs>(), p->st>>>(tg, n, nch, sp, pre0);
+        launch_k(k_ss_walk<TG, kSsEPTs>, dim3(nch, NS), kSsT, ss_walk_smem<kSsEPTs>(), p->st, tg, n, nch, sp, pre0);
     else
-        k_ss_walk<TG, kSsEPT><<<dim3(nch, NS), kSsT, ss_walk_smem<kSsEPT>(), p->st>>>(tg, n, nch, sp, pre0);
+        launch_k(k_ss_walk<TG, kSsEPT>, dim3(nch, NS), kSsT, ss_walk_smem<kSsEPT>(), p->st, tg, n, nch, sp, pre0);
     const dim3 sg((nch + kSsScanB - 1) / kSsScanB, NS);
     if (fused_out)
-        k_ss_scan_chain<TG><<<sg, kSsScanB, ss_chain_smem(), p->st>>>(tg, n, sp, nch, fused_out, fused_start);
+        launch_k(k_ss_scan_chain<TG>, sg, kSsScanB, ss_chain_smem(), p->st, tg, n, sp, nch, fused_out, fused_start);
     else
-        k_ss_scan2<<<sg, kSsScanB, 0, p->st>>>(sp, nch);
+        launch_k(k_ss_scan2, sg, kSsScanB, 0, p->st, sp, nch);
     KCHECK();
 }
 
@@ -435,13 +469,13 @@ void seqsum_chain(gmg_problem* p, const TG& tg, long long n, double* out, const 
         return;
     }
     if (n <= kSsDirect) {
-        k_ss_direct<TG><<<NS, 256, n * sizeof(double), p->st>>>(tg, (int)n, out, start);
+        launch_k(k_ss_direct<TG>, NS, 256, n * sizeof(double), p->st, tg, (int)n, out, start);
         KCHECK();
         return;
     }
     const int nch = (int)((n + kSsC - 1) / kSsC);
     const SsPair sp = ss_state(p, nch);
-    k_ss_chain<TG><<<NS, kSsT, ss_chain_smem(), p->st>>>(tg, n, sp, out, start);
+    launch_k(k_ss_chain<TG>, NS, kSsT, ss_chain_smem(), p->st, tg, n, sp, out, start);
     KCHECK();
 }
 
@@ -460,8 +494,8 @@ void seqsum_fast(gmg_problem* p, const TG& tg, long long n, double* out, const d
             if (g_debug_sync) dbg_sync(__LINE__);
         return;
     }
-    k_ss_partial<TG><<<dim3(nch, NS), kSsT, 0, p->st>>>(tg, n, p->csum, nch);
-    k_fast_final<<<1, 1024, 0, p->st>>>(p->csum, nch, NS, out, start);
+    launch_k(k_ss_partial<TG>, dim3(nch, NS), kSsT, 0, p->st, tg, n, p->csum, nch);
+    launch_k(k_fast_final, 1, 1024, 0, p->st, p->csum, nch, NS, out, start);
     KCHECK();
 }
 
@@ -506,7 +540,7 @@ void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.rows() + seg - 1) / seg);
-    k_smooth<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
+    launch_k(k_smooth<M, kTW, PF, Coef, Src>, grid, kTW, 0, p->st, L.grid(), A, src, om, g, out, wd, seg);
     KCHECK();
 }
 
@@ -518,7 +552,7 @@ void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& sr
     constexpr int PF = sizeof(typename Src::Raw) > 32 ? 2 : 3;
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
-    k_smooth2<M, kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, om, g, out, wd, seg);
+    launch_k(k_smooth2<M, kTW, PF, Coef, Src>, grid, kTW, 0, p->st, L.grid(), A, src, om, g, out, wd, seg);
     KCHECK();
 }
 
@@ -538,7 +572,7 @@ void launch_smooth3_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
-    k_smooth3<M, kTW, D, SK, Coef><<<grid, kTW, sizeof(SM), p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
+    launch_k(k_smooth3<M, kTW, D, SK, Coef>, grid, kTW, sizeof(SM), p->st, L.grid(), A, u, P, om, g, out, wd, seg);
     KCHECK();
 }
 
@@ -558,7 +592,7 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     const int seg = seg_rows(L.nx, L.rows());
     const int strips = (L.nx + OW - 1) / OW;
     dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
-    k_smooth4<M, SK, Coef><<<grid, kS4W * 32, smem, p->st>>>(L.grid(), A, u, P, om, g, out, wd, seg);
+    launch_k(k_smooth4<M, SK, Coef>, grid, kS4W * 32, smem, p->st, L.grid(), A, u, P, om, g, out, wd, seg);
     KCHECK();
 }
 
@@ -687,7 +721,7 @@ void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src,
         rw = C.rw;
     }
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
-    k_resid<kTW, PF, Coef, Src><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg, neg,
+    launch_k(k_resid<kTW, PF, Coef, Src>, grid, kTW, 0, p->st, L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg, neg,
                                                           om);
     KCHECK();
 }
@@ -711,7 +745,7 @@ void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* 
     const int seg = seg_rows(L.nx, L.rows());
     const int strips = (L.nx + 123) / 124;
     dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
-    k_resid4<SUM, Coef><<<grid, kS4W * 32, smem, p->st>>>(L.grid(), A, u, e, g, dout, x0out, cg, rw, gc, seg);
+    launch_k(k_resid4<SUM, Coef>, grid, kS4W * 32, smem, p->st, L.grid(), A, u, e, g, dout, x0out, cg, rw, gc, seg);
     KCHECK();
 }
 
@@ -775,7 +809,7 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
         set_smem(k_gs_wave<Pol>, gs_smem());
         attr = true;
     }
-    k_gs_wave<Pol><<<blocks, kGsWarps * 32, gs_smem(), p->st>>>(L.grid(), pol, d, x, xo, damp, p->gs_edge,
+    launch_k(k_gs_wave<Pol>, blocks, kGsWarps * 32, gs_smem(), p->st, L.grid(), pol, d, x, xo, damp, p->gs_edge,
                                                                  p->gs_prog);
     KCHECK();
 }
@@ -800,7 +834,7 @@ template <int DIR, int MODE>
 void launch_line(gmg_problem* p, const Lev& L, const LineFactors& f, const double* rhs, double* ybuf,
                  const double* x, const double* z1, double* out, double damp) {
     const int nl = DIR == 0 ? L.ny : L.nx;
-    k_line<DIR, MODE><<<(nl + kLineT - 1) / kLineT, kLineT, 0, p->st>>>(L.grid(), f, rhs, ybuf, x, z1, out, damp);
+    launch_k(k_line<DIR, MODE>, (nl + kLineT - 1) / kLineT, kLineT, 0, p->st, L.grid(), f, rhs, ybuf, x, z1, out, damp);
     KCHECK();
 }
 
@@ -810,7 +844,7 @@ void launch_gstri(gmg_problem* p, const Lev& L, double om, const LineFactors& f,
     const int nmax = std::max(p->lev(p->L).nx, p->lev(p->L).ny);
     with_coef(L, [&](const auto& A) {
         using C = std::decay_t<decltype(A)>;
-        k_gstri<DIR, MODE, C><<<1, 32, 0, p->st>>>(L.grid(), A, om, f, rhs, x, z1, out, p->linebuf,
+        launch_k(k_gstri<DIR, MODE, C>, 1, 32, 0, p->st, L.grid(), A, om, f, rhs, x, z1, out, p->linebuf,
                                                    p->linebuf + nmax, damp);
     });
     KCHECK();
@@ -829,7 +863,7 @@ void pc_apply(gmg_problem* p, const Lev& L, const gmg_cycle_desc& sp, const SmLe
             return;
         case GMG_SMOOTHER_RICHARDSON: {
             dim3 gr((L.nx + 127) / 128, L.ny);
-            k_rich_update<<<gr, 128, 0, p->st>>>(L.grid(), d, x, out, m->rich, damp);
+            launch_k(k_rich_update, gr, 128, 0, p->st, L.grid(), d, x, out, m->rich, damp);
             KCHECK();
             return;
         }
@@ -913,13 +947,13 @@ void launch_restrict(gmg_problem* p, int fine_level, const double* f, double* c)
     const Lev& F = p->lev(fine_level);
     const Lev& C = p->lev(fine_level - 1);
     dim3 b(32, 8), gr((C.nx + 31) / 32, (C.ny + 7) / 8);
-    k_restrict_simple<<<gr, b, 0, p->st>>>(F.grid(), f, C.grid(), C.rw, c);
+    launch_k(k_restrict_simple, gr, b, 0, p->st, F.grid(), f, C.grid(), C.rw, c);
     KCHECK();
 }
 
 void launch_coarse(gmg_problem* p, const double* g, double* x) {
     const Lev& L = p->lev(1);
-    k_coarse_chol<<<1, 32, 0, p->st>>>(p->band, p->cn, p->cbw, L.grid(), g, x, p->cscr);
+    launch_k(k_coarse_chol, 1, 32, 0, p->st, p->band, p->cn, p->cbw, L.grid(), g, x, p->cscr);
     KCHECK();
 }
 
@@ -938,7 +972,7 @@ void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc,
     double* T1 = p->T + p->lev(p->L).n();
     with_coef(L, [&](const auto& A) {
         using C = std::decay_t<decltype(A)>;
-        k_omega_terms<kTW, 2, C><<<grid, kTW, 0, p->st>>>(L.grid(), A, src, d, T0, T1, p->nz, seg);
+        launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, p->st, L.grid(), A, src, d, T0, T1, p->nz, seg);
     });
     KCHECK();
     seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, mode);
@@ -1064,13 +1098,17 @@ void threshold_rows(const DistCtx& D, int l, std::vector<int>& a, std::vector<in
     }
 }
 
-__global__ void k_nz_to_d(const int* __restrict__ nz, double* __restrict__ out) { out[0] = nz[0] ? 1.0 : 0.0; }
+__global__ void k_nz_to_d(const int* __restrict__ nz, double* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger(); out[0] = nz[0] ? 1.0 : 0.0; }
 
 // From the gathered per-rank approximate totals g[r*8 + k] (k < NS; k == NS:
 // nz flag): pre[k] = sum over ranks below `rank` (seeds the walk), nz = OR,
 // and for the fast mode the rank-ordered total.
 __global__ void k_dist_prefix(const double* __restrict__ g, int rank, int world, int ns, int with_nz,
                               double* __restrict__ pre, int* __restrict__ nz, double* __restrict__ total) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     if (threadIdx.x != 0) return;
     for (int k = 0; k < ns; ++k) {
         double a = 0.0, t = 0.0;
@@ -1109,7 +1147,7 @@ void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int o
     for (auto* q : S) {
         auto tn = make(q);
         seqsum_fast(q, tn.first, tn.second, q->dscr, nullptr);
-        if (with_nz) k_nz_to_d<<<1, 1, 0, st>>>(q->nz, q->dscr + NS);
+        if (with_nz) launch_k(k_nz_to_d, 1, 1, 0, st, q->nz, q->dscr + NS);
     }
     KCHECK();
     if (D->local) {
@@ -1121,7 +1159,7 @@ void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int o
         NC(nccl().allGather(S[0]->dscr, S[0]->dscr + 32, 8, kNcclFloat64, D->comm, st));
     }
     for (auto* q : S)
-        k_dist_prefix<<<1, 32, 0, st>>>(q->dscr + 32, q->rank, D->world, NS, with_nz ? 1 : 0, q->dscr + 8, q->nz,
+        launch_k(k_dist_prefix, 1, 32, 0, st, q->dscr + 32, q->rank, D->world, NS, with_nz ? 1 : 0, q->dscr + 8, q->nz,
                                         mode == GMG_REDUCE_FAST ? q->sums + out_off : nullptr);
     KCHECK();
     if (mode == GMG_REDUCE_FAST) return;
@@ -1280,7 +1318,7 @@ struct Driver {
             set_smem(k_vsmall, kVSmemMax);
             attr = true;
         }
-        k_vsmall<<<1, kVThreads, vsmall_smem(l), q->st>>>(V);
+        launch_k(k_vsmall, 1, kVThreads, vsmall_smem(l), q->st, V);
         KCHECK();
     }
 
@@ -1351,10 +1389,10 @@ struct Driver {
                     }
                     const int strips = (L.nx + 123) / 124;
                     dim3 g4((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
-                    k_omega4<C><<<g4, kS4W * 32, omega4_smem(), q->st>>>(L.grid(), A, src.P, L.buf[DD], T0, T1,
+                    launch_k(k_omega4<C>, g4, kS4W * 32, omega4_smem(), q->st, L.grid(), A, src.P, L.buf[DD], T0, T1,
                                                                           q->nz, seg);
                 } else {
-                    k_omega_terms<kTW, 2, C><<<grid, kTW, 0, q->st>>>(L.grid(), A, src, L.buf[DD], T0, T1, q->nz,
+                    launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, q->st, L.grid(), A, src, L.buf[DD], T0, T1, q->nz,
                                                                        seg);
                 }
             });
@@ -1603,13 +1641,13 @@ double richardson_omega(gmg_problem* p, Lev& L, double omega) {
     for (int t = 0; t < 20; ++t) {
         with_coef(L, [&](const auto& A) {
             dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
-            k_apply_simple<<<gr, b, 0, p->st>>>(L.grid(), A, xa, ya);
+            launch_k(k_apply_simple<std::decay_t<decltype(A)>>, gr, b, 0, p->st, L.grid(), A, xa, ya);
         });
         KCHECK();
         norm_sum(p, L, ya, p->sums + 3, GMG_REDUCE_EXACT);
         lambda = std::sqrt(fetch_scalar(p, p->sums + 3));
         if (lambda == 0.0) break;
-        k_div_scalar<<<dim3((L.nx + 127) / 128, L.ny), 128, 0, p->st>>>(L.grid(), ya, lambda);
+        launch_k(k_div_scalar, dim3((L.nx + 127) / 128, L.ny), 128, 0, p->st, L.grid(), ya, lambda);
         KCHECK();
         std::swap(xa, ya);
     }
@@ -1672,13 +1710,13 @@ const SmSetup* ensure_smoother(gmg_problem* p, int kind, double omega) {
                 with_coef(L, [&](const auto& A) {
                     if (fx) {
                         m.fx = LineFactors{base, base + L.elems, base + 2 * L.elems};
-                        k_tri_factor<0><<<(L.ny + 127) / 128, 128, 0, p->st>>>(
+                        launch_k(k_tri_factor<0, std::decay_t<decltype(A)>>, (L.ny + 127) / 128, 128, 0, p->st, 
                             L.grid(), A, omega, base, base + L.elems, base + 2 * L.elems, p->status);
                         base += 3 * L.elems;
                     }
                     if (fy) {
                         m.fy = LineFactors{base, base + L.elems, base + 2 * L.elems};
-                        k_tri_factor<1><<<(L.nx + 127) / 128, 128, 0, p->st>>>(
+                        launch_k(k_tri_factor<1, std::decay_t<decltype(A)>>, (L.nx + 127) / 128, 128, 0, p->st, 
                             L.grid(), A, omega, base, base + L.elems, base + 2 * L.elems, p->status);
                     }
                 });
@@ -2225,7 +2263,7 @@ int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y) {
         upload(p, L, L.buf[U0], x, cudaMemcpyHostToDevice);
         with_coef(L, [&](const auto& A) {
             dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
-            k_apply_simple<<<gr, b, 0, p->st>>>(L.grid(), A, L.buf[U0], L.buf[U1]);
+            launch_k(k_apply_simple<std::decay_t<decltype(A)>>, gr, b, 0, p->st, L.grid(), A, L.buf[U0], L.buf[U1]);
         });
         KCHECK();
         download(p, L, y, L.buf[U1], cudaMemcpyDeviceToHost);
@@ -2304,7 +2342,7 @@ int gmg_dev_prolongation(gmg_problem* p, int coarse_level, const double* coarse,
         Lev& F = p->lev(coarse_level + 1);
         upload(p, C, C.buf[U0], coarse, cudaMemcpyHostToDevice);
         dim3 b(32, 8), gr((F.nx + 31) / 32, (F.ny + 7) / 8);
-        k_prolong_simple<<<gr, b, 0, p->st>>>(prolong_from(p, coarse_level, C.buf[U0]), F.grid(), F.buf[U1]);
+        launch_k(k_prolong_simple, gr, b, 0, p->st, prolong_from(p, coarse_level, C.buf[U0]), F.grid(), F.buf[U1]);
         KCHECK();
         download(p, F, fine, F.buf[U1], cudaMemcpyDeviceToHost);
         CK(cudaStreamSynchronize(p->st));
@@ -2326,7 +2364,7 @@ int gmg_dev_adaptive_omega(gmg_problem* p, int level, const double* d, const dou
         double* T1 = p->T + p->lev(p->L).n();
         with_coef(L, [&](const auto& A) {
             dim3 b(32, 8), gr((L.nx + 31) / 32, (L.ny + 7) / 8);
-            k_omega_terms_field<<<gr, b, 0, p->st>>>(L.grid(), A, L.buf[DD], L.buf[U0], T0, T1, p->nz);
+            launch_k(k_omega_terms_field<std::decay_t<decltype(A)>>, gr, b, 0, p->st, L.grid(), A, L.buf[DD], L.buf[U0], T0, T1, p->nz);
         });
         KCHECK();
         seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, GMG_REDUCE_EXACT);
@@ -2418,7 +2456,7 @@ int gmg_dev_axpy(gmg_problem* p, long long n, double alpha, const double* x, dou
         if (g_debug_sync) dbg_sync(__LINE__);
         CK(cudaMemcpyAsync(dy, y, n * sizeof(double), cudaMemcpyHostToDevice, p->st));
         if (g_debug_sync) dbg_sync(__LINE__);
-        k_axpy_flat<<<(unsigned)((n + 255) / 256), 256, 0, p->st>>>(n, alpha, dx, dy);
+        launch_k(k_axpy_flat, (unsigned)((n + 255) / 256), 256, 0, p->st, n, alpha, dx, dy);
         KCHECK();
         CK(cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, p->st));
         if (g_debug_sync) dbg_sync(__LINE__);

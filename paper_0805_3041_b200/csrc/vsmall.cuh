@@ -81,6 +81,8 @@ __device__ __forceinline__ double prolong_dense(const double* tx, const double* 
 }
 
 __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
     extern __shared__ double vs[];
     const int t = threadIdx.x;
     double* T = vs + P.toff;                      // smoothing ping-pong / correction
