@@ -1,24 +1,28 @@
 // Exact-order (bit-identical to a left-to-right loop) fp64 summation on the GPU.
-// Algorithm and invariants: seqsum_core.h. Two launches per call (+1 memset):
+// Algorithm and invariants: seqsum_core.h. Two launches per sum (+1 memset):
 //
-//   k_ss_walk  : one CTA per chunk of C = 8192 terms, chunks taken from an
-//                atomic ticket so every predecessor is already running.
-//                (1) load the chunk's terms; (2) publish its approximate sum and
-//                get the approximate prefix of all earlier chunks by decoupled
-//                look-back: the speculated running sum at the chunk start;
-//                (3) each thread walks its 32 consecutive terms from its
-//                speculated state, splitting them into in-binade integer
-//                segments and break elements; (4) a block segmented scan merges
-//                segments across threads; (5) a second decoupled look-back — a
-//                segmented scan over chunks — carries the run since the last
-//                break into the chunk and gives its record offset. Chunks without
-//                a break emit nothing; each break emits one record (the merged
-//                run before it + the break value), stored compactly in order.
-//   k_ss_chain : one CTA per sum replays the records from the exact state 0.0
-//                (warps 1.. stage batches into shared memory): validate the run
-//                and apply it as one integer add, then one real IEEE add for the
-//                break. A run that fails validation (wrong speculation) is
-//                re-summed literally over its own element range.
+//   k_ss_walk       : one CTA per chunk of 256*EPT terms (EPT = 32; 8 for sums of
+//                     <= 2^20 terms), chunk = blockIdx.x (in-order dispatch, so every
+//                     look-back predecessor is resident). (1) load the chunk's terms
+//                     (striped, coalesced) into shared memory; (2) publish its
+//                     approximate sum and get the approximate prefix of all earlier
+//                     chunks by a decoupled look-back on 16-byte value+status words:
+//                     the speculated running sum at the chunk start; (3) each thread
+//                     walks its EPT consecutive terms from its speculated state,
+//                     splitting them into in-binade integer segments and break
+//                     elements; (4) uniform chunks (every thread one segment in the
+//                     same binade) merge by an int64 scan, others by a block
+//                     segmented scan; each break emits one record (the merged run
+//                     before it + the break value) into the chunk's record slots.
+//   k_ss_scan_chain : a thread per chunk: segmented scan of the chunk aggregates with
+//                     a look-back over CTA aggregates (the run carried into each
+//                     chunk, its first record's position), record compaction; then
+//                     the CTA that finishes last replays the records from the exact
+//                     state 0.0: validate the run and apply it as one integer add,
+//                     then one real IEEE add for the break. A run that fails
+//                     validation (wrong speculation) is re-summed literally over its
+//                     own element range. (k_ss_scan2 + k_ss_chain when row slabs chain
+//                     across ranks.)
 //
 // Term generators: `double term(int s, long long k)` returns term k (in the
 // reference's k = j*nx + i order) of sum s.
@@ -52,7 +56,7 @@ struct SsState {
     unsigned char* cagg;   // [nch] ChunkAgg
     unsigned char* cincl;  // [nch] ChunkAgg
     gmg_ss::Rec* recs;   // [nch * kSsRMax] per-chunk record slots written by the walk
-    gmg_ss::Rec* recs2;  // compacted records in order (k_ss_compact), read by the chain
+    gmg_ss::Rec* recs2;  // compacted records in order (k_ss_scan2), read by the chain
     unsigned long long* stats;  // [16] calls, records, chain cycles, re-walk cycles, break adds, re-walks,
                                 //      re-walked terms, chunks; walk phase cycles [8..13]
 };
@@ -515,10 +519,10 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     const int R = tot.cnt + (close ? 1 : 0);
     const bool literal = R > kSsRMax;
 
-    // (5) the chunk's aggregate for k_ss_scan (the run it carries on, the
+    // (5) the chunk's aggregate for k_ss_scan2 (the run it carries on, the
     //     records it stores). No look-back: the cross-chunk segmented scan runs
     //     as one small kernel after all walks, and the chunk's first record is
-    //     stored "open" (kRecOpen) for k_ss_compact to prepend the run carried in.
+    //     stored "open" (kRecOpen) for k_ss_scan2 to prepend the run carried in.
     SegF mine = tot;
     mine.cnt = literal ? 1 : R;
     if (literal || close) {
@@ -565,75 +569,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 }
 
 // ---- cross-chunk scan and record compaction --------------------------------
-// grid (NS); 1024 threads. Exclusive ordered segmented scan of the chunk
-// aggregates: cincl[c] = the run carried into chunk c (cnt = its first record's
-// position); *total = records of the sum.
-constexpr int kSsScanT = 1024;
-__global__ void __launch_bounds__(kSsScanT) k_ss_scan(SsPair sts, int nch) {
-    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
-    pdl_trigger();
-    __shared__ SegF sw[kSsScanT / 32 + 1];
-    const SsState& S = sts.s[blockIdx.x];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int nt = blockDim.x, nw = nt >> 5;
-    const int per = (nch + nt - 1) / nt;
-    const int c0 = min(t * per, nch), c1 = min(c0 + per, nch);
-    SegF a = segf_id();
-    for (int c = c0; c < c1; ++c) a = segf_combine(a, agg_load(S.cagg, c));
-    // block exclusive scan of the thread aggregates
-    SegF inc = a;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const SegF y = segf_shfl(inc, 0, true, o);
-        if (lane >= o) inc = segf_combine(y, inc);
-    }
-    const SegF ex_w = segf_shfl(inc, 0, true, 1);
-    if (lane == 31) sw[w] = inc;
-    __syncthreads();
-    if (t == 0) {  // exclusive bases of the warp totals, block total in sw[nw]
-        SegF acc = segf_id();
-        for (int q = 0; q < nw; ++q) {
-            const SegF v = sw[q];
-            sw[q] = acc;
-            acc = segf_combine(acc, v);
-        }
-        sw[nw] = acc;
-    }
-    __syncthreads();
-    const SegF base = sw[w], tot = sw[nw];
-    SegF ex = lane == 0 ? base : segf_combine(base, ex_w);
-    for (int c = c0; c < c1; ++c) {
-        agg_store(S.cincl, c, ex);
-        ex = segf_combine(ex, agg_load(S.cagg, c));
-    }
-    if (t == 0) *S.total = tot.cnt;
-}
-
-// grid (ceil(nch/8), NS); 256 threads, a warp per chunk: copies the chunk's
-// records to their place in the ordered list, prepending the carried-in run to
-// an open record (seg_merge is associative, so this equals merging in order).
-__global__ void __launch_bounds__(256) k_ss_compact(SsPair sts, int nch) {
-    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
-    pdl_trigger();
-    const SsState& S = sts.s[blockIdx.y];
-    const int c = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (c >= nch) return;
-    const int cnt = __ldcg(&reinterpret_cast<const ChunkAgg*>(S.cagg)[c].cnt);
-    if (cnt == 0) return;
-    const SegF cin = agg_load(S.cincl, c);
-    const gmg_ss::Rec* src = S.recs + (long long)c * kSsRMax;
-    gmg_ss::Rec* dst = S.recs2 + cin.cnt;
-    for (int j = lane; j < cnt; j += 32) {
-        gmg_ss::Rec r = src[j];
-        if (r.meta & kRecOpen) {
-            const bool brk = (r.meta >> 12) & 1u;
-            r = gmg_ss::rec_make(gmg_ss::seg_merge(cin.g, gmg_ss::rec_seg(r)), brk, r.pb, r.kb);
-        }
-        dst[j] = r;
-    }
-}
-
-// Single-pass replacement for k_ss_scan + k_ss_compact. grid (ceil(nch/256), NS);
+// Cross-chunk segmented scan + record compaction, single pass. grid (ceil(nch/256), NS);
 // 256 threads, a thread per chunk. Block exclusive segmented scan of the chunk
 // aggregates, then a decoupled look-back over the CTA aggregates (CTA order
 // from the ticket the walk left at nch, so every predecessor is running),
