@@ -346,9 +346,16 @@ int seg_rows(int nx, int ny) {
         const char* e = getenv("GMG_SEG_TARGET");
         return e ? atoll(e) : 32LL * 148;  // warps: ~2 full waves of the 16-warp/SM streaming kernels
     }();
+    static const int seg_min_big = [] {
+        const char* e = getenv("GMG_SEG_MIN");
+        return e ? atoi(e) : 8;
+    }();
     const int strips = (nx + 123) / 124;
+    // large levels (the warp-strip kernels): segments no shorter than seg_min_big rows, so the
+    // 2M-row vertical halo of a fused smoothing launch stays a small share of the march
+    const int smin = nx >= 255 ? seg_min_big : 8;
     int seg = 128;
-    while (seg > 8 && (long long)strips * ((ny + seg - 1) / seg) < target) seg /= 2;
+    while (seg > smin && (long long)strips * ((ny + seg - 1) / seg) < target) seg /= 2;
     return seg;
 }
 
