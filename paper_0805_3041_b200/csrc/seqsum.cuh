@@ -33,17 +33,19 @@
 
 namespace gmg_dev {
 
-constexpr int kSsT = 256;             // threads per chunk
+constexpr int kSsT = 256;             // threads of the chain / partial-sum kernels
+constexpr int kSsWT = 128;            // threads per chunk in the walk (6 CTAs per SM)
 constexpr int kSsEPT = 32;            // terms per thread
-constexpr int kSsC = kSsT * kSsEPT;   // terms per chunk (large sums)
+constexpr int kSsC = kSsWT * kSsEPT;  // terms per chunk (large sums)
+constexpr int kSsPC = kSsT * kSsEPT;  // terms per CTA of the fast-mode partial sums
 constexpr int kSsEPTs = 8;            // terms per thread for small sums
-constexpr int kSsCs = kSsT * kSsEPTs; // terms per chunk (small sums)
+constexpr int kSsCs = kSsWT * kSsEPTs; // terms per chunk (small sums)
 constexpr long long kSsSmallMax = 1ll << 20;  // sums up to this length walk in small chunks (GMG_SS_SMALL_MAX)
 constexpr uint32_t kRecOpen = 1u << 16;  // Rec.meta: the carried-in run is still to be prepended
 constexpr int kSsBatch = 1024;        // records staged per chain batch
 constexpr int kSsMaxSums = 2;
-constexpr int kSsRMax = 1024;          // records a chunk may store; more -> exact re-walk
-constexpr int kSsRunCap = 16;         // a merged run never spans more than this many chunks
+constexpr int kSsRMax = 512;           // records a chunk may store; more -> exact re-walk
+constexpr int kSsRunCap = 32;         // a merged run never spans more than this many chunks
 
 // Per-sum look-back state (flags, ticket and total zeroed before each walk).
 struct SsState {
@@ -259,8 +261,9 @@ __device__ __forceinline__ double block_sum_d(double x, double* sw /* [8] */) {
     return t;
 }
 
-// Block exclusive sum (256 threads) and the block total, one barrier pair.
-__device__ __forceinline__ double block_excl_sum_tot_d(double x, double* sw /* [8] */, double* total) {
+// Block exclusive sum (NW warps) and the block total, one barrier pair.
+template <int NW>
+__device__ __forceinline__ double block_excl_sum_tot_d(double x, double* sw /* [NW] */, double* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double inc = x;
 #pragma unroll
@@ -272,7 +275,7 @@ __device__ __forceinline__ double block_excl_sum_tot_d(double x, double* sw /* [
     __syncthreads();
     double base = 0.0, t = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NW; ++q) {
         if (q == w) base = t;
         t += sw[q];
     }
@@ -284,7 +287,8 @@ __device__ __forceinline__ double block_excl_sum_tot_d(double x, double* sw /* [
 // One segment per thread, all in the same binade and sign (uniform chunk):
 // the merged segment's total (returned) and its prefix extremes. P, mn, mx are
 // the thread's exact integer total and prefix extremes as doubles.
-__device__ __forceinline__ long long block_seg_i64(double Pd, double mnd, double mxd, long long (*sw)[8],
+template <int NW>
+__device__ __forceinline__ long long block_seg_i64(double Pd, double mnd, double mxd, long long (*sw)[NW],
                                                    long long* lo, long long* hi) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long P = (long long)Pd;
@@ -298,7 +302,7 @@ __device__ __forceinline__ long long block_seg_i64(double Pd, double mnd, double
     __syncthreads();
     long long base = 0, t = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NW; ++q) {
         if (q == w) base = t;
         t += sw[0][q];
     }
@@ -317,7 +321,7 @@ __device__ __forceinline__ long long block_seg_i64(double Pd, double mnd, double
     a = sw[1][0];
     b = sw[2][0];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) {
+    for (int q = 1; q < NW; ++q) {
         a = min(a, sw[1][q]);
         b = max(b, sw[2][q]);
     }
@@ -326,8 +330,9 @@ __device__ __forceinline__ long long block_seg_i64(double Pd, double mnd, double
     return t;
 }
 
-// Block exclusive segmented scan (256 threads); returns the block inclusive total too.
-__device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [9] */, SegF* total) {
+// Block exclusive segmented scan (NW warps); returns the block inclusive total too.
+template <int NW>
+__device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [NW + 1] */, SegF* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     SegF inc = x;
 #pragma unroll
@@ -338,20 +343,20 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [9
     const SegF ex = segf_shfl(inc, 0, true, 1);
     if (lane == 31) sw[w] = inc;
     __syncthreads();
-    // one thread turns the 8 warp totals into exclusive bases (in place, the
-    // block total in sw[8]); every thread then reads its warp's base
+    // one thread turns the NW warp totals into exclusive bases (in place, the
+    // block total in sw[NW]); every thread then reads its warp's base
     if (threadIdx.x == 0) {
         SegF acc = segf_id();
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NW; ++q) {
             const SegF v = sw[q];
             sw[q] = acc;
             acc = segf_combine(acc, v);
         }
-        sw[8] = acc;
+        sw[NW] = acc;
     }
     __syncthreads();
     const SegF base = sw[w];
-    *total = sw[8];
+    *total = sw[NW];
     __syncthreads();
     if (lane == 0) return base;
     return segf_combine(base, ex);
@@ -360,19 +365,20 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [9
 __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 
 // ---- walk ---------------------------------------------------------------------
-// grid (nch, NS); block kSsT; dynamic smem (C + C/32) doubles, C = kSsT * EPT terms
+// grid (nch, NS); block kSsWT; dynamic smem (C + C/32) doubles, C = kSsWT * EPT terms
 // per chunk (EPT = 32, or 8 for small sums: 4x shorter serial thread walks).
 template <class TG, int EPT>
-__global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
+__global__ void __launch_bounds__(kSsWT, 6) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
                                                        const double* __restrict__ pre0) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
     pdl_trigger();
     extern __shared__ double tm[];
-    __shared__ double swd[8];
-    __shared__ SegF sws[9];
+    constexpr int NW = kSsWT / 32;
+    __shared__ double swd[NW];
+    __shared__ SegF sws[NW + 1];
     __shared__ int s_chunk, s_key;
     __shared__ double s_pre;
-    __shared__ long long s_i64[3][8];
+    __shared__ long long s_i64[3][NW];
 
     const int s = blockIdx.y;
     const SsState& S = sts.s[s];
@@ -388,7 +394,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 #endif
     __syncthreads();
     const int c = s_chunk;
-    constexpr int kC = kSsT * EPT;
+    constexpr int kC = kSsWT * EPT;
     const long long base = (long long)c * kC;
     const int clen = (int)min((long long)kC, n - base);
 
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
         double v[EPT];
         tg.template striped<EPT>(s, base + t, clen, v);
 #pragma unroll
-        for (int m = 0; m < EPT; ++m) tm[ss_pad(m * kSsT + t)] = v[m];
+        for (int m = 0; m < EPT; ++m) tm[ss_pad(m * kSsWT + t)] = v[m];
     }
     __syncthreads();
     const int e0 = t * EPT;
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
 
     // (2) approximate prefix by look-back
     double tot_approx;
-    const double ex_approx = block_excl_sum_tot_d(ts, swd, &tot_approx);
+    const double ex_approx = block_excl_sum_tot_d<NW>(ts, swd, &tot_approx);
     // pre0: approximate sum of the terms before this range (earlier row slabs)
     const double base_pre = pre0 ? pre0[s] : 0.0;
     if (t == 0) {
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
     if (uni) {
         tot = segf_id();
         long long lo, hi;
-        tot.g.Q[0] = tot.g.Q[1] = block_seg_i64(wk.Q[0], wk.mn[0], wk.mx[0], s_i64, &lo, &hi);
+        tot.g.Q[0] = tot.g.Q[1] = block_seg_i64<NW>(wk.Q[0], wk.mn[0], wk.mx[0], s_i64, &lo, &hi);
         tot.g.mn[0] = tot.g.mn[1] = lo;
         tot.g.mx[0] = tot.g.mx[1] = hi;
         tot.g.E = wk.segE;
@@ -509,7 +515,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
         x.f = r > 0;
         x.g = r > 0 ? cur : lead;
         x.cnt = r;
-        carry = block_excl_segscan(x, sws, &tot);
+        carry = block_excl_segscan<NW>(x, sws, &tot);
     }
     ph[4] = clock64();
     const bool last = c == nch - 1;
@@ -561,7 +567,7 @@ __global__ void __launch_bounds__(kSsT, 3) k_ss_walk(TG tg, long long n, int nch
             }
         }
     }
-    if (close && t == kSsT - 1) {
+    if (close && t == kSsWT - 1) {
         gmg_ss::Rec rec = gmg_ss::rec_make(tot.g, false, 0.0, (uint32_t)(base + clen - 1));
         if (!tot.f) rec.meta |= kRecOpen;
         out[R - 1] = rec;
@@ -596,7 +602,7 @@ __device__ __forceinline__ void ss_scan2_body(const SsPair& sts, int nch) {
     const int c = b * kSsScanB + t;
     const SegF a = c < nch ? agg_load(S.cagg, c) : segf_id();
     SegF tot;
-    const SegF ex = block_excl_segscan(a, sws, &tot);
+    const SegF ex = block_excl_segscan<kSsScanB / 32>(a, sws, &tot);
     unsigned char* bagg = S.cincl;
     unsigned char* bincl = S.cincl + (size_t)nb * sizeof(ChunkAgg);
     if (t == 0) {
@@ -980,7 +986,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double*
     pdl_trigger();
     __shared__ double swd[8];
     const int s = blockIdx.y;
-    const long long base = (long long)blockIdx.x * kSsC;
+    const long long base = (long long)blockIdx.x * kSsPC;
     double acc = 0.0;
 #pragma unroll 4
     for (int m = 0; m < kSsEPT; ++m) {
@@ -992,7 +998,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double*
 }
 
 template <int EPT>
-constexpr size_t ss_walk_smem() { return sizeof(double) * (kSsT * EPT + kSsT * EPT / 32); }
+constexpr size_t ss_walk_smem() { return sizeof(double) * (kSsWT * EPT + kSsWT * EPT / 32); }
 constexpr size_t ss_chain_smem() { return sizeof(gmg_ss::Rec) * 2 * kSsBatch; }
 
 // ---- term generators ----------------------------------------------------------
@@ -1005,14 +1011,14 @@ __device__ __forceinline__ int row_of(long long k, int nx, double inv_nx) {
 }
 
 // Each generator also loads a chunk's terms for one thread of the walk:
-// `striped(s, k0, clen, v)` fills v[m] = term k0 + m*kSsT (0 past the chunk),
+// `striped(s, k0, clen, v)` fills v[m] = term k0 + m*kSsWT (0 past the chunk),
 // where k0 = chunk base + threadIdx.x and clen = terms in the chunk.
 #define GMG_SS_STRIPED_DEFAULT                                                              \
     template <int EPT>                                                                       \
     __device__ __forceinline__ void striped(int s, long long k0, int clen, double (&v)[EPT]) const { \
         _Pragma("unroll") for (int m = 0; m < EPT; ++m) {                                   \
-            const int kl = m * kSsT + (int)threadIdx.x;                                      \
-            v[m] = kl < clen ? term(s, k0 + m * kSsT) : 0.0;                                 \
+            const int kl = m * kSsWT + (int)threadIdx.x;                                      \
+            v[m] = kl < clen ? term(s, k0 + m * kSsWT) : 0.0;                                 \
         }                                                                                    \
     }
 
@@ -1026,17 +1032,17 @@ struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid f
         const double v = __ldg(r + g.at(i, j));
         return v * v;
     }
-    // row/column of the first term once, then stepped by kSsT (no per-term division)
+    // row/column of the first term once, then stepped by kSsWT (no per-term division)
     template <int EPT>
     __device__ __forceinline__ void striped(int, long long k0, int clen, double (&v)[EPT]) const {
         int j = row_of(k0, g.nx, inv_nx), i = (int)(k0 - (long long)j * g.nx);
 #pragma unroll
         for (int m = 0; m < EPT; ++m) {
-            const int kl = m * kSsT + (int)threadIdx.x;
+            const int kl = m * kSsWT + (int)threadIdx.x;
             double x = 0.0;
             if (kl < clen) x = __ldg(r + g.at(i, j));
             v[m] = x * x;
-            i += kSsT;
+            i += kSsWT;
             while (i >= g.nx) {
                 i -= g.nx;
                 ++j;

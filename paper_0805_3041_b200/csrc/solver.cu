@@ -453,9 +453,9 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0, 
     for (int s = 0; s < NS; ++s)
         CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
     if (small)
-        launch_k(k_ss_walk<TG, kSsEPTs>, dim3(nch, NS), kSsT, ss_walk_smem<kSsEPTs>(), p->st, tg, n, nch, sp, pre0);
+        launch_k(k_ss_walk<TG, kSsEPTs>, dim3(nch, NS), kSsWT, ss_walk_smem<kSsEPTs>(), p->st, tg, n, nch, sp, pre0);
     else
-        launch_k(k_ss_walk<TG, kSsEPT>, dim3(nch, NS), kSsT, ss_walk_smem<kSsEPT>(), p->st, tg, n, nch, sp, pre0);
+        launch_k(k_ss_walk<TG, kSsEPT>, dim3(nch, NS), kSsWT, ss_walk_smem<kSsEPT>(), p->st, tg, n, nch, sp, pre0);
     const dim3 sg((nch + kSsScanB - 1) / kSsScanB, NS);
     if (fused_out)
         launch_k(k_ss_scan_chain<TG>, sg, kSsScanB, ss_chain_smem(), p->st, tg, n, sp, nch, fused_out, fused_start);
@@ -491,7 +491,7 @@ void seqsum_chain(gmg_problem* p, const TG& tg, long long n, double* out, const 
 template <class TG>
 void seqsum_fast(gmg_problem* p, const TG& tg, long long n, double* out, const double* start) {
     constexpr int NS = TG::NS;
-    const int nch = (int)((n + kSsC - 1) / kSsC);
+    const int nch = (int)((n + kSsPC - 1) / kSsPC);  // partial-sum CTAs (kSsT threads x kSsEPT terms)
     if (nch > p->nch_max) throw GmgError{GMG_ERR_LOGIC, "seqsum: workspace too small"};
     if (n == 0) {
         if (start)
