@@ -948,6 +948,10 @@ __global__ void __launch_bounds__(kSsScanB) k_ss_scan_chain(TG tg, long long n, 
     if (!s_last) return;
     __threadfence();
     ss_chain_body(tg, n, S, (int)blockIdx.y, out, start, smraw);
+    // every other CTA of this sum is done with the flags: leave them zeroed for the
+    // next sum on this workspace (the host then skips its memset)
+    __syncthreads();
+    for (int q = threadIdx.x; q < 2 + 2 * nch; q += blockDim.x) S.ticket[q] = 0;
 }
 
 // Small sums (n <= kSsDirect): the reference's loop literally. The CTA stages

@@ -205,6 +205,7 @@ struct gmg_problem {
     gmg_ss::Rec* recs = nullptr;     // per sum: rec_cap records (per-chunk slots)
     gmg_ss::Rec* recs2 = nullptr;    // per sum: rec_cap records (compacted, in order)
     int rec_cap = 0;
+    bool ss_clean = false;  // exact-sum flags known zero (the last walk ended in a fused scan+chain)
     unsigned long long* ss_stats = nullptr;  // [16] exact-sum engine counters (seqsum.cuh)
     double* gs_edge = nullptr;               // Gauss-Seidel wavefront warp-edge rows
     int* gs_prog = nullptr;                  // and their progress counters
@@ -450,8 +451,13 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0, 
     seqsum_attrs<TG>();
     if (n <= kSsDirect) return;  // the direct kernel needs no walk
     const SsPair sp = ss_state(p, nch);
-    for (int s = 0; s < NS; ++s)
-        CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)nch) * sizeof(int), p->st));
+    // A fused scan+chain leaves the flags it used zeroed; after the split path (row
+    // slabs) they are dirty and the whole per-sum flag region is cleared (a later sum
+    // with more chunks reads further into it).
+    if (!(fused_out && p->ss_clean))
+        for (int s = 0; s < NS; ++s)
+            CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)p->nch_max) * sizeof(int), p->st));
+    p->ss_clean = fused_out != nullptr;
     if (small)
         launch_k(k_ss_walk<TG, kSsEPTs>, dim3(nch, NS), kSsWT, ss_walk_smem<kSsEPTs>(), p->st, tg, n, nch, sp, pre0);
     else
@@ -2011,6 +2017,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         CK(cudaMemset(p->lb, 0, 2 * 2 * nm * sizeof(double)));  // look-back words start empty
         CK(dmalloc(&p->lbs, 2 * 2 * nm * sizeof(ChunkAgg)));
         CK(dmalloc(&p->flags, 2 * (2 + 2 * nm) * sizeof(int)));
+        CK(cudaMemset(p->flags, 0, 2 * (2 + 2 * nm) * sizeof(int)));
         // records: at most kSsRMax per chunk (a chunk with more stores one literal-resum marker)
         p->rec_cap = (int)std::min<size_t>(nm * kSsRMax, (size_t)INT_MAX / 2);
         CK(dmalloc(&p->recs, 2 * (size_t)p->rec_cap * sizeof(gmg_ss::Rec)));
