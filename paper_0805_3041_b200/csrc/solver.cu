@@ -206,6 +206,12 @@ struct gmg_problem {
     gmg_ss::Rec* recs2 = nullptr;    // per sum: rec_cap records (compacted, in order)
     int rec_cap = 0;
     bool ss_clean = false;  // exact-sum flags known zero (the last walk ended in a fused scan+chain)
+    // "correction nonzero" flags of adaptive omega, one slot per level visit of a cycle
+    // (reset by one memset per cycle instead of one per visit); nz_cur: the current visit's
+    static constexpr int kNzSlots = 1024;
+    int* nz_slots = nullptr;
+    int nz_next = 0;
+    int* nz_cur = nullptr;
     unsigned long long* ss_stats = nullptr;  // [16] exact-sum engine counters (seqsum.cuh)
     double* gs_edge = nullptr;               // Gauss-Seidel wavefront warp-edge rows
     int* gs_prog = nullptr;                  // and their progress counters
@@ -1160,7 +1166,7 @@ void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int o
     for (auto* q : S) {
         auto tn = make(q);
         seqsum_fast(q, tn.first, tn.second, q->dscr, nullptr);
-        if (with_nz) launch_k(k_nz_to_d, 1, 1, 0, st, q->nz, q->dscr + NS);
+        if (with_nz) launch_k(k_nz_to_d, 1, 1, 0, st, q->nz_cur, q->dscr + NS);
     }
     KCHECK();
     if (D->local) {
@@ -1172,7 +1178,7 @@ void dist_sum(const std::vector<gmg_problem*>& S, DistCtx* D, MakeTG make, int o
         NC(nccl().allGather(S[0]->dscr, S[0]->dscr + 32, 8, kNcclFloat64, D->comm, st));
     }
     for (auto* q : S)
-        launch_k(k_dist_prefix, 1, 32, 0, st, q->dscr + 32, q->rank, D->world, NS, with_nz ? 1 : 0, q->dscr + 8, q->nz,
+        launch_k(k_dist_prefix, 1, 32, 0, st, q->dscr + 32, q->rank, D->world, NS, with_nz ? 1 : 0, q->dscr + 8, q->nz_cur,
                                         mode == GMG_REDUCE_FAST ? q->sums + out_off : nullptr);
     KCHECK();
     if (mode == GMG_REDUCE_FAST) return;
@@ -1235,7 +1241,7 @@ struct Driver {
         r.kind = s.kind;
         if (s.u >= 0) r.u = bufptr(q, l, s.u);
         if (s.uc >= 0) r.uc = bufptr(q, l - 1, s.uc);
-        r.om = s.adaptive ? OmegaSrc{q->sums, q->nz, 0.0, q->status}
+        r.om = s.adaptive ? OmegaSrc{q->sums, q->nz_cur, 0.0, q->status}
                           : OmegaSrc{nullptr, nullptr, sp.correction_omega, q->status};
         return r;
     }
@@ -1385,8 +1391,13 @@ struct Driver {
     void omega_sums_d(int l, int uc) {
         for (auto* q : S) {
             Lev& L = q->lev(l);
-            CK(cudaMemsetAsync(q->nz, 0, sizeof(int), q->st));
-            if (g_debug_sync) dbg_sync(__LINE__);
+            // this visit's flag slot (zeroed at the cycle start); beyond the slots, a memset
+            if (q->nz_next < gmg_problem::kNzSlots) {
+                q->nz_cur = q->nz_slots + q->nz_next++;
+            } else {
+                q->nz_cur = q->nz;
+                CK(cudaMemsetAsync(q->nz, 0, sizeof(int), q->st));
+            }
             const int seg = seg_rows(L.nx, L.rows());
             dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.rows() + seg - 1) / seg);
             SrcProlong src{prolong_from(q, l - 1, q->lev(l - 1).buf[uc]), L.nx, L.ny, 0.0};
@@ -1403,9 +1414,9 @@ struct Driver {
                     const int strips = (L.nx + 123) / 124;
                     dim3 g4((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
                     launch_k(k_omega4<C>, g4, kS4W * 32, omega4_smem(), q->st, L.grid(), A, src.P, L.buf[DD], T0, T1,
-                                                                          q->nz, seg);
+                                                                          q->nz_cur, seg);
                 } else {
-                    launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, q->st, L.grid(), A, src, L.buf[DD], T0, T1, q->nz,
+                    launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, q->st, L.grid(), A, src, L.buf[DD], T0, T1, q->nz_cur,
                                                                        seg);
                 }
             });
@@ -1446,6 +1457,10 @@ struct Driver {
     // One outer cycle: x_out = cycle(x_in); r = b - A x_out -> DCAS[L]; norm^2 -> sums[2].
     void cycle(int xin, int xout) {
         const int L = p()->L;
+        for (auto* q : S) {  // fresh "correction nonzero" slots for this cycle's level visits
+            CK(cudaMemsetAsync(q->nz_slots, 0, gmg_problem::kNzSlots * sizeof(int), q->st));
+            q->nz_next = 0;
+        }
         if (sp.cycle == GMG_CYCLE_F) {
             // fcycle_pass (cycle.cpp:119-142): DCAS[L], DCAS[L-1] are current
             for (int l = L - 1; l >= 2; --l) {
@@ -1864,6 +1879,7 @@ void free_problem(gmg_problem* p) {
     dfree(p->gs_prog);
     dfree(p->sums);
     dfree(p->nz);
+    dfree(p->nz_slots);
     dfree(p->status);
     if (p->hostbuf) cudaFreeHost(p->hostbuf);
     if (p->ev0) cudaEventDestroy(p->ev0);
@@ -2036,6 +2052,9 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         CK(dmalloc(&p->sums, 8 * sizeof(double)));
         CK(cudaMemset(p->sums, 0, 8 * sizeof(double)));
         CK(dmalloc(&p->nz, sizeof(int)));
+        CK(dmalloc(&p->nz_slots, gmg_problem::kNzSlots * sizeof(int)));
+        CK(cudaMemset(p->nz_slots, 0, gmg_problem::kNzSlots * sizeof(int)));
+        p->nz_cur = p->nz;
         CK(dmalloc(&p->status, sizeof(int)));
         CK(cudaMemset(p->status, 0, sizeof(int)));
     }
