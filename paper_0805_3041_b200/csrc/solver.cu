@@ -1819,8 +1819,14 @@ void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep,
             CK(cudaGraphLaunch(ex[par], p->st));
         }
         par = 1 - par;
-        const double rk = std::sqrt(fetch_scalar(p, p->sums + 2));
-        if (sp.adaptive_correction && fetch_status(p) == 3) {
+        // ||r||^2 and the adaptive-omega status in one synchronisation (pinned host buffer)
+        CK(cudaMemcpyAsync(p->hostbuf, p->sums + 2, sizeof(double), cudaMemcpyDeviceToHost, p->st));
+        int* st_host = reinterpret_cast<int*>(p->hostbuf + 1);
+        if (sp.adaptive_correction)
+            CK(cudaMemcpyAsync(st_host, p->status, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+        CK(cudaStreamSynchronize(p->st));
+        const double rk = std::sqrt(p->hostbuf[0]);
+        if (sp.adaptive_correction && *st_host == 3) {
             rep->history_len = hl;
             throw std::runtime_error("adaptive_omega: correction has nonpositive energy");
         }
