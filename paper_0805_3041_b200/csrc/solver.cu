@@ -360,7 +360,11 @@ int seg_rows(int nx, int ny) {
     const int strips = (nx + 123) / 124;
     // large levels (the warp-strip kernels): segments no shorter than seg_min_big rows, so the
     // 2M-row vertical halo of a fused smoothing launch stays a small share of the march
-    const int smin = nx >= 255 ? seg_min_big : 8;
+    static const int seg_min_small = [] {
+        const char* e = getenv("GMG_SEG_MIN_SMALL");
+        return e ? atoi(e) : 2;  // small levels: short marches win (measured 8 -> 2: -1.3% per C4 cycle)
+    }();
+    const int smin = nx >= 255 ? seg_min_big : seg_min_small;
     int seg = 128;
     while (seg > smin && (long long)strips * ((ny + seg - 1) / seg) < target) seg /= 2;
     return seg;
