@@ -365,47 +365,24 @@ __device__ __forceinline__ SegF block_excl_segscan(const SegF& x, SegF* sw /* [N
 __device__ __forceinline__ int ss_pad(int e) { return e + (e >> 5); }
 
 // ---- walk ---------------------------------------------------------------------
-// grid (nch, NS); block kSsWT; dynamic smem (C + C/32) doubles, C = kSsWT * EPT terms
-// per chunk (EPT = 32, or 8 for small sums: 4x shorter serial thread walks).
-template <class TG, int EPT>
-__global__ void __launch_bounds__(kSsWT, 6) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
-                                                       const double* __restrict__ pre0) {
-    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
-    pdl_trigger();
-    extern __shared__ double tm[];
-    constexpr int NW = kSsWT / 32;
+// One chunk of WT*EPT terms, already in shared memory (padded layout ss_pad, striped
+// by WT): (2) approximate prefix by look-back, (3) thread walks, (4) merge across
+// threads, (5) the chunk's aggregate and its records. Block-uniform; WT threads.
+template <class TG, int EPT, int WT>
+__device__ __forceinline__ void walk_chunk(long long n, int nch, const SsState& S, int s, int c,
+                                           const double* __restrict__ tm, const double* __restrict__ pre0) {
+    constexpr int NW = WT / 32;
     __shared__ double swd[NW];
     __shared__ SegF sws[NW + 1];
-    __shared__ int s_chunk, s_key;
+    __shared__ int s_key;
     __shared__ double s_pre;
     __shared__ long long s_i64[3][NW];
-
-    const int s = blockIdx.y;
-    const SsState& S = sts.s[s];
     const int t = threadIdx.x;
-    long long ph[7];
-    ph[0] = clock64();
-#ifdef GMG_SS_TICKET
-    if (t == 0) s_chunk = atomicAdd(S.ticket, 1);
-#else
-    // chunk = blockIdx.x: CTAs are dispatched in increasing linear block order, so every
-    // look-back predecessor is already resident (no ticket atomic on the critical path)
-    if (t == 0) s_chunk = blockIdx.x;
-#endif
-    __syncthreads();
-    const int c = s_chunk;
-    constexpr int kC = kSsWT * EPT;
+    constexpr int kC = WT * EPT;
     const long long base = (long long)c * kC;
     const int clen = (int)min((long long)kC, n - base);
-
-    // (1) terms: striped (coalesced) loads, all in flight before the smem stores
-    {
-        double v[EPT];
-        tg.template striped<EPT>(s, base + t, clen, v);
-#pragma unroll
-        for (int m = 0; m < EPT; ++m) tm[ss_pad(m * kSsWT + t)] = v[m];
-    }
-    __syncthreads();
+    long long ph[7];
+    ph[0] = clock64();
     const int e0 = t * EPT;
     const int ne = max(0, min(EPT, clen - e0));
     double ts = 0.0;  // approximate (tree-order) sum of this thread's terms
@@ -567,11 +544,37 @@ __global__ void __launch_bounds__(kSsWT, 6) k_ss_walk(TG tg, long long n, int nc
             }
         }
     }
-    if (close && t == kSsWT - 1) {
+    if (close && t == WT - 1) {
         gmg_ss::Rec rec = gmg_ss::rec_make(tot.g, false, 0.0, (uint32_t)(base + clen - 1));
         if (!tot.f) rec.meta |= kRecOpen;
         out[R - 1] = rec;
     }
+}
+
+
+// grid (nch, NS); block kSsWT; dynamic smem (C + C/32) doubles, C = kSsWT * EPT terms
+// per chunk (EPT = 32, or 8 for small sums: 4x shorter serial thread walks).
+template <class TG, int EPT>
+__global__ void __launch_bounds__(kSsWT, 6) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
+                                                       const double* __restrict__ pre0) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
+    extern __shared__ double tm[];
+    const int s = blockIdx.y, t = threadIdx.x;
+    // chunk = blockIdx.x: CTAs are dispatched in increasing linear block order, so every
+    // look-back predecessor is already resident (no ticket atomic on the critical path)
+    const int c = blockIdx.x;
+    constexpr int kC = kSsWT * EPT;
+    const long long base = (long long)c * kC;
+    const int clen = (int)min((long long)kC, n - base);
+    {  // (1) terms: striped (coalesced) loads, all in flight before the smem stores
+        double v[EPT];
+        tg.template striped<EPT, kSsWT>(s, base + t, clen, v);
+#pragma unroll
+        for (int m = 0; m < EPT; ++m) tm[ss_pad(m * kSsWT + t)] = v[m];
+    }
+    __syncthreads();
+    walk_chunk<TG, EPT, kSsWT>(n, nch, sts.s[s], s, c, tm, pre0);
 }
 
 // ---- cross-chunk scan and record compaction --------------------------------
@@ -1018,11 +1021,11 @@ __device__ __forceinline__ int row_of(long long k, int nx, double inv_nx) {
 // `striped(s, k0, clen, v)` fills v[m] = term k0 + m*kSsWT (0 past the chunk),
 // where k0 = chunk base + threadIdx.x and clen = terms in the chunk.
 #define GMG_SS_STRIPED_DEFAULT                                                              \
-    template <int EPT>                                                                       \
+    template <int EPT, int WT>                                                               \
     __device__ __forceinline__ void striped(int s, long long k0, int clen, double (&v)[EPT]) const { \
         _Pragma("unroll") for (int m = 0; m < EPT; ++m) {                                   \
-            const int kl = m * kSsWT + (int)threadIdx.x;                                      \
-            v[m] = kl < clen ? term(s, k0 + m * kSsWT) : 0.0;                                 \
+            const int kl = m * WT + (int)threadIdx.x;                                         \
+            v[m] = kl < clen ? term(s, k0 + m * WT) : 0.0;                                    \
         }                                                                                    \
     }
 
@@ -1037,16 +1040,16 @@ struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid f
         return v * v;
     }
     // row/column of the first term once, then stepped by kSsWT (no per-term division)
-    template <int EPT>
+    template <int EPT, int WT>
     __device__ __forceinline__ void striped(int, long long k0, int clen, double (&v)[EPT]) const {
         int j = row_of(k0, g.nx, inv_nx), i = (int)(k0 - (long long)j * g.nx);
 #pragma unroll
         for (int m = 0; m < EPT; ++m) {
-            const int kl = m * kSsWT + (int)threadIdx.x;
+            const int kl = m * WT + (int)threadIdx.x;
             double x = 0.0;
             if (kl < clen) x = __ldg(r + g.at(i, j));
             v[m] = x * x;
-            i += kSsWT;
+            i += WT;
             while (i >= g.nx) {
                 i -= g.nx;
                 ++j;
