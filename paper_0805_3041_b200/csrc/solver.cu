@@ -620,7 +620,11 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
 }
 
 // levels at least this wide use the strip-per-warp smoother (k_smooth4)
-constexpr int kRingMinNx = 255;
+// levels at least this wide use the warp-strip kernels (march4.cuh); GMG_RING_MIN_NX for A/B
+static const int kRingMinNx = [] {
+    const char* e = getenv("GMG_RING_MIN_NX");
+    return e ? atoi(e) : 255;
+}();
 // 4: the warp-strip kernels (k_smooth4, k_resid4, k_omega4); 3: the earlier
 // row-streaming kernels (GMG_STREAM_KERNELS=3, for A/B timing)
 static int g_smooth_variant = [] {
