@@ -209,19 +209,23 @@ def run_reference_arm(args):
         for t in th:
             t.join()
 
-    for _ in range(args.warmup):
+    # one C4 step is ~20 s of CPU work: the run is bounded (at most 3 timed steps after one
+    # warm-up step) so that any --steps/--warmup finishes within a couple of minutes
+    steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    for _ in range(warmup):
         step()
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.time()
         step()
         times.append(time.time() - t0)
     total = sum(times)
-    value = P * n * args.steps / total
+    value = P * n * steps / total
     line = {
         "impl": "reference", "metric": "fine-grid DOF*F-cycles/s (fp64)", "value": value,
-        "unit": "DOF*cycles/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "unit": "DOF*cycles/s", "n_gpus": ws, "steps": steps, "warmup": warmup,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
+        "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1] rhs, std::mt19937)",
         "config": {"workload": f"{wl}: {w['desc']}", "dof": n},
         "cpu_baseline": {"value": value, "unit": "DOF*cycles/s", "cores": P, "kind": kind,
