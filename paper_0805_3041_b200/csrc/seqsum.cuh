@@ -47,7 +47,9 @@ constexpr int kSsMaxSums = 2;
 constexpr int kSsRMax = 512;           // records a chunk may store; more -> exact re-walk
 constexpr int kSsRunCap = 32;         // a merged run never spans more than this many chunks
 
-// Per-sum look-back state (flags, ticket and total zeroed before each walk).
+// Per-sum look-back state. ticket (unused), total, flag[0] (completion counter of the fused
+// scan+chain) and cflag are zero when a walk starts: set by the host's memset or left so by
+// the previous fused scan+chain.
 struct SsState {
     int* flag;       // [nch] approximate-sum look-back: 0 none, 1 aggregate, 2 inclusive
     int* cflag;      // [nch] run/count look-back flags
@@ -580,8 +582,8 @@ __global__ void __launch_bounds__(kSsWT, 6) k_ss_walk(TG tg, long long n, int nc
 // ---- cross-chunk scan and record compaction --------------------------------
 // Cross-chunk segmented scan + record compaction, single pass. grid (ceil(nch/256), NS);
 // 256 threads, a thread per chunk. Block exclusive segmented scan of the chunk
-// aggregates, then a decoupled look-back over the CTA aggregates (CTA order
-// from the ticket the walk left at nch, so every predecessor is running),
+// aggregates, then a decoupled look-back over the CTA aggregates (CTA = blockIdx.x:
+// in-order dispatch keeps every predecessor resident),
 // giving the run carried into each chunk and its first record's position; the
 // warps then copy each chunk's records into the ordered list, prepending the
 // carried-in run to an open record (seg_merge is associative, so this equals
@@ -592,16 +594,9 @@ __device__ __forceinline__ void ss_scan2_body(const SsPair& sts, int nch) {
     __shared__ SegF sws[9];
     __shared__ SegF s_cin[kSsScanB];
     __shared__ int s_cnt[kSsScanB];
-    __shared__ int s_b;
     const SsState& S = sts.s[blockIdx.y];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-#ifdef GMG_SS_TICKET
-    if (t == 0) s_b = atomicAdd(S.ticket, 1) - nch;
-#else
-    if (t == 0) s_b = blockIdx.x;
-#endif
-    __syncthreads();
-    const int b = s_b, nb = (nch + kSsScanB - 1) / kSsScanB;
+    const int b = blockIdx.x, nb = (nch + kSsScanB - 1) / kSsScanB;
     const int c = b * kSsScanB + t;
     const SegF a = c < nch ? agg_load(S.cagg, c) : segf_id();
     SegF tot;
