@@ -35,6 +35,9 @@ namespace gmg_dev {
 
 constexpr int kSsT = 256;             // threads of the chain / partial-sum kernels
 constexpr int kSsWT = 128;            // threads per chunk in the walk (6 CTAs per SM)
+#ifndef GMG_WALK_MINB
+#define GMG_WALK_MINB 6  // walk CTAs per SM the register budget is sized for
+#endif
 constexpr int kSsEPT = 32;            // terms per thread
 constexpr int kSsC = kSsWT * kSsEPT;  // terms per chunk (large sums)
 constexpr int kSsPC = kSsT * kSsEPT;  // terms per CTA of the fast-mode partial sums
@@ -557,7 +560,7 @@ __device__ __forceinline__ void walk_chunk(long long n, int nch, const SsState& 
 // grid (nch, NS); block kSsWT; dynamic smem (C + C/32) doubles, C = kSsWT * EPT terms
 // per chunk (EPT = 32, or 8 for small sums: 4x shorter serial thread walks).
 template <class TG, int EPT>
-__global__ void __launch_bounds__(kSsWT, 6) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
+__global__ void __launch_bounds__(kSsWT, GMG_WALK_MINB) k_ss_walk(TG tg, long long n, int nch, SsPair sts,
                                                        const double* __restrict__ pre0) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
     pdl_trigger();
