@@ -9,6 +9,7 @@ std::mt19937(seed_f=1) + uniform_real_distribution(-1,1) over the finest interio
     python oracle/make_golden.py c4         # the 8191^2 history (~5 min of CPU)
     python oracle/make_golden.py c2         # the 12 anisotropic Gauss-Seidel cases (~3 min)
     python oracle/make_golden.py c5         # one 16383^2 cycle (~4 min, ~36 GB RAM)
+    python oracle/make_golden.py c5_10      # all 10 C5 cycles (~23 min, ~36 GB RAM)
 
 Floats are stored as float.hex() strings so the fixtures are bit-exact.
 """
@@ -143,6 +144,14 @@ def c5():
     spec = CycleSpec(smoother="jacobi", smoothing_omega=0.7, pre_steps=3, post_steps=3,
                      tolerance=1e-30, max_cycles=1)
     solve_case("c5_1cycle", 14, spec, alpha=1e-2, beta=1.0, seed_x=2)
+
+
+def c5_10():
+    """BASELINE config 5 exactly: 10 F-cycles (tol=1e-30, max_cycles=10, the reference's
+    fixed-budget idiom, tests/test_study.cpp:112-113). ~23 min of CPU, ~36 GB RAM."""
+    spec = CycleSpec(smoother="jacobi", smoothing_omega=0.7, pre_steps=3, post_steps=3,
+                     tolerance=1e-30, max_cycles=10)
+    solve_case("c5_10cycle", 14, spec, alpha=1e-2, beta=1.0, seed_x=2)
 
 
 if __name__ == "__main__":

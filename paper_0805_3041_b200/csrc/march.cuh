@@ -170,91 +170,6 @@ __device__ __forceinline__ double jacobi_point(const Coef& A, int i, int j, doub
     return xc - omega * z;
 }
 
-// Launch: grid (ceil(nx/(TW-2M)), ceil(ny/seg)), block TW.
-// For SrcCorrect the correction weight is finished in the prologue from `om`.
-template <int M, int TW, int PF, class Coef, class Src>
-__global__ void __launch_bounds__(TW) k_smooth(Grid fg, Coef A, Src src, OmegaSrc om,
-                                               const double* __restrict__ g,
-                                               double* __restrict__ out, double omega_damp, int seg) {
-    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
-    pdl_trigger();
-    constexpr int OUTW = TW - 2 * M;
-    constexpr int ML = M > 0 ? M : 1;
-    __shared__ double sh[2][ML][TW];
-
-    const int t = threadIdx.x;
-    const int i = blockIdx.x * OUTW - M + t;
-    const int j0 = fg.w0 + blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.w1);
-    const bool col_in = i >= 0 && i < fg.nx;
-    const bool owner = col_in && t >= M && t < TW - M;
-
-    src.prepare(i);
-    if constexpr (std::is_same<Src, SrcCorrect>::value) {
-        src.omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && t == 0);
-    }
-
-    double win[ML][3];
-    double gring[ML];
-#pragma unroll
-    for (int l = 0; l < ML; ++l) {
-        win[l][0] = win[l][1] = win[l][2] = 0.0;
-        gring[l] = 0.0;
-    }
-
-    const int Jbeg = j0 - M;
-    const int Jend = j1 - 1 + M;  // inclusive
-    typename Src::Raw q[PF];
-    double gq[PF];
-#pragma unroll
-    for (int p = 0; p < PF; ++p) {
-        const int Jf = Jbeg + p;
-        q[p] = src.fetch(i, Jf);
-        gq[p] = (M > 0 && col_in && Jf >= 0 && Jf < fg.ny) ? __ldg(g + fg.at(i, Jf)) : 0.0;
-    }
-
-    for (int Jb = Jbeg; Jb <= Jend; Jb += PF) {
-#pragma unroll
-        for (int p = 0; p < PF; ++p) {
-            const int J = Jb + p;
-            if (J > Jend) break;  // uniform across the CTA
-            const typename Src::Raw raw = q[p];
-            const double gnew = gq[p];
-            {
-                const int Jf = J + PF;
-                q[p] = src.fetch(i, Jf);
-                gq[p] = (M > 0 && col_in && Jf >= 0 && Jf < fg.ny) ? __ldg(g + fg.at(i, Jf)) : 0.0;
-            }
-            const bool row_in = J >= 0 && J < fg.ny;
-            double nv = (col_in && row_in) ? src.make(raw, i, J) : 0.0;
-            if constexpr (M == 0) {
-                if (owner && J >= j0 && J < j1) out[fg.at(i, J)] = nv;
-            } else {
-                const int pb = (J - 1) & 1, cb = J & 1;
-#pragma unroll
-                for (int l = 0; l < M; ++l) {
-                    win[l][0] = win[l][1];
-                    win[l][1] = win[l][2];
-                    win[l][2] = nv;
-                    sh[cb][l][t] = nv;
-                    const int R = J - l - 1;
-                    const double xl = t > 0 ? sh[pb][l][t - 1] : 0.0;
-                    const double xr = t < TW - 1 ? sh[pb][l][t + 1] : 0.0;
-                    const double y = jacobi_point(A, cix(i, fg.nx), cix(R, fg.ny), win[l][1], xl, xr, win[l][0], win[l][2],
-                                                  gring[l], omega_damp);
-                    nv = (col_in && R >= 0 && R < fg.ny) ? y : 0.0;
-                }
-                const int RM = J - M;
-                if (owner && RM >= j0 && RM < j1) out[fg.at(i, RM)] = nv;
-#pragma unroll
-                for (int l = ML - 1; l > 0; --l) gring[l] = gring[l - 1];
-                gring[0] = gnew;
-                __syncthreads();
-            }
-        }
-    }
-}
-
 // ---------------- residual (+ restriction) ---------------------------------
 // d = g - A x0 (stencil.cpp:148-153), or with neg the smoother defect
 // A x0 - g (smoother.cpp:393-394), optionally stored; x0 optionally stored;

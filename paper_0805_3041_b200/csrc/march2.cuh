@@ -216,10 +216,9 @@ __global__ void __launch_bounds__(TW) k_smooth2(Grid fg, Coef A, Src src, OmegaS
 namespace gmg_dev {
 
 // ---------------------------------------------------------------------------
-// k_smooth3: k_smooth2 with the input rows staged through a shared-memory ring
-// by cp.async (16-byte pair copies; zero-fill for everything outside the
-// interior), D rows ahead. Registers keep only the stencil windows, so more
-// CTAs are resident and ~D rows of every CTA are in flight.
+// cp.async helpers of the warp-strip kernels (march4.cuh): 16- and 8-byte copies
+// into shared memory, zero-filled beyond src_bytes (rows/columns outside the
+// interior read nothing and land as +0).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cpa16(void* smem, const void* gmem, int src_bytes) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -235,18 +234,6 @@ __device__ __forceinline__ void cpa_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
-// stage a fine pair (i even) of row j: zeros outside the interior
-__device__ __forceinline__ void stage_pair(double2* dst, const double* a, const Grid& g, int i, int j) {
-    int bytes = 0;
-    const double* src = a;  // any valid address when nothing is read
-    if (j >= 0 && j < g.ny && i + 1 >= 0 && i < g.nx) {
-        if (i >= 0) {
-            src = a + g.at(i, j);
-            bytes = (i + 1 < g.nx) ? 16 : 8;
-        }
-    }
-    cpa16(dst, src, bytes);
-}
 // stage one coarse value (zeros outside the coarse interior)
 __device__ __forceinline__ void stage_coarse(double* dst, const double* uc, const Grid& cg, int ci, int cj) {
     const bool in = cg.inside(ci, cj);
@@ -254,145 +241,5 @@ __device__ __forceinline__ void stage_coarse(double* dst, const double* uc, cons
 }
 
 enum SrcKind3 { K3_ZERO = 0, K3_U = 1, K3_PROLONG = 2, K3_CORRECT = 3 };
-
-template <int M, int TW, int D, int SK, class Coef>
-struct Smooth3Smem {
-    static constexpr bool HAS_U = SK == K3_U || SK == K3_CORRECT;
-    static constexpr bool HAS_C = SK == K3_PROLONG || SK == K3_CORRECT;
-    static constexpr int ML = M > 0 ? M : 1;
-    double2 u[HAS_U ? D : 1][TW];
-    double2 g[D][TW];
-    double c[HAS_C ? D : 1][2][TW + 2];
-    double2 sh[2][ML][TW];
-};
-
-template <int M, int TW, int D, int SK, class Coef>
-__global__ void __launch_bounds__(TW) k_smooth3(Grid fg, Coef A, const double* __restrict__ u, Prolong P,
-                                                OmegaSrc om, const double* __restrict__ g,
-                                                double* __restrict__ out, double omega_damp, int seg) {
-    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
-    pdl_trigger();
-    using SM = Smooth3Smem<M, TW, D, SK, Coef>;
-    constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C;
-    constexpr int H = (M + 1) & ~1;
-    constexpr int OUTW = 2 * TW - 2 * H;
-    constexpr int ML = SM::ML;
-    extern __shared__ __align__(16) unsigned char smraw3[];
-    SM& S = *reinterpret_cast<SM*>(smraw3);
-
-    const int t = threadIdx.x;
-    const int i = blockIdx.x * OUTW - H + 2 * t;  // even
-    const int j0 = fg.w0 + blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.w1);
-    const bool in0 = i >= 0 && i < fg.nx, in1 = i + 1 >= 0 && i + 1 < fg.nx;
-    const bool owner = 2 * t >= H && 2 * t < 2 * TW - H;
-    const int m0 = (i - 2 * t) / 2 - 1;  // first coarse column staged (slot 0)
-    const double tX = (HAS_C && in0) ? __ldg(P.tx + i) : 0.0;
-    double omega = 0.0;
-    if constexpr (SK == K3_CORRECT) omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && t == 0);
-
-    const int Jbeg = j0 - M;
-    const int Jend = j1 - 1 + M;
-    // stage row J into ring slot J mod D
-    auto stage = [&](int J) {
-        const int sl = ((J % D) + D) % D;
-        if constexpr (HAS_U) stage_pair(&S.u[sl][t], u, fg, i, J);
-        if constexpr (M > 0) stage_pair(&S.g[sl][t], g, fg, i, J);
-        if constexpr (HAS_C) {
-            const int pj = J + 1;
-            const int r0 = (pj & 1) ? (pj - 1) / 2 - 1 : pj / 2 - 1;
-            const bool row_in = J >= 0 && J < fg.ny;
-            for (int rr = 0; rr < 2; ++rr) {
-                const int cj = row_in ? r0 + rr : -100;
-                stage_coarse(&S.c[sl][rr][t], P.uc, P.cg, m0 + t, cj);
-                if (t < 2) stage_coarse(&S.c[sl][rr][TW + t], P.uc, P.cg, m0 + TW + t, cj);
-            }
-        }
-        cpa_commit();
-    };
-#pragma unroll
-    for (int p = 0; p < D - 1; ++p) stage(Jbeg + p);
-    cpa_wait<D - 2>();
-    __syncthreads();
-
-    double2 win[ML][3];
-    double2 gring[ML];
-#pragma unroll
-    for (int l = 0; l < ML; ++l) {
-        win[l][0] = win[l][1] = win[l][2] = make_double2(0.0, 0.0);
-        gring[l] = make_double2(0.0, 0.0);
-    }
-    for (int J = Jbeg; J <= Jend; ++J) {
-        stage(J + D - 1);  // the slot of row J-1, released by the previous barrier
-        const int sl = ((J % D) + D) % D;
-        const bool row_in = J >= 0 && J < fg.ny;
-        double2 nv = make_double2(0.0, 0.0);
-        if (row_in) {
-            if constexpr (SK == K3_U) nv = S.u[sl][t];
-            if constexpr (HAS_C) {
-                Pair2Raw r;
-                r.a = S.c[sl][0][t];
-                r.b = S.c[sl][0][t + 1];
-                r.c = S.c[sl][1][t];
-                r.d = S.c[sl][1][t + 1];
-                r.ty = ((J + 1) & 1) ? __ldg(P.ty + J) : 0.0;
-                const double2 cv = prolong2_make(r, i, J, fg.nx, tX);
-                if constexpr (SK == K3_PROLONG) {
-                    nv = cv;
-                } else {
-                    const double2 uu = S.u[sl][t];
-                    nv = make_double2(uu.x + omega * cv.x, uu.y + omega * cv.y);
-                }
-            }
-        }
-        if (!in0) nv.x = 0.0;
-        if (!in1) nv.y = 0.0;
-        if constexpr (M == 0) {
-            if (owner && J >= j0 && J < j1) {
-                if (in0 && in1) {
-                    *reinterpret_cast<double2*>(out + fg.at(i, J)) = nv;
-                } else {
-                    if (in0) out[fg.at(i, J)] = nv.x;
-                    if (in1) out[fg.at(i + 1, J)] = nv.y;
-                }
-            }
-        } else {
-            const double2 gnew = S.g[sl][t];
-            const int pb = (J - 1) & 1, cb = J & 1;
-#pragma unroll
-            for (int l = 0; l < M; ++l) {
-                win[l][0] = win[l][1];
-                win[l][1] = win[l][2];
-                win[l][2] = nv;
-                S.sh[cb][l][t] = nv;
-                const int R = J - l - 1;
-                const double xl = t > 0 ? S.sh[pb][l][t - 1].y : 0.0;
-                const double xr = t < TW - 1 ? S.sh[pb][l][t + 1].x : 0.0;
-                const double2 c = win[l][1], dn = win[l][0], upv = win[l][2];
-                const int Rc = cix(R, fg.ny);
-                const double y0 = jacobi_point(A, cix(i, fg.nx), Rc, c.x, xl, c.y, dn.x, upv.x, gring[l].x, omega_damp);
-                const double y1 =
-                    jacobi_point(A, cix(i + 1, fg.nx), Rc, c.y, c.x, xr, dn.y, upv.y, gring[l].y, omega_damp);
-                const bool rin = R >= 0 && R < fg.ny;
-                nv = make_double2((rin && in0) ? y0 : 0.0, (rin && in1) ? y1 : 0.0);
-            }
-            const int RM = J - M;
-            if (owner && RM >= j0 && RM < j1) {
-                if (in0 && in1) {
-                    *reinterpret_cast<double2*>(out + fg.at(i, RM)) = nv;
-                } else {
-                    if (in0) out[fg.at(i, RM)] = nv.x;
-                    if (in1) out[fg.at(i + 1, RM)] = nv.y;
-                }
-            }
-#pragma unroll
-            for (int l = ML - 1; l > 0; --l) gring[l] = gring[l - 1];
-            gring[0] = gnew;
-        }
-        cpa_wait<D - 2>();  // row J+1 has landed (for this thread)
-        __syncthreads();    // ... for every thread; slot of row J is free again
-    }
-    cpa_wait<0>();
-}
 
 }  // namespace gmg_dev

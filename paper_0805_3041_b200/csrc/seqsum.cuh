@@ -1,7 +1,9 @@
 // Exact-order (bit-identical to a left-to-right loop) fp64 summation on the GPU.
-// Algorithm and invariants: seqsum_core.h. Two launches per sum (+1 memset):
+// Algorithm and invariants: seqsum_core.h. Two launches per sum (the look-back
+// flags are left zeroed by the fused scan+chain; only the split path of row slabs
+// clears them with a memset):
 //
-//   k_ss_walk       : one CTA per chunk of 256*EPT terms (EPT = 32; 8 for sums of
+//   k_ss_walk       : one CTA of kSsWT = 128 threads per chunk of 128*EPT terms (EPT = 32; 8 for sums of
 //                     <= 2^20 terms), chunk = blockIdx.x (in-order dispatch, so every
 //                     look-back predecessor is resident). (1) load the chunk's terms
 //                     (striped, coalesced) into shared memory; (2) publish its

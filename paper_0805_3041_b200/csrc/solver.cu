@@ -22,6 +22,7 @@
 #include <memory>
 #include <mutex>
 #include <random>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -377,8 +378,22 @@ void with_coef(const Lev& L, F&& f) {
     else f(L.cfield);
 }
 
+// Once-per-device setup (function attributes apply to the current device only):
+// a (key, device) set guarded by a mutex, so problems on several devices and
+// concurrent creates/solves on different threads each configure their device.
+bool first_on_device(const void* key) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    return done.insert({key, dev}).second;
+}
+
+// Dynamic shared memory opt-in of kernel fn on the current device (once per device).
 template <class T>
 void set_smem(T* fn, size_t bytes) {
+    if (!first_on_device(reinterpret_cast<const void*>(fn))) return;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)bytes));
 }
@@ -414,21 +429,17 @@ SsPair ss_state(gmg_problem* p, int nch) {
 
 template <class TG>
 void seqsum_attrs() {
-    static bool attr_done = false;
-    if (!attr_done) {
-        set_smem(k_ss_walk<TG, kSsEPT>, ss_walk_smem<kSsEPT>());
-        set_smem(k_ss_walk<TG, kSsEPTs>, ss_walk_smem<kSsEPTs>());
-        set_smem(k_ss_chain<TG>, ss_chain_smem());
-        set_smem(k_ss_scan_chain<TG>, ss_chain_smem());
-        attr_done = true;
-    }
+    set_smem(k_ss_walk<TG, kSsEPT>, ss_walk_smem<kSsEPT>());
+    set_smem(k_ss_walk<TG, kSsEPTs>, ss_walk_smem<kSsEPTs>());
+    set_smem(k_ss_chain<TG>, ss_chain_smem());
+    set_smem(k_ss_scan_chain<TG>, ss_chain_smem());
 }
 
 // Loads (lazy module loading) and configures every exact-sum kernel before any
 // graph capture, so no kernel is first touched while a stream is capturing.
 void preload_seqsum_kernels() {
-    static bool done = false;
-    if (done) return;
+    static const char key = 0;
+    if (!first_on_device(&key)) return;
     seqsum_attrs<NormTerms>();
     seqsum_attrs<ArrTerms>();
     seqsum_attrs<DotTerms>();
@@ -439,7 +450,6 @@ void preload_seqsum_kernels() {
     CK(cudaFuncGetAttributes(&fa, k_ss_direct<ArrTerms>));
     CK(cudaFuncGetAttributes(&fa, k_ss_direct<DotTerms>));
     CK(cudaFuncGetAttributes(&fa, k_ss_direct<FlatNormTerms>));
-    done = true;
 }
 
 // Sums of TG's NS term sequences, each bit-identical to the reference's
@@ -558,16 +568,6 @@ struct SmoothSrc {
 };
 
 template <int M, class Coef, class Src>
-void launch_smooth_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, OmegaSrc om,
-                     const double* g, double* out, double wd) {
-    constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
-    const int seg = seg_rows(L.nx, L.rows());
-    dim3 grid((L.nx + (kTW - 2 * M) - 1) / (kTW - 2 * M), (L.rows() + seg - 1) / seg);
-    launch_k(k_smooth<M, kTW, PF, Coef, Src>, grid, kTW, 0, p->st, L.grid(), A, src, om, g, out, wd, seg);
-    KCHECK();
-}
-
-template <int M, class Coef, class Src>
 void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, OmegaSrc om,
                       const double* g, double* out, double wd) {
     constexpr int H = (M + 1) & ~1;
@@ -580,36 +580,12 @@ void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& sr
 }
 
 template <int M, int SK, class Coef>
-void launch_smooth3_t(gmg_problem* p, const Lev& L, const Coef& A, const double* u, const double* uc,
-                      OmegaSrc om, const double* g, double* out, double wd) {
-    constexpr int D = 6;
-    constexpr int H = (M + 1) & ~1;
-    constexpr int OUTW = 2 * kTW - 2 * H;
-    using SM = Smooth3Smem<M, kTW, D, SK, Coef>;
-    static bool attr = false;
-    if (!attr) {
-        set_smem(k_smooth3<M, kTW, D, SK, Coef>, sizeof(SM));
-        attr = true;
-    }
-    Prolong P{};
-    if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
-    const int seg = seg_rows(L.nx, L.rows());
-    dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
-    launch_k(k_smooth3<M, kTW, D, SK, Coef>, grid, kTW, sizeof(SM), p->st, L.grid(), A, u, P, om, g, out, wd, seg);
-    KCHECK();
-}
-
-template <int M, int SK, class Coef>
 void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* u, const double* uc,
                       OmegaSrc om, const double* g, double* out, double wd) {
     constexpr int H = (M + 1) & ~1;
     constexpr int OW = 128 - 2 * H;
     constexpr size_t smem = smooth4_smem<SK>();
-    static bool attr = false;
-    if (!attr) {
-        set_smem(k_smooth4<M, SK, Coef>, smem);
-        attr = true;
-    }
+    set_smem(k_smooth4<M, SK, Coef>, smem);
     Prolong P{};
     if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
     const int seg = seg_rows(L.nx, L.rows());
@@ -619,19 +595,11 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     KCHECK();
 }
 
-// levels at least this wide use the strip-per-warp smoother (k_smooth4)
 // levels at least this wide use the warp-strip kernels (march4.cuh); GMG_RING_MIN_NX for A/B
 static const int kRingMinNx = [] {
     const char* e = getenv("GMG_RING_MIN_NX");
     return e ? atoi(e) : 255;
 }();
-// 4: the warp-strip kernels (k_smooth4, k_resid4, k_omega4); 3: the earlier
-// row-streaming kernels (GMG_STREAM_KERNELS=3, for A/B timing)
-static int g_smooth_variant = [] {
-    const char* e = std::getenv("GMG_STREAM_KERNELS");
-    return (e && e[0] == '3') ? 3 : 4;
-}();
-
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
                        double* out, double wd) {
@@ -644,21 +612,12 @@ void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const Smooth
             default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
         }
     } else {
-    if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
+    if (L.nx >= kRingMinNx) {
         switch (s.kind) {
             case S_ZERO: launch_smooth4_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
             case S_U: launch_smooth4_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
             case S_PROLONG: launch_smooth4_t<M, K3_PROLONG>(p, L, A, nullptr, s.uc, s.om, g, out, wd); return;
             case S_CORRECT: launch_smooth4_t<M, K3_CORRECT>(p, L, A, s.u, s.uc, s.om, g, out, wd); return;
-            default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
-        }
-    }
-    if (L.nx >= kRingMinNx) {
-        switch (s.kind) {
-            case S_ZERO: launch_smooth3_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
-            case S_U: launch_smooth3_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
-            case S_PROLONG: launch_smooth3_t<M, K3_PROLONG>(p, L, A, nullptr, s.uc, s.om, g, out, wd); return;
-            case S_CORRECT: launch_smooth3_t<M, K3_CORRECT>(p, L, A, s.u, s.uc, s.om, g, out, wd); return;
             default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
         }
     }
@@ -688,7 +647,7 @@ void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const Smooth
 // One launch of M <= 4 Jacobi steps.
 void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, const double* g, double* out,
                    double wd) {
-    if (L.kind == 0 && L.cconst.c_pow2 && L.nx >= kRingMinNx && g_smooth_variant == 4) {  // k_smooth4
+    if (L.kind == 0 && L.cconst.c_pow2 && L.nx >= kRingMinNx) {  // k_smooth4
         CoefConstP2 A;
         static_cast<CoefConst&>(A) = L.cconst;
         switch (M) {
@@ -714,26 +673,6 @@ void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, cons
 
 constexpr int kMaxFuse = 4;
 
-// `steps` smoothing steps from source s; writes alternate between bufA and
-// bufB (first launch -> bufA). Returns the buffer holding the result.
-double* smooth_steps(gmg_problem* p, const Lev& L, int steps, SmoothSrc s, const double* g, double* bufA,
-                     double* bufB, double wd) {
-    double* dst = bufA;
-    int left = steps;
-    bool first = true;
-    while (first || left > 0) {
-        const int M = std::min(left, kMaxFuse);
-        launch_smooth(p, L, M, s, g, dst, wd);
-        left -= M;
-        first = false;
-        s = SmoothSrc{};
-        s.kind = S_U;
-        s.u = dst;
-        if (left > 0) dst = (dst == bufA) ? bufB : bufA;
-    }
-    return dst;
-}
-
 template <class Coef, class Src>
 void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src, const double* g,
                     double* dout, double* x0out, double* gc, int neg = 0,
@@ -757,11 +696,7 @@ template <bool SUM, class Coef>
 void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* u, const double* e, const double* g,
                      double* dout, double* x0out, double* gc) {
     constexpr size_t smem = resid4_smem<SUM>();
-    static bool attr = false;
-    if (!attr) {
-        set_smem(k_resid4<SUM, Coef>, smem);
-        attr = true;
-    }
+    set_smem(k_resid4<SUM, Coef>, smem);
     Grid cg{0, 0, 0};
     RestrictW rw{};
     if (gc) {
@@ -779,7 +714,7 @@ void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* 
 // residual of (u, or x+e when e != null) against g; optional outputs.
 void launch_resid(gmg_problem* p, const Lev& L, const double* u, const double* e, const double* g,
                   double* dout, double* x0out, double* gc) {
-    if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
+    if (L.nx >= kRingMinNx) {
         with_coef(L, [&](const auto& A) {
             if (e)
                 launch_resid4_t<true>(p, L, A, u, e, g, dout, x0out, gc);
@@ -831,11 +766,7 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
     if (blocks > 148) throw GmgError{GMG_ERR_UNSUPPORTED, "gs: more rows than one co-resident wavefront"};
     CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
     if (g_debug_sync) dbg_sync(__LINE__);
-    static bool attr = false;
-    if (!attr) {
-        set_smem(k_gs_wave<Pol>, gs_smem());
-        attr = true;
-    }
+    set_smem(k_gs_wave<Pol>, gs_smem());
     launch_k(k_gs_wave<Pol>, blocks, kGsWarps * 32, gs_smem(), p->st, L.grid(), pol, d, x, xo, damp, p->gs_edge,
                                                                  p->gs_prog);
     KCHECK();
@@ -988,31 +919,13 @@ void norm_sum(gmg_problem* p, const Lev& L, const double* v, double* out, int mo
     seqsum(p, NormTerms{v, L.grid(), 1.0 / L.nx}, L.n(), out, mode);
 }
 
-// adaptive_omega sums for corr = P uc: terms materialised by k_omega_terms.
-void omega_sums(gmg_problem* p, const Lev& L, const double* d, const double* uc, int mode) {
-    CK(cudaMemsetAsync(p->nz, 0, sizeof(int), p->st));
-    if (g_debug_sync) dbg_sync(__LINE__);
-    const int seg = seg_rows(L.nx, L.rows());
-    dim3 grid((L.nx + (kTW - 2) - 1) / (kTW - 2), (L.rows() + seg - 1) / seg);
-    SrcProlong src{prolong_from(p, L.l - 1, uc), L.nx, L.ny, 0.0};
-    double* T0 = p->T;
-    double* T1 = p->T + p->lev(p->L).n();
-    with_coef(L, [&](const auto& A) {
-        using C = std::decay_t<decltype(A)>;
-        launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, p->st, L.grid(), A, src, d, T0, T1, p->nz, seg);
-    });
-    KCHECK();
-    seqsum(p, ArrTerms{T0, T1}, L.n(), p->sums, mode);
-}
-
 // ---------------------------------------------------------------------------
 // row-slab transport: halo rows, gathers, the exact-sum handoff
 // ---------------------------------------------------------------------------
 NcclApi& nccl() {
     static NcclApi a;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    static std::once_flag once;
+    std::call_once(once, [] {
         void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (h) {
             a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
@@ -1026,7 +939,7 @@ NcclApi& nccl() {
             a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(dlsym(h, "ncclGroupEnd"));
             a.errStr = reinterpret_cast<decltype(a.errStr)>(dlsym(h, "ncclGetErrorString"));
         }
-    }
+    });
     if (!a.send || !a.recv || !a.bcast || !a.allGather || !a.groupStart || !a.groupEnd || !a.commInitRank)
         throw GmgError{GMG_ERR_UNSUPPORTED, "row-slab mode needs libnccl.so.2"};
     return a;
@@ -1340,11 +1253,7 @@ struct Driver {
         V.uc = s.kind == S_PROLONG ? bufptr(q, l - 1, s.uc) : nullptr;
         V.out = q->lev(l).buf[U0];
         V.status = q->status;
-        static bool attr = false;
-        if (!attr) {
-            set_smem(k_vsmall, kVSmemMax);
-            attr = true;
-        }
+        set_smem(k_vsmall, kVSmemMax);
         launch_k(k_vsmall, 1, kVThreads, vsmall_smem(l), q->st, V);
         KCHECK();
     }
@@ -1413,12 +1322,8 @@ struct Driver {
             double* T1 = q->T + q->lev(q->L).n();
             with_coef(L, [&](const auto& A) {
                 using C = std::decay_t<decltype(A)>;
-                if (L.nx >= kRingMinNx && g_smooth_variant == 4) {
-                    static bool attr = false;
-                    if (!attr) {
-                        set_smem(k_omega4<C>, omega4_smem());
-                        attr = true;
-                    }
+                if (L.nx >= kRingMinNx) {
+                    set_smem(k_omega4<C>, omega4_smem());
                     const int strips = (L.nx + 123) / 124;
                     dim3 g4((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
                     launch_k(k_omega4<C>, g4, kS4W * 32, omega4_smem(), q->st, L.grid(), A, src.P, L.buf[DD], T0, T1,
