@@ -18,6 +18,7 @@
  *   gmg_dev_adaptive_omega  <- gmg::adaptive_omega           include/gmg/cycle.hpp:86-87 (src/cycle.cpp:40-51)
  *   gmg_dev_coarse_solve    <- gmg::BandedCholesky::solve    include/gmg/stencil.hpp:54 (src/stencil.cpp:190-210)
  *   gmg_dev_norm_l2/dot/axpy<- gmg::norm_l2 / dot / axpy     include/gmg/grid_function.hpp:29-34 (src/stencil.cpp:9-31)
+ *   gmg_dev_make_start_vector <- gmg::make_start_vector      include/gmg/study.hpp:20-21 (src/study.cpp:40-79)
  *
  * Exceptions become status codes; the C++ shim
  * include/gmg_b200.hpp re-throws the reference's own exception types.
@@ -165,6 +166,13 @@ int gmg_dev_solve_devptr(gmg_problem* p, const gmg_cycle_desc* spec, const doubl
 /* gmg::mg_cycle on level `level` (u0, g in, u out; host pointers). */
 int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, const double* u0,
                      const double* g, double* u);
+
+/* gmg::make_start_vector (study.cpp:40-79) on the finest level: kind 0 zero,
+ * 1 nested (restrict b to level 1, direct solve, then per level prolongation
+ * and one smooth_step of spec's smoother). b, x: host arrays of the finest
+ * level. Continuation (kind 2) is a host copy of another solution and has no
+ * device counterpart: GMG_ERR_INVALID. */
+int gmg_dev_make_start_vector(gmg_problem* p, const gmg_cycle_desc* spec, int kind, const double* b, double* x);
 
 /* ---- per-operator entry points (host arrays; unit parity) ------------------- */
 int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y);

@@ -985,3 +985,52 @@ done:
     free(sm);
     return st;
 }
+
+/* make_start_vector, study.cpp:40-79: kind 0 zero, 1 nested (a direct level-1
+ * solve of the restricted right-hand side, then prolongation + one smooth_step
+ * per level, study.cpp:46-58). Continuation (kind 2) is a host copy and has no
+ * arithmetic of its own. */
+int orc_start_vector(const orc_problem* p, const orc_cycle* spec, int kind, const double* b, double* x) {
+    const int L = p->L;
+    const size_t nL = nlev(&p->g[L - 1]);
+    if (kind == 0) {
+        memset(x, 0, nL * sizeof(double));
+        return ORC_OK;
+    }
+    if (kind != 1) return fail(ORC_ERR_INVALID, "start: kind must be zero or nested");
+    if (L == 1) {
+        chol_solve(p, b, x);
+        return ORC_OK;
+    }
+    double** rhs = (double**)calloc((size_t)L + 1, sizeof(double*));
+    rhs[L] = dalloc(nL);
+    memcpy(rhs[L], b, nL * sizeof(double));
+    for (int l = L; l >= 2; --l) {
+        rhs[l - 1] = dalloc(nlev(&p->g[l - 2]));
+        restrict_(&p->g[l - 1], &p->g[l - 2], rhs[l], rhs[l - 1]);
+    }
+    smoother_t* sm = NULL;
+    int st = setup_all(p, spec, &sm);
+    if (st) goto out;
+    {
+        double* u = dalloc(nlev(&p->g[0]));
+        chol_solve(p, rhs[1], u);
+        for (int l = 2; l <= L && !st; ++l) {
+            const size_t n = nlev(&p->g[l - 1]);
+            double* pu = dalloc(n);
+            prolong(&p->g[l - 2], &p->g[l - 1], u, pu);
+            free(u);
+            u = dalloc(n);
+            st = sm_step(&sm[l - 1], pu, rhs[l], spec->smoothing_omega, u);
+            free(pu);
+        }
+        if (!st) memcpy(x, u, nL * sizeof(double));
+        free(u);
+    }
+    for (int l = 0; l < L; ++l) sm_free(&sm[l]);
+    free(sm);
+out:
+    for (int l = 1; l <= L; ++l) free(rhs[l]);
+    free(rhs);
+    return st;
+}

@@ -72,6 +72,9 @@ int orc_mg_cycle(const orc_problem* p, const orc_cycle* spec, int level, const d
 int orc_solve(const orc_problem* p, const orc_cycle* spec, const double* b, double* x,
               double* history, int* history_len, int* iterations, int* converged);
 
+/* make_start_vector (study.cpp:40-79): kind 0 zero, 1 nested */
+int orc_start_vector(const orc_problem* p, const orc_cycle* spec, int kind, const double* b, double* x);
+
 void orc_random_vector(long long n, unsigned seed, double* out);
 
 #ifdef __cplusplus

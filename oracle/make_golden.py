@@ -99,6 +99,30 @@ def ops_case(name, levels, coarse, coords, alpha, beta, grading):
     save(name, out)
 
 
+START_CASES = [
+    # levels, coarse, coords, alpha, grading, smoother, smoother_omega
+    (5, (1, 1), "cartesian", 1.0, (1.0, 1.0), "jacobi", 1.0),
+    (5, (2, 3), "cylindrical", 0.3, (1.0, 1.0), "gauss_seidel", 1.0),
+    (4, (1, 1), "spherical", 1.3, (1.1, 0.93), "adi", 0.9),
+    (4, (3, 2), "cartesian", 0.1, (1.0, 1.02), "ilu0", 1.1),
+    (4, (1, 1), "cartesian", 1.0, (1.0, 1.0), "richardson", 5.0),
+    (1, (5, 4), "cartesian", 1.0, (1.0, 1.0), "sor", 1.3),
+]
+
+
+def start_vectors():
+    """gmg::make_start_vector (study.cpp:40-79), nested, on small problems: full vectors."""
+    cases = []
+    for levels, coarse, coords, alpha, grading, sm, som in START_CASES:
+        ref = Reference(levels, coarse[0], coarse[1], grading, coords, alpha, 1.0)
+        b = Reference.random_vector(ref.n(levels), 5)
+        spec = CycleSpec(smoother=sm, smoother_omega=som, smoothing_omega=0.7)
+        cases.append(dict(problem=dict(levels=levels, coarse_nx=coarse[0], coarse_ny=coarse[1], coords=coords,
+                                       alpha=alpha, beta=1.0, grading=list(grading)),
+                          b_seed=5, spec=spec.__dict__, nested=hx(ref.start_vector(spec, "nested", b))))
+    save("start_vectors", dict(cases=cases, generator="oracle/make_golden.py via oracle/_ref (reference sources)"))
+
+
 def fast():
     rv = Reference.random_vector(64, 1)
     save("random_vector", dict(seed=1, n=64, values=hx(rv)))
@@ -125,6 +149,7 @@ def fast():
     solve_case("diverge_omega", 6, jac(tolerance=1e-12, adaptive_correction=False, correction_omega=40.0,
                                        max_cycles=30))
     solve_case("c4_small_2047", 11, jac(tolerance=1e-10, max_cycles=3))
+    start_vectors()
 
 
 def c4():

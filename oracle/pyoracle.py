@@ -27,6 +27,7 @@ COORDS = {"cartesian": 0, "cylindrical": 1, "spherical": 2}
 SMOOTHERS = ["richardson", "jacobi", "gauss_seidel", "sor", "ilu0", "tri_x", "tri_y",
              "adi", "gstri_x", "gstri_y", "gsadi"]
 CYCLES = {"V": 0, "W": 1, "F": 2}
+START_KINDS = ["zero", "nested", "continuation"]  # gmg::StartVectorKind (config.hpp:11)
 UNLIMITED = (1 << 64) - 1
 
 _dp = C.POINTER(C.c_double)
@@ -233,6 +234,14 @@ class Oracle(_Backend):
         msg = self.lib.orc_last_error().decode() if st else ""
         return SolveResult(st, hist[: hl.value].tolist(), it.value, bool(cv.value), 0.0, msg)
 
+    def start_vector(self, spec: CycleSpec, kind, b):
+        """make_start_vector (study.cpp:40-79); kind "zero" or "nested"."""
+        x = np.zeros(self.n(self.levels))
+        cs = spec.to_c()
+        self.lib_call("start_vector", C.byref(cs), START_KINDS.index(kind),
+                      _ptr(np.ascontiguousarray(b, np.float64)), _ptr(x))
+        return x
+
     @classmethod
     def random_vector(cls, n, seed):
         v = np.zeros(n)
@@ -351,6 +360,17 @@ class Reference(_Backend):
                                 _ptr(wall), err, 256)
         return SolveResult(st, hist[: hl.value].tolist(), it.value, bool(cv.value), float(wall[0]),
                            err.value.decode())
+
+    def start_vector(self, spec: CycleSpec, kind, b):
+        """gmg::make_start_vector (study.cpp:40-79); kind "zero" or "nested"."""
+        x = np.zeros(self.n(self.levels))
+        cs = spec.to_c()
+        err = C.create_string_buffer(256)
+        st = self.lib.ref_start_vector(self.handle, C.byref(cs), START_KINDS.index(kind),
+                                       _ptr(np.ascontiguousarray(b, np.float64)), _ptr(x), err, 256)
+        if st:
+            raise CheckerError(st, err.value.decode())
+        return x
 
     @classmethod
     def random_vector(cls, n, seed):

@@ -250,14 +250,15 @@ int ref_solve(void* h, const ref_cycle* spec, const double* b, double* x, double
     return st;
 }
 
-// Start vector per gmg::make_start_vector (kind 0 zero, 1 nested).
-int ref_start_vector(void* h, const ref_cycle* spec, int kind, const double* b, double* x) {
-    auto* p = static_cast<RefProblem*>(h);
-    const auto& g = p->prob->grid(p->prob->num_levels());
-    gmg::StartVectorStrategy strat;
-    strat.kind = static_cast<gmg::StartVectorKind>(kind);
-    out(gmg::make_start_vector(strat, *p->prob, to_spec(spec), wrap(g, b)), x);
-    return 0;
+// Start vector per gmg::make_start_vector (kind 0 zero, 1 nested), study.cpp:40-79.
+int ref_start_vector(void* h, const ref_cycle* spec, int kind, const double* b, double* x, char* err, int len) {
+    return guarded(Err{err, len}, [&] {
+        auto* p = static_cast<RefProblem*>(h);
+        const auto& g = p->prob->grid(p->prob->num_levels());
+        gmg::StartVectorStrategy strat;
+        strat.kind = static_cast<gmg::StartVectorKind>(kind);
+        out(gmg::make_start_vector(strat, *p->prob, to_spec(spec), wrap(g, b)), x);
+    });
 }
 
 // std::mt19937(seed) + uniform_real_distribution<double>(-1, 1), the recipe of

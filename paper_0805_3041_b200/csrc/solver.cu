@@ -2205,6 +2205,50 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
     });
 }
 
+int gmg_dev_make_start_vector(gmg_problem* p, const gmg_cycle_desc* spec, int kind, const double* b, double* x) {
+    return guarded([&] {
+        checked(p);
+        single(p, "make_start_vector");
+        std::lock_guard<std::mutex> lk(p->mu);
+        const int L = p->L;
+        Lev& F = p->lev(L);
+        if (kind == 0) {  // StartVectorKind::zero
+            std::memset(x, 0, (size_t)F.n() * sizeof(double));
+            return;
+        }
+        if (kind != 1) throw std::invalid_argument("start: kind must be zero or nested");
+        // nested (study.cpp:46-58): rhs[L] = b, rhs[l-1] = R rhs[l] (the DCAS buffers)
+        upload(p, F, F.buf[DCAS], b, cudaMemcpyHostToDevice);
+        int cur = U0;
+        if (L == 1) {
+            launch_coarse(p, F.buf[DCAS], F.buf[U0]);
+        } else {
+            for (int l = L; l >= 2; --l) launch_restrict(p, l, p->lev(l).buf[DCAS], p->lev(l - 1).buf[DCAS]);
+            check_smoother(*spec);
+            const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
+            if (!(spec->smoothing_omega > 0.0)) throw std::invalid_argument("omega: damping must be > 0");
+            // u = coarse_solver().solve(rhs[1]); per level u = smooth_step(P u, rhs[l])
+            launch_coarse(p, p->lev(1).buf[DCAS], p->lev(1).buf[U0]);
+            for (int l = 2; l <= L; ++l) {
+                Lev& Lv = p->lev(l);
+                SmoothSrc s;
+                s.kind = S_PROLONG;
+                s.uc = p->lev(l - 1).buf[cur];
+                if (spec->smoother_kind == GMG_SMOOTHER_JACOBI) {
+                    launch_smooth(p, Lv, 1, s, Lv.buf[DCAS], Lv.buf[U0], spec->smoothing_omega);
+                    cur = U0;
+                } else {
+                    const double* r = pc_steps(p, Lv, 1, s, Lv.buf[DCAS], Lv.buf[U0], Lv.buf[U1], *spec,
+                                               sm ? &sm->lev[l - 1] : nullptr);
+                    cur = r == Lv.buf[U0] ? U0 : U1;
+                }
+            }
+        }
+        download(p, F, x, F.buf[cur], cudaMemcpyDeviceToHost);
+        CK(cudaStreamSynchronize(p->st));
+    });
+}
+
 int gmg_dev_apply(gmg_problem* p, int level, const double* x, double* y) {
     return guarded([&] {
         checked(p);

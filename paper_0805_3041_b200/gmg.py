@@ -53,7 +53,9 @@ EXPORTS = [
     "gmg_dev_time_smoother", "gmg_dev_cycle_kernel_count", "gmg_dev_seqsum_stats", "gmg_host_problem_create",
     "gmg_host_random_vector", "gmg_host_seqsum_emulate", "gmg_dev_problem_create_slabs", "gmg_dist_unique_id",
     "gmg_dev_dist_info", "gmg_dev_level_window", "gmg_host_problem_create_slabs", "gmg_host_slab_plan",
+    "gmg_dev_make_start_vector",
 ]
+START_KINDS = ["zero", "nested", "continuation"]  # gmg::StartVectorKind (config.hpp:11)
 
 
 class GmgError(Exception):
@@ -145,6 +147,7 @@ def lib() -> C.CDLL:
                                            C.POINTER(_Report)]
         L.gmg_dev_mg_cycle.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, _dp, _dp, _dp]
         L.gmg_dev_apply.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+        L.gmg_dev_make_start_vector.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, _dp, _dp]
         L.gmg_dev_residual.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp]
         L.gmg_dev_smooth_step.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp, _dp]
         L.gmg_dev_restriction.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
@@ -385,6 +388,28 @@ def mg_cycle(prob: MultilevelProblem, level: int, u0, g, spec: CycleSpec) -> np.
     u = np.zeros(prob.n(level))
     _check(lib().gmg_dev_mg_cycle(prob._h, C.byref(spec._c()), level, _p(u0), _p(g), _p(u)))
     return u
+
+
+def make_start_vector(kind: str, prob: MultilevelProblem, spec: CycleSpec, b, source=None) -> np.ndarray:
+    """gmg::make_start_vector (study.hpp:20-21, study.cpp:40-79) on the device: "zero",
+    "nested" (level-1 solve of the restricted b, then prolongation + one smooth_step of
+    spec's smoother per level) or "continuation" (a copy of `source`, the solution of
+    a related problem with the same finest shape)."""
+    L = prob.num_levels
+    n = prob.n(L)
+    if kind == "continuation":
+        if source is None:
+            raise InvalidArgument("start: continuation requires a source solution")
+        src = _arr(source)
+        if src.size != n:
+            raise InvalidArgument("start: continuation source shape does not match")
+        return src.copy()
+    if kind not in START_KINDS:
+        raise InvalidArgument(f"start: unknown start vector '{kind}'")
+    b = _arr(b, n)
+    x = np.zeros(n)
+    _check(lib().gmg_dev_make_start_vector(prob._h, C.byref(spec._c()), START_KINDS.index(kind), _p(b), _p(x)))
+    return x
 
 
 def apply(prob: MultilevelProblem, level: int, x) -> np.ndarray:

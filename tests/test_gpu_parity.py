@@ -295,3 +295,18 @@ def test_c4_full_size_history(gpu):
     assert bits_equal(rep.residual_history, unhex(g["history"])), \
         first_mismatch(rep.residual_history, unhex(g["history"]))
     assert bits_equal(x[:8], unhex(g["x_head"])) and bits_equal(x[-8:], unhex(g["x_tail"]))
+    import hashlib
+    assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == g["x_sha256"]
+
+
+@pytest.mark.slow
+def test_c5_full_size_ten_cycles(gpu):
+    """BASELINE configs[4] exactly: 10 F-cycles (tol=1e-30, max_cycles=10, the reference's
+    fixed-budget idiom): all 11 residuals and the final solution, bit for bit."""
+    g, d, b, x, spec = run_fixture("c5_10cycle")
+    rep = gmg.solve(d, b, spec, x)
+    assert rep.iterations == g["iterations"] == 10
+    assert bits_equal(rep.residual_history, unhex(g["history"])), \
+        first_mismatch(rep.residual_history, unhex(g["history"]))
+    import hashlib
+    assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == g["x_sha256"]

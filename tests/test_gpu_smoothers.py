@@ -129,3 +129,25 @@ def test_line_smoother_omega_range_is_checked(problems):
             gmg.solve(d, np.ones(n), gmg.CycleSpec(smoother=kind, smoother_omega=1.5), np.zeros(n))
     with pytest.raises(gmg.InvalidArgument, match="must be > 0"):
         gmg.solve(d, np.ones(n), gmg.CycleSpec(smoother="ilu0", smoother_omega=0.0), np.zeros(n))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["adi", "gsadi", "ilu0"])
+def test_solve_1023_line_and_ilu_bitexact(gpu, kind):
+    """C2/C3'-size grids (1023^2, 10 levels): whole-grid wavefront (ilu0) and per-line
+    (adi) / serial-chain (gsadi) kernels at full size, 3 F-cycles from a random start,
+    anisotropic eps = 1e-2 (the paper's line-smoother case): histories and solution
+    bit for bit against the oracle."""
+    a = (10, 1, 1, (1.0, 1.0), "cartesian", 1e-2, 1.0)
+    d, o = gmg.MultilevelProblem(*a), Oracle(*a)
+    n = d.n(10)
+    b = Oracle.random_vector(n, 1)
+    x0 = Oracle.random_vector(n, 2)
+    kw = dict(cycle="F", smoother=kind, smoother_omega=1.0 if kind != "ilu0" else 1.1, pre_steps=2,
+              post_steps=2, tolerance=1e-30, max_cycles=3)
+    xg, xo = x0.copy(), x0.copy()
+    rg = gmg.solve(d, b, gmg.CycleSpec(**kw), xg)
+    ro = o.solve(OSpec(**kw), b, xo)
+    assert rg.iterations == ro.iterations == 3
+    assert bits_equal(np.asarray(rg.residual_history), np.asarray(ro.history)), kind
+    assert bits_equal(xg, xo), (kind, first_mismatch(xg, xo))

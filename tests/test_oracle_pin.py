@@ -118,3 +118,36 @@ def test_oracle_errors_match_reference():
         rr = r.solve(spec, b, np.zeros(o.n(3)))
         assert ro.status == rr.status != 0
         assert ro.message == rr.message
+
+
+def test_oracle_start_vector_matches_reference_golden():
+    """make_start_vector nested (study.cpp:46-58) for 6 smoothers / 3 coordinate systems."""
+    g = load_golden("start_vectors")
+    for case in g["cases"]:
+        o = make(case["problem"])
+        b = Oracle.random_vector(o.n(case["problem"]["levels"]), case["b_seed"])
+        got = o.start_vector(CycleSpec(**case["spec"]), "nested", b)
+        assert bits_equal(got, unhex(case["nested"])), (case["spec"]["smoother"], first_mismatch(got, unhex(case["nested"])))
+
+
+@needs_ref
+@pytest.mark.parametrize("coords", ["cartesian", "cylindrical", "spherical"])
+def test_oracle_start_vector_vs_reference(coords):
+    for levels, cn, sm, som in [(6, (1, 1), "jacobi", 1.0), (5, (2, 1), "sor", 1.2), (4, (1, 3), "tri_y", 0.8),
+                                (4, (1, 1), "gstri_x", 1.0), (1, (3, 3), "jacobi", 1.0)]:
+        o = Oracle(levels, cn[0], cn[1], (1.0, 1.0), coords, 0.05, 1.0)
+        r = Reference(levels, cn[0], cn[1], (1.0, 1.0), coords, 0.05, 1.0)
+        b = Oracle.random_vector(o.n(levels), 11)
+        spec = CycleSpec(smoother=sm, smoother_omega=som, smoothing_omega=0.6)
+        for kind in ("zero", "nested"):
+            assert bits_equal(o.start_vector(spec, kind, b), r.start_vector(spec, kind, b)), (levels, sm, kind)
+    # the reference's errors: damping checked by smooth_step, smoother omega by setup
+    o = Oracle(3)
+    r = Reference(3)
+    b = Oracle.random_vector(o.n(3), 1)
+    for spec in (CycleSpec(smoother="jacobi", smoothing_omega=0.0), CycleSpec(smoother="sor", smoother_omega=2.5)):
+        with pytest.raises(Exception) as eo:
+            o.start_vector(spec, "nested", b)
+        with pytest.raises(Exception) as er:
+            r.start_vector(spec, "nested", b)
+        assert eo.value.code == er.value.code == 2 and eo.value.msg == er.value.msg
