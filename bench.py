@@ -26,7 +26,17 @@ Multi-GPU (N>1 via torchrun): by default the one grid is split into row slabs
 over the ranks, halos and the rank-ordered exact reductions go over NCCL, the
 coarse levels are replicated. Strong scaling; value = the grid's DOF*cycles/s.
 --parallel replicas runs one independent copy of the workload per rank (weak).
-Timing = max over ranks either way.
+Timing = max over ranks either way. `--gpus N` without torchrun re-launches this
+script under torch.distributed.run with N ranks (127.0.0.1); under torchrun it
+must agree with WORLD_SIZE. NCCL logs its communicator setup (NCCL_DEBUG=INFO,
+subsystem INIT) to stderr.
+per_level: one extra cycle with CUDA events around every launch
+         (gmg_dev_profile_cycle): GB/s and HBM fraction per kernel family and
+         level from §8d's algorithmic bytes; levels whose per-launch traffic fits
+         in L2 are flagged l2_resident (their GB/s is not an HBM number).
+c5     : BASELINE config 5 (16383^2, 14 levels, eps=1e-2, 3+3, random f and x0,
+         exactly 10 F-cycles) device-resident on the same GPU, with its own
+         per-level table (--no-c5 skips it).
 """
 from __future__ import annotations
 
@@ -55,6 +65,52 @@ WORKLOADS = {
     "C1": dict(levels=7, alpha=1.0, beta=1.0, pre=2, post=2, tol=1e-8, seed_x=0,
                desc="127^2 interior (129^2 vertices), 7 levels, isotropic Poisson, jacobi 0.7 2+2"),
 }
+
+
+def common_config(wl, n):
+    """The config both arms report (identical keys and values)."""
+    w = WORKLOADS[wl]
+    return {"workload": f"{wl}: {w['desc']}", "dof": n, "reduction": "exact",
+            "l2": "inputs larger than L2 (537 MB per vector at C4, 2.1 GB at C5, vs 126 MB L2); no flush"}
+
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0))}
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args):
+    """--gpus N (N > 1) outside torchrun: re-run this script as N ranks under
+    torch.distributed.run on 127.0.0.1 and exit with its status."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None:
+        if args.gpus is not None and int(ws_env) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} disagrees with WORLD_SIZE={ws_env}")
+        return
+    if args.gpus is None or args.gpus <= 1 or args.impl == "reference":
+        return
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd, env=env).returncode)
 
 
 def load_peaks():
@@ -157,9 +213,15 @@ def cpu_reference_fcycle(wl, threads=1, cycles=1, seconds_cap=None):
                               post_steps=w["post"], tolerance=1e-300, max_cycles=cycles)
     xs = [np.zeros(n) if not w["seed_x"] else B.random_vector(n, w["seed_x"]) for _ in range(threads)]
     res = [None] * threads
+    cpus = sorted(os.sched_getaffinity(0))
 
     def run(q):
-        res[q] = prob.solve(spec, b, xs[q])
+        # pin this solve's thread to one core (sched_setaffinity(0) is per thread on Linux)
+        os.sched_setaffinity(0, {cpus[q % len(cpus)]})
+        try:
+            res[q] = prob.solve(spec, b, xs[q])
+        finally:
+            os.sched_setaffinity(0, cpus)
 
     ts = time.time()
     th = [threading.Thread(target=run, args=(q,)) for q in range(threads)]
@@ -168,7 +230,8 @@ def cpu_reference_fcycle(wl, threads=1, cycles=1, seconds_cap=None):
     for t in th:
         t.join()
     dt = time.time() - ts
-    return threads * n * cycles / dt, dict(kind=kind, setup_s=round(setup, 2), seconds=round(dt, 2), n=n)
+    return threads * n * cycles / dt, dict(kind=kind, setup_s=round(setup, 2), seconds=round(dt, 2), n=n,
+                                           pinned_cpus=[cpus[q % len(cpus)] for q in range(threads)])
 
 
 def usable_threads(n_dof):
@@ -223,12 +286,13 @@ def run_reference_arm(args):
     value = P * n * steps / total
     line = {
         "impl": "reference", "metric": "fine-grid DOF*F-cycles/s (fp64)", "value": value,
-        "unit": "DOF*cycles/s", "n_gpus": ws, "steps": steps, "warmup": warmup,
+        "unit": "DOF*cycles/s", "n_gpus": ws if ws > 1 else (args.gpus or 1), "steps": steps, "warmup": warmup,
         "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": 1e3 * total / steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1] rhs, std::mt19937)",
-        "config": {"workload": f"{wl}: {w['desc']}", "dof": n},
-        "cpu_baseline": {"value": value, "unit": "DOF*cycles/s", "cores": P, "kind": kind,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U[-1,1] rhs from std::mt19937, as the reference tests)",
+        "config": common_config(wl, n),
+        "parallelism": f"{P} independent reference solves in parallel host threads",
+        "cpu_baseline": {"value": value, "unit": "DOF*cycles/s", "cores": P, "kind": kind, "host": host_info(),
                          "sample": f"each step = 1 F-cycle (gmg::solve, max_cycles=1, incl. its r0/|b| norms) "
                                    f"of {wl} on each of {P} independent solves in parallel threads"},
         "e2e": {"value": value, "unit": "DOF*cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -236,10 +300,73 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def per_level_table(prof, peak, l2_bytes):
+    """Aggregate gmg.profile_cycle entries per (kernel family, level)."""
+    rows = {}
+    for e in prof:
+        k = (e["kernel"], e["level"])
+        r = rows.setdefault(k, dict(kernel=e["kernel"], level=e["level"], launches=0, ms=0.0, bytes=0.0,
+                                    max_launch_bytes=0.0))
+        r["launches"] += 1
+        r["ms"] += e["ms"]
+        r["bytes"] += e["bytes"]
+        r["max_launch_bytes"] = max(r["max_launch_bytes"], e["bytes"])
+    out = []
+    for (kern, lev), r in sorted(rows.items(), key=lambda kv: (-kv[0][1], kv[0][0])):
+        gbs = r["bytes"] / (r["ms"] / 1e3) / 1e9 if r["ms"] > 0 and r["bytes"] > 0 else None
+        out.append({"kernel": kern, "level": lev, "launches": r["launches"], "ms": round(r["ms"], 4),
+                    "GBps": None if gbs is None else round(gbs, 1),
+                    "frac": None if gbs is None else round(gbs / peak, 3),
+                    "l2_resident": bool(0 < r["max_launch_bytes"] <= l2_bytes)})
+    total = sum(e["ms"] for e in prof)
+    return {"entries": out, "profiled_ms_per_cycle": round(total, 4),
+            "how": "one cycle outside the graph, CUDA events around every launch on the solver stream; bytes = "
+                   "SURVEY.md 8(d) algorithmic bytes per DOF x level DOFs; ss_* chains carry no streamed bytes"}
+
+
+def run_c5(gmg, torch, peak, l2_bytes, reduction):
+    """BASELINE config 5 exactly: 10 F-cycles device-resident, plus its per-level table."""
+    w = WORKLOADS["C5"]
+    t0 = time.time()
+    prob = gmg.MultilevelProblem(w["levels"], 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+    n = prob.n(w["levels"])
+    b = torch.from_numpy(gmg.random_vector(n, 1)).cuda()
+    x0 = gmg.random_vector(n, w["seed_x"])
+    x = torch.from_numpy(x0).cuda()
+    setup = time.time() - t0
+    kw = dict(smoother="jacobi", smoother_omega=1.0, smoothing_omega=0.7, pre_steps=w["pre"], post_steps=w["post"],
+              cycle="F", adaptive_correction=True, reduction=reduction)
+    gmg.solve_device(prob, b.data_ptr(), x.data_ptr(), gmg.CycleSpec(tolerance=1e-30, max_cycles=2, **kw))  # warm
+    x.copy_(torch.from_numpy(x0))
+    spec = gmg.CycleSpec(tolerance=1e-30, max_cycles=10, **kw)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    rep = gmg.solve_device(prob, b.data_ptr(), x.data_ptr(), spec)
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    table = per_level_table(gmg.profile_cycle(prob, spec), peak, l2_bytes)
+    out = {"config": "C5: " + w["desc"] + ", exactly 10 F-cycles (tol 1e-30, max_cycles 10)", "dof": n,
+           "cycles": rep.iterations, "ms_per_cycle": ms / rep.iterations,
+           "value": n * rep.iterations / (ms / 1e3), "unit": "DOF*cycles/s",
+           "residual_first_last": [rep.residual_history[0], rep.residual_history[-1]],
+           "host_setup_s": round(setup, 1), "per_level": table,
+           "timing": "one gmg_dev_solve_devptr call of 10 cycles, CUDA events on the solver stream (incl. r0 and "
+                     "|b| norms)"}
+    prob.close()
+    del b, x
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
     if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -256,7 +383,8 @@ def run_ours(args):
         torch.distributed.broadcast_object_list(ids, src=0)
         prob = gmg.MultilevelProblem(*pargs, device=local,
                                      slabs=gmg.Slabs(world=ws, rank=rank, min_rows=255, nccl_id=ids[0]))
-        single = gmg.MultilevelProblem(*pargs, device=local)  # for the single-kernel roofline timing
+        # rank 0 also keeps an unsharded copy for the single-kernel roofline and per-level legs
+        single = gmg.MultilevelProblem(*pargs, device=local) if rank == 0 else None
     else:
         prob = gmg.MultilevelProblem(*pargs, device=local)
         single = prob
@@ -278,7 +406,6 @@ def run_ours(args):
                      gmg.CycleSpec(tolerance=1e-300, max_cycles=max(1, args.warmup), **spec_kw))
     x_dev.copy_(torch.from_numpy(x0_host))
     spec = gmg.CycleSpec(tolerance=1e-300, max_cycles=args.steps, **spec_kw)
-    per_cycle = gmg.cycle_kernel_count(single, spec)
 
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -296,18 +423,35 @@ def run_ours(args):
     jobs = 1 if sharded else ws  # grids solved by the whole job
     value = jobs * n * args.steps / (ms_max / 1e3)
 
-    # roofline: the finest post-smoother, timed live (CUDA events on the solver stream)
     peak, peak_src = load_peaks()
-    ms_k, bytes_k = gmg.time_smoother(single, spec, variant=1, reps=20)
-    achieved = bytes_k / (ms_k / 1e3) / 1e9
-    ms_pre, bytes_pre = gmg.time_smoother(single, spec, variant=0, reps=20)
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
-        try:
-            traffic = json.load(open(tfile)).get(f"{wl}/post_smoother")
-        except Exception:
-            traffic = None
+    l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
+    roof, per_level, per_cycle = None, None, None
+    if rank == 0:
+        # roofline: the finest post-smoother, timed live (CUDA events on the solver stream)
+        ms_k, bytes_k = gmg.time_smoother(single, spec, variant=1, reps=20)
+        achieved = bytes_k / (ms_k / 1e3) / 1e9
+        ms_pre, bytes_pre = gmg.time_smoother(single, spec, variant=0, reps=20)
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tfile):
+            try:
+                traffic = json.load(open(tfile)).get(f"{wl}/post_smoother")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "traffic_source": "profile constant: dram__bytes_read.sum + dram__bytes_write.sum of this kernel "
+                                  "from the committed ncu --set full capture (profiles/traffic.json); not measured "
+                                  "in this run",
+                "kernel": "k_smooth4<2,CORRECT> finest post-smoother (u+omega*P uc, 2 Jacobi steps fused)",
+                "bytes_per_launch": bytes_k, "ms_per_launch": ms_k, "peak_source": peak_src,
+                "pre_smoother_GBps": bytes_pre / (ms_pre / 1e3) / 1e9}
+        per_cycle = gmg.cycle_kernel_count(single, spec)
+        if ws == 1 and not args.no_per_level:
+            x_dev.copy_(torch.from_numpy(x0_host))
+            per_level = per_level_table(gmg.profile_cycle(single, spec), peak, l2_bytes)
+    if ws > 1:
+        barrier()
 
     # e2e: public C-ABI solve with pinned host buffers, to the reference tolerance
     pin_b = torch.from_numpy(b_host).pin_memory()
@@ -329,39 +473,54 @@ def run_ours(args):
     if ws > 1:
         torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
     e2e_value = jobs * n * e2e_cycles / float(et.item())
+    # the drop-in C++ shim passes pageable std::vector memory: the same call on pageable buffers
+    e2e_pageable = None
+    if rank == 0 and ws == 1:
+        xp = x0_host.copy()
+        t0 = time.perf_counter()
+        r = gmg.solve(prob, b_host, e2e_spec, xp)
+        e2e_pageable = n * r.iterations / (time.perf_counter() - t0)
+    del pin_b, pin_x
+
+    c5 = None
+    if rank == 0 and ws == 1 and wl == "C4" and not args.no_c5:
+        if single is not prob:
+            single.close()
+        c5 = run_c5(gmg, torch, peak, l2_bytes, args.reduction)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_fcycle(wl, threads=1, cycles=1)
-        cpu = {"value": v, "unit": "DOF*cycles/s", "cores": 1, "kind": info["kind"],
-               "sample": f"1 F-cycle of {wl} (gmg::solve max_cycles=1 incl. r0/|b| norms) on 1 host core; "
-                         f"{info['seconds']} s timed, setup {info['setup_s']} s excluded"}
+        cpu = {"value": v, "unit": "DOF*cycles/s", "cores": 1, "kind": info["kind"], "host": host_info(),
+               "pinned_cpu": info["pinned_cpus"][0],
+               "sample": f"1 F-cycle of {wl} (gmg::solve max_cycles=1 incl. r0/|b| norms) on 1 host core "
+                         f"(thread pinned with sched_setaffinity); {info['seconds']} s timed, setup "
+                         f"{info['setup_s']} s excluded"}
 
     if rank == 0:
         hist = rep.residual_history
+        info = prob.dist_info()
         line = {
             "metric": "fine-grid DOF*F-cycles/s (fp64)", "value": value, "unit": "DOF*cycles/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded U[-1,1] rhs from std::mt19937, as the reference tests)",
-            "config": {"workload": f"{wl}: {w['desc']}", "dof": n, "cycles_timed": args.steps,
-                       "l2": "inputs larger than L2 (537 MB per vector at C4 vs 126 MB L2); no flush",
-                       "reduction": args.reduction,
-                       "parallelism": (f"row slabs over {ws} GPUs (levels >= {prob.dist_info()[2]} sharded, "
-                                       f"NCCL halos + rank-ordered exact reductions)") if sharded
-                       else ("replicas" if ws > 1 else "single GPU"),
-                       "residual_first_last": [hist[0], hist[-1]]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_smooth4<2,CORRECT> finest post-smoother (u+omega*P uc, 2 Jacobi steps fused)",
-                         "bytes_per_launch": bytes_k, "ms_per_launch": ms_k, "peak_source": peak_src,
-                         "pre_smoother_GBps": bytes_pre / (ms_pre / 1e3) / 1e9},
+            "config": common_config(wl, n),
+            "parallelism": (f"row slabs over {ws} GPUs (levels >= {info[2]} sharded, NCCL halos + rank-ordered "
+                            f"exact reductions; NCCL communicator of {info[1]} ranks)") if sharded
+            else ("replicas" if ws > 1 else "single GPU"),
+            "cycles_timed": args.steps, "residual_first_last": [hist[0], hist[-1]],
+            "roofline": roof,
+            "per_level": per_level,
+            "c5": c5,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "DOF*cycles/s", "h2d_bytes_per_step": 2 * n * 8,
                     "d2h_bytes_per_step": n * 8 + 8 * 51, "cycles_per_step": e2e_cycles / e2e_steps,
-                    "note": "gmg_dev_solve on pinned host buffers to the reference tolerance"},
-            "gpu_launches": per_cycle * args.steps + 9,
+                    "pageable_value": e2e_pageable,
+                    "note": "gmg_dev_solve on pinned host buffers to the reference tolerance (pageable_value: the "
+                            "same call on pageable numpy buffers, as the C++ shim passes std::vector memory)"},
+            "gpu_launches": (per_cycle or 0) * args.steps + 9,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -371,7 +530,7 @@ def run_ours(args):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -381,7 +540,10 @@ def main():
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--parallel", choices=["slabs", "replicas"], default="slabs")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (config 5) sub-measurement")
+    ap.add_argument("--no-per-level", action="store_true")
     args = ap.parse_args()
+    maybe_spawn(args)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

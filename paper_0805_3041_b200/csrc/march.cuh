@@ -34,6 +34,7 @@ namespace gmg_dev {
 // rows ahead of the arithmetic.
 
 struct SrcZero {  // u0 = 0 (inner V-cycle visits, cycle.cpp:89)
+    static constexpr double kReads = 0;  // fine-level arrays read per DOF (coarse = 1/4)
     struct Raw {};
     __device__ __forceinline__ void prepare(int) {}
     __device__ __forceinline__ Raw fetch(int, int) const { return Raw{}; }
@@ -41,6 +42,7 @@ struct SrcZero {  // u0 = 0 (inner V-cycle visits, cycle.cpp:89)
 };
 
 struct SrcU {  // u0 = u
+    static constexpr double kReads = 1;  // fine-level arrays read per DOF (coarse = 1/4)
     const double* u;
     Grid g;
     struct Raw {
@@ -54,6 +56,7 @@ struct SrcU {  // u0 = u
 };
 
 struct SrcSum {  // x + e: fcycle_pass's out = x; axpy(1.0, e, out) (cycle.cpp:139-140)
+    static constexpr double kReads = 2;  // fine-level arrays read per DOF (coarse = 1/4)
     const double *x, *e;
     Grid g;
     struct Raw {
@@ -102,6 +105,7 @@ __device__ __forceinline__ double prolong_make(const ProlongRaw& r, int i, int j
 }
 
 struct SrcProlong {  // u0 = P e (fcycle_pass, cycle.cpp:135)
+    static constexpr double kReads = 0.25;  // fine-level arrays read per DOF (coarse = 1/4)
     Prolong P;
     int fnx, fny;
     double tX;
@@ -136,6 +140,7 @@ struct OmegaSrc {
 };
 
 struct SrcCorrect {  // u + omega * P uc  (axpy(wl, corr, u), cycle.cpp:93-96)
+    static constexpr double kReads = 1.25;  // fine-level arrays read per DOF (coarse = 1/4)
     const double* u;
     Grid g;
     Prolong P;

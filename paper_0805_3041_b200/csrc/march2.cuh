@@ -23,6 +23,8 @@ __device__ __forceinline__ double2 ld_pair(const double* a, const Grid& g, int i
 }
 
 struct Src2Zero {
+    static constexpr const char* kProfName = "smooth(from 0)";
+    static constexpr double kBytesPerDof = 16.0;
     struct Raw {};
     __device__ __forceinline__ void prepare(int) {}
     __device__ __forceinline__ Raw fetch(int, int) const { return Raw{}; }
@@ -30,6 +32,8 @@ struct Src2Zero {
 };
 
 struct Src2U {
+    static constexpr const char* kProfName = "smooth(from u)";
+    static constexpr double kBytesPerDof = 24.0;
     const double* u;
     Grid g;
     struct Raw {
@@ -78,6 +82,8 @@ __device__ __forceinline__ double2 prolong2_make(const Pair2Raw& r, int i, int j
 }
 
 struct Src2Prolong {
+    static constexpr const char* kProfName = "smooth(from P e)";
+    static constexpr double kBytesPerDof = 18.0;
     Prolong P;
     int fnx, fny;
     double tX;
@@ -90,6 +96,8 @@ struct Src2Prolong {
 };
 
 struct Src2Correct {  // u + omega * P uc (axpy(wl, corr, u), cycle.cpp:93-96)
+    static constexpr const char* kProfName = "smooth(u + w P uc)";
+    static constexpr double kBytesPerDof = 26.0;
     const double* u;
     Grid g;
     Prolong P;

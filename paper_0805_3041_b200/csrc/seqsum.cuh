@@ -1031,6 +1031,8 @@ __device__ __forceinline__ int row_of(long long k, int nx, double inv_nx) {
 
 struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid function
     static constexpr int NS = 1;
+    static constexpr const char* kProfName = "ss_walk(norm)";
+    static constexpr double kBytesPerTerm = 8.0;  // algorithmic bytes read per term (all sums)
     const double* r;
     Grid g;
     double inv_nx;
@@ -1060,6 +1062,8 @@ struct NormTerms {  // r_k * r_k (norm_l2, stencil.cpp:9-13) on a pitched grid f
 
 struct DotTerms {  // a_k * b_k (dot, stencil.cpp:21-26) on flat arrays
     static constexpr int NS = 1;
+    static constexpr const char* kProfName = "ss_walk(dot)";
+    static constexpr double kBytesPerTerm = 16.0;  // algorithmic bytes read per term (all sums)
     const double *a, *b;
     __device__ __forceinline__ double term(int, long long k) const { return __ldg(a + k) * __ldg(b + k); }
     GMG_SS_STRIPED_DEFAULT
@@ -1067,6 +1071,8 @@ struct DotTerms {  // a_k * b_k (dot, stencil.cpp:21-26) on flat arrays
 
 struct FlatNormTerms {  // v_k * v_k on a flat array
     static constexpr int NS = 1;
+    static constexpr const char* kProfName = "ss_walk(norm)";
+    static constexpr double kBytesPerTerm = 8.0;  // algorithmic bytes read per term (all sums)
     const double* a;
     __device__ __forceinline__ double term(int, long long k) const {
         const double v = __ldg(a + k);
@@ -1077,6 +1083,8 @@ struct FlatNormTerms {  // v_k * v_k on a flat array
 
 struct ArrTerms {  // materialised terms: sum s reads t[s][k]
     static constexpr int NS = 2;
+    static constexpr const char* kProfName = "ss_walk(omega dots)";
+    static constexpr double kBytesPerTerm = 16.0;  // algorithmic bytes read per term (all sums)
     const double* t0;
     const double* t1;
     __device__ __forceinline__ double term(int s, long long k) const { return __ldg((s ? t1 : t0) + k); }

@@ -77,8 +77,41 @@ inline void dbg_sync(int line) {
 // cycle graph as programmatic edges, so each launch overlaps its predecessor's
 // tail. GMG_NO_PDL=1 launches plainly (A/B).
 static const bool g_pdl = getenv("GMG_NO_PDL") == nullptr;
+
+// Per-launch profile of one cycle run outside the graph (gmg_dev_profile_cycle):
+// the launch helpers tag each launch with its kernel, level and algorithmic
+// bytes (SURVEY.md §8d per-kernel bytes x the DOFs it covers); launch_k brackets
+// it with events on the launching stream.
+struct ProfEntry {
+    std::string kernel;
+    int level;
+    double bytes;
+    cudaEvent_t e0, e1;
+};
+thread_local std::vector<ProfEntry>* g_prof = nullptr;
+thread_local std::string g_prof_kernel;
+thread_local int g_prof_level = 0;
+thread_local double g_prof_bytes = 0.0;
+thread_local int g_cur_level = 0;  // level of the sums the driver is about to launch
+inline void prof_tag(const char* kernel, int level, double bytes) {
+    if (!g_prof) return;
+    g_prof_kernel = kernel;
+    g_prof_level = level;
+    g_prof_bytes = bytes;
+}
+
 template <typename... KArgs, typename... Args>
 void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    if (g_prof) {
+        ProfEntry e{g_prof_kernel.empty() ? std::string("other") : g_prof_kernel, g_prof_level, g_prof_bytes,
+                    nullptr, nullptr};
+        g_prof_kernel.clear();
+        g_prof_bytes = 0.0;
+        CK(cudaEventCreate(&e.e0));
+        CK(cudaEventCreate(&e.e1));
+        CK(cudaEventRecord(e.e0, st));
+        g_prof->push_back(e);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -90,6 +123,7 @@ void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
     cfg.attrs = at;
     cfg.numAttrs = g_pdl ? 1 : 0;
     CK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(std::forward<Args>(args))...));
+    if (g_prof) CK(cudaEventRecord(g_prof->back().e1, st));
 }
 
 template <class F>
@@ -478,11 +512,13 @@ void seqsum_walk(gmg_problem* p, const TG& tg, long long n, const double* pre0, 
         for (int s = 0; s < NS; ++s)
             CK(cudaMemsetAsync(sp.s[s].ticket, 0, (2 + 2 * (size_t)p->nch_max) * sizeof(int), p->st));
     p->ss_clean = fused_out != nullptr;
+    prof_tag(TG::kProfName, g_cur_level, (double)n * TG::kBytesPerTerm);
     if (small)
         launch_k(k_ss_walk<TG, kSsEPTs>, dim3(nch, NS), kSsWT, ss_walk_smem<kSsEPTs>(), p->st, tg, n, nch, sp, pre0);
     else
         launch_k(k_ss_walk<TG, kSsEPT>, dim3(nch, NS), kSsWT, ss_walk_smem<kSsEPT>(), p->st, tg, n, nch, sp, pre0);
     const dim3 sg((nch + kSsScanB - 1) / kSsScanB, NS);
+    prof_tag(fused_out ? "ss_scan_chain" : "ss_scan", g_cur_level, 0.0);
     if (fused_out)
         launch_k(k_ss_scan_chain<TG>, sg, kSsScanB, ss_chain_smem(), p->st, tg, n, sp, nch, fused_out, fused_start);
     else
@@ -502,12 +538,14 @@ void seqsum_chain(gmg_problem* p, const TG& tg, long long n, double* out, const 
         return;
     }
     if (n <= kSsDirect) {
+        prof_tag("ss_direct", g_cur_level, (double)n * TG::kBytesPerTerm);
         launch_k(k_ss_direct<TG>, NS, 256, n * sizeof(double), p->st, tg, (int)n, out, start);
         KCHECK();
         return;
     }
     const int nch = (int)((n + kSsC - 1) / kSsC);
     const SsPair sp = ss_state(p, nch);
+    prof_tag("ss_chain", g_cur_level, 0.0);
     launch_k(k_ss_chain<TG>, NS, kSsT, ss_chain_smem(), p->st, tg, n, sp, out, start);
     KCHECK();
 }
@@ -575,6 +613,7 @@ void launch_smooth2_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& sr
     constexpr int PF = sizeof(typename Src::Raw) > 32 ? 2 : 3;
     const int seg = seg_rows(L.nx, L.rows());
     dim3 grid((L.nx + OUTW - 1) / OUTW, (L.rows() + seg - 1) / seg);
+    prof_tag(Src::kProfName, L.l, Src::kBytesPerDof * (double)L.nx * L.rows());
     launch_k(k_smooth2<M, kTW, PF, Coef, Src>, grid, kTW, 0, p->st, L.grid(), A, src, om, g, out, wd, seg);
     KCHECK();
 }
@@ -591,6 +630,11 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
     const int seg = seg_rows(L.nx, L.rows());
     const int strips = (L.nx + OW - 1) / OW;
     dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
+    {
+        static const char* names[4] = {"smooth(from 0)", "smooth(from u)", "smooth(from P e)", "smooth(u + w P uc)"};
+        static const double bpd[4] = {16.0, 24.0, 18.0, 26.0};  // §8d: g in + out (+u) (+ coarse N/4)
+        prof_tag(names[SK], L.l, bpd[SK] * (double)L.nx * L.rows());
+    }
     launch_k(k_smooth4<M, SK, Coef>, grid, kS4W * 32, smem, p->st, L.grid(), A, u, P, om, g, out, wd, seg);
     KCHECK();
 }
@@ -687,6 +731,9 @@ void launch_resid_t(gmg_problem* p, const Lev& L, const Coef& A, const Src& src,
         rw = C.rw;
     }
     constexpr int PF = sizeof(typename Src::Raw) > 16 ? 2 : 4;
+    prof_tag(gc ? "residual+restrict" : "residual", L.l,
+             (8.0 * (Src::kReads + 1) + 8.0 * ((dout != nullptr) + (x0out != nullptr)) + (gc ? 2.0 : 0.0)) *
+                 (double)L.nx * L.rows());
     launch_k(k_resid<kTW, PF, Coef, Src>, grid, kTW, 0, p->st, L.grid(), A, src, g, dout, x0out, cg, rw, gc, seg, neg,
                                                           om);
     KCHECK();
@@ -707,6 +754,9 @@ void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* 
     const int seg = seg_rows(L.nx, L.rows());
     const int strips = (L.nx + 123) / 124;
     dim3 grid((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
+    prof_tag(SUM ? (gc ? "x+e, residual+restrict" : "x+e, residual") : (gc ? "residual+restrict" : "residual"), L.l,
+             (8.0 * (SUM ? 3 : 2) + 8.0 * ((dout != nullptr) + (x0out != nullptr)) + (gc ? 2.0 : 0.0)) *
+                 (double)L.nx * L.rows());
     launch_k(k_resid4<SUM, Coef>, grid, kS4W * 32, smem, p->st, L.grid(), A, u, e, g, dout, x0out, cg, rw, gc, seg);
     KCHECK();
 }
@@ -905,12 +955,14 @@ void launch_restrict(gmg_problem* p, int fine_level, const double* f, double* c)
     const Lev& F = p->lev(fine_level);
     const Lev& C = p->lev(fine_level - 1);
     dim3 b(32, 8), gr((C.nx + 31) / 32, (C.ny + 7) / 8);
+    prof_tag("restrict", fine_level, 10.0 * (double)F.n());
     launch_k(k_restrict_simple, gr, b, 0, p->st, F.grid(), f, C.grid(), C.rw, c);
     KCHECK();
 }
 
 void launch_coarse(gmg_problem* p, const double* g, double* x) {
     const Lev& L = p->lev(1);
+    prof_tag("coarse_solve", 1, 16.0 * (double)L.n());
     launch_k(k_coarse_chol, 1, 32, 0, p->st, p->band, p->cn, p->cbw, L.grid(), g, x, p->cscr);
     KCHECK();
 }
@@ -1254,6 +1306,7 @@ struct Driver {
         V.out = q->lev(l).buf[U0];
         V.status = q->status;
         set_smem(k_vsmall, kVSmemMax);
+        prof_tag("vsmall(V below)", l, 0.0);
         launch_k(k_vsmall, 1, kVThreads, vsmall_smem(l), q->st, V);
         KCHECK();
     }
@@ -1326,15 +1379,18 @@ struct Driver {
                     set_smem(k_omega4<C>, omega4_smem());
                     const int strips = (L.nx + 123) / 124;
                     dim3 g4((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
+                    prof_tag("omega terms", l, 26.0 * (double)L.nx * L.rows());
                     launch_k(k_omega4<C>, g4, kS4W * 32, omega4_smem(), q->st, L.grid(), A, src.P, L.buf[DD], T0, T1,
                                                                           q->nz_cur, seg);
                 } else {
+                    prof_tag("omega terms", l, 26.0 * (double)L.nx * L.rows());
                     launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, q->st, L.grid(), A, src, L.buf[DD], T0, T1, q->nz_cur,
                                                                        seg);
                 }
             });
             KCHECK();
         }
+        g_cur_level = l;
         dist_sum(S, sharded(l) ? D() : nullptr, [&](gmg_problem* q) {
             const Lev& L = q->lev(l);
             const long long o = (long long)L.w0 * L.nx;
@@ -1344,6 +1400,7 @@ struct Driver {
 
     // exact-order ||v||^2 of a level-l buffer over the owned rows -> sums[off]
     void norm_d(int l, int id, int off) {
+        g_cur_level = l;
         dist_sum(S, sharded(l) ? D() : nullptr, [&](gmg_problem* q) {
             const Lev& L = q->lev(l);
             Grid gv{L.nx, L.rows(), L.pitch, 0, L.rows()};
@@ -2498,6 +2555,51 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
         CK(cudaEventElapsedTime(&t, p->ev0, p->ev1));
         *ms = (double)t / reps;
         *bytes = per_dof * (double)F.n();
+    });
+}
+
+int gmg_dev_profile_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int cap, gmg_prof_entry* out, int* count) {
+    return guarded([&] {
+        checked(p);
+        std::lock_guard<std::mutex> lk(p->mu);
+        check_smoother(*spec);
+        const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
+        check_cycle(p, *spec);
+        std::vector<ProfEntry> prof;
+        prof.reserve(4096);
+        struct Reset {
+            ~Reset() { g_prof = nullptr; }
+        } reset;
+        CK(cudaStreamSynchronize(p->st));
+        g_prof = &prof;
+        try {
+            Driver d{driver_slabs(p), *spec, sm};
+            d.cycle(B_X0, B_X1);
+            CK(cudaStreamSynchronize(p->st));
+        } catch (...) {
+            g_prof = nullptr;
+            for (auto& e : prof) {
+                cudaEventDestroy(e.e0);
+                cudaEventDestroy(e.e1);
+            }
+            throw;
+        }
+        g_prof = nullptr;
+        int k = 0;
+        for (auto& e : prof) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e.e0, e.e1));
+            if (k < cap) {
+                std::snprintf(out[k].kernel, sizeof out[k].kernel, "%s", e.kernel.c_str());
+                out[k].level = e.level;
+                out[k].bytes = e.bytes;
+                out[k].ms = ms;
+            }
+            ++k;
+            cudaEventDestroy(e.e0);
+            cudaEventDestroy(e.e1);
+        }
+        *count = k;
     });
 }
 

@@ -53,7 +53,7 @@ EXPORTS = [
     "gmg_dev_time_smoother", "gmg_dev_cycle_kernel_count", "gmg_dev_seqsum_stats", "gmg_host_problem_create",
     "gmg_host_random_vector", "gmg_host_seqsum_emulate", "gmg_dev_problem_create_slabs", "gmg_dist_unique_id",
     "gmg_dev_dist_info", "gmg_dev_level_window", "gmg_host_problem_create_slabs", "gmg_host_slab_plan",
-    "gmg_dev_make_start_vector",
+    "gmg_dev_make_start_vector", "gmg_dev_profile_cycle",
 ]
 START_KINDS = ["zero", "nested", "continuation"]  # gmg::StartVectorKind (config.hpp:11)
 
@@ -119,6 +119,10 @@ class _CycleDesc(C.Structure):
                 ("reduction", C.c_int)]
 
 
+class _ProfEntry(C.Structure):
+    _fields_ = [("kernel", C.c_char * 48), ("level", C.c_int), ("bytes", C.c_double), ("ms", C.c_double)]
+
+
 class _Report(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("wall_seconds", C.c_double),
                 ("residual_history", _dp), ("convergence_factors", _dp), ("history_len", C.c_int),
@@ -159,6 +163,8 @@ def lib() -> C.CDLL:
         L.gmg_dev_axpy.argtypes = [C.c_void_p, C.c_longlong, C.c_double, _dp, _dp]
         L.gmg_dev_time_smoother.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, C.c_int, _dp, _dp]
         L.gmg_dev_seqsum_stats.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_ulonglong)]
+        L.gmg_dev_profile_cycle.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, C.POINTER(_ProfEntry),
+                                            C.POINTER(C.c_int)]
         L.gmg_dev_cycle_kernel_count.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.POINTER(C.c_int)]
         L.gmg_host_problem_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                               C.c_int, C.c_double, C.c_double, C.c_int,
@@ -510,6 +516,16 @@ def time_smoother(prob: MultilevelProblem, spec: CycleSpec, variant: int = 0, re
     ms, by = np.zeros(1), np.zeros(1)
     _check(lib().gmg_dev_time_smoother(prob._h, C.byref(spec._c()), variant, reps, _p(ms), _p(by)))
     return float(ms[0]), float(by[0])
+
+
+def profile_cycle(prob: MultilevelProblem, spec: CycleSpec, cap: int = 8192):
+    """One cycle with CUDA events around every launch: list of dicts
+    (kernel, level, bytes = algorithmic bytes, ms)."""
+    buf = (_ProfEntry * cap)()
+    n = C.c_int()
+    _check(lib().gmg_dev_profile_cycle(prob._h, C.byref(spec._c()), cap, buf, C.byref(n)))
+    return [dict(kernel=buf[k].kernel.decode(), level=buf[k].level, bytes=buf[k].bytes, ms=buf[k].ms)
+            for k in range(min(n.value, cap))]
 
 
 def cycle_kernel_count(prob: MultilevelProblem, spec: CycleSpec) -> int:
