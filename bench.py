@@ -320,7 +320,8 @@ def per_level_table(prof, peak, l2_bytes):
                     "l2_resident": bool(0 < r["max_launch_bytes"] <= l2_bytes)})
     total = sum(e["ms"] for e in prof)
     return {"entries": out, "profiled_ms_per_cycle": round(total, 4),
-            "how": "one cycle outside the graph, CUDA events around every launch on the solver stream; bytes = "
+            "how": "cycle 5 of the solve run outside the graph, CUDA events around every launch on the solver "
+                   "stream; bytes = "
                    "SURVEY.md 8(d) algorithmic bytes per DOF x level DOFs; ss_* chains carry no streamed bytes"}
 
 
@@ -346,7 +347,8 @@ def run_c5(gmg, torch, peak, l2_bytes, reduction):
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    table = per_level_table(gmg.profile_cycle(prob, spec), peak, l2_bytes)
+    x.copy_(torch.from_numpy(x0))
+    table = per_level_table(gmg.profile_cycle(prob, spec, b.data_ptr(), x.data_ptr(), skip=4), peak, l2_bytes)
     out = {"config": "C5: " + w["desc"] + ", exactly 10 F-cycles (tol 1e-30, max_cycles 10)", "dof": n,
            "cycles": rep.iterations, "ms_per_cycle": ms / rep.iterations,
            "value": n * rep.iterations / (ms / 1e3), "unit": "DOF*cycles/s",
@@ -449,7 +451,9 @@ def run_ours(args):
         per_cycle = gmg.cycle_kernel_count(single, spec)
         if ws == 1 and not args.no_per_level:
             x_dev.copy_(torch.from_numpy(x0_host))
-            per_level = per_level_table(gmg.profile_cycle(single, spec), peak, l2_bytes)
+            # cycle 5 of the solve (mid-convergence; a cycle's exact-sum records depend on the data)
+            per_level = per_level_table(gmg.profile_cycle(single, spec, b_dev.data_ptr(), x_dev.data_ptr(), skip=4),
+                                        peak, l2_bytes)
     if ws > 1:
         barrier()
 

@@ -206,19 +206,21 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
  * block merge, run/offset look-back), [13] walk CTAs, [14] literal (dense-break)
  * chunks among [5], [15] their cycles. out16 holds 16 values. */
 int gmg_dev_seqsum_stats(gmg_problem* p, int reset, unsigned long long* out16);
-/* One solver cycle run outside the CUDA graph with CUDA events around every
- * launch (on the solver stream): per launch the kernel family, the level it
- * works on, its algorithmic bytes (SURVEY.md §8d per-DOF bytes x the level's
- * DOFs; 0 for the exact-sum chains and the one-CTA coarse V-cycles) and its
- * duration. Advances the solution like one cycle of gmg_dev_solve_devptr from
- * the current device state. count = launches (entries beyond cap dropped). */
+/* Cycle skip+1 of a solve from b_dev, x_dev (device, reference layout) run
+ * outside the CUDA graph with CUDA events around every launch (on the solver
+ * stream): per launch the kernel family, the level it works on, its algorithmic
+ * bytes (SURVEY.md §8d per-DOF bytes x the level's DOFs; 0 for the exact-sum
+ * chains and the one-CTA coarse V-cycles) and its duration. The first `skip`
+ * cycles replay the solve's graph unprofiled. count = launches (entries beyond
+ * cap dropped). */
 typedef struct gmg_prof_entry {
     char kernel[48];
     int level;
     double bytes;
     double ms;
 } gmg_prof_entry;
-int gmg_dev_profile_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int cap, gmg_prof_entry* out, int* count);
+int gmg_dev_profile_cycle(gmg_problem* p, const gmg_cycle_desc* spec, const double* b_dev, const double* x_dev,
+                          int skip, int cap, gmg_prof_entry* out, int* count);
 /* Number of kernels one solver cycle launches (from the captured graph). */
 int gmg_dev_cycle_kernel_count(gmg_problem* p, const gmg_cycle_desc* spec, int* count);
 

@@ -55,13 +55,32 @@ struct Grid {
 //   ROWX  : coefficients depend on i only (uniform cylindrical, C3'): 1-D tables.
 //   FIELD : general graded / spherical: five pitched arrays.
 // `div_by_c` is the Jacobi preconditioner z = r / c (smoother.cpp:293-295):
-// a true IEEE division, or a multiplication by the exact reciprocal when c is a
-// power of two (identical result).
+// the IEEE round-to-nearest quotient, computed as a multiplication by the exact
+// reciprocal when c is a power of two, else by div_rcp from the host-rounded
+// reciprocal (three fp64 ops instead of the division's iteration; identical
+// result), else by a true division.
 // ---------------------------------------------------------------------------
+
+// RN(d / c) from y = RN(1 / c) (Markstein's theorem: q0 = RN(d y) is within one
+// ulp of d / c, so r = d - q0 c is exact in one FMA and RN(q0 + r y) is the
+// correctly rounded quotient; no underflow or overflow on the way for
+// 2^-960 < |d| < 2^960 and c, y normal in [2^-500, 2^500], which the host checks).
+// Zeros (keeping their sign), huge/tiny, inf and NaN dividends take the division.
+__device__ __forceinline__ double div_rcp(double d, double c, double y) {
+    const double q0 = d * y;
+    const double a = fabs(d);
+    if (!(a > 0x1p-960 && a < 0x1p960)) return d == 0.0 ? q0 : d / c;
+    const double r = __fma_rn(-q0, c, d);
+    return __fma_rn(r, y, q0);
+}
+
 struct CoefConst {
+    static constexpr bool kUnitWE = false, kUnitSN = false;  // legs known to be exactly -1
     double c, w, e, s, n;
     double inv_c;  // exact reciprocal (valid only when c_pow2)
     int c_pow2;
+    int rcp_ok;   // rcp = RN(1/c) usable by div_rcp (c in the checked range)
+    double rcp;
     __device__ __forceinline__ void load(int, int, double& C, double& W, double& E, double& S,
                                          double& N) const {
         C = c;
@@ -72,18 +91,33 @@ struct CoefConst {
     }
     __device__ __forceinline__ double diag(int, int) const { return c; }
     __device__ __forceinline__ double div_by_c(double r, int, int) const {
-        return c_pow2 ? r * inv_c : r / c;
+        return c_pow2 ? r * inv_c : (rcp_ok ? div_rcp(r, c, rcp) : r / c);
     }
 };
 
-// CoefConst whose c is a power of two: the division is the exact multiplication
-// unconditionally (chosen on the host, so kernels carry no per-point branch).
-struct CoefConstP2 : CoefConst {
+// Specialised constant rows for the streaming kernels of large levels (chosen on
+// the host, so kernels carry no per-point branch). Multiplying by -1 is an exact
+// negation and a + (-b) is a - b bit for bit, so a -1 leg is a subtraction.
+//   CoefIso   : c a power of two and all four legs -1 (isotropic Poisson: C1, C4):
+//               acc = c x - xw - xe - xs - xn, z = r * (1/c) exactly.
+//   CoefUnitSN: s = n = -1 (beta = 1: the anisotropic C2, C5), w and e general:
+//               acc = c x + w xw + e xe - xs - xn, z by the exact reciprocal
+//               (c a power of two) or div_rcp.
+struct CoefIso : CoefConst {
+    static constexpr bool kUnitWE = true, kUnitSN = true;
     __device__ __forceinline__ double div_by_c(double r, int, int) const { return r * inv_c; }
+};
+struct CoefUnitSN : CoefConst {
+    static constexpr bool kUnitSN = true;
+    __device__ __forceinline__ double div_by_c(double r, int, int) const {
+        return c_pow2 ? r * inv_c : div_rcp(r, c, rcp);
+    }
 };
 
 struct CoefRowX {
+    static constexpr bool kUnitWE = false, kUnitSN = false;
     const double *c, *w, *e, *s, *n;  // length nx each
+    const double* rc;                 // RN(1/c[i]) for div_rcp, or null (some c outside the checked range)
     __device__ __forceinline__ void load(int i, int, double& C, double& W, double& E, double& S,
                                          double& N) const {
         C = __ldg(c + i);
@@ -93,10 +127,13 @@ struct CoefRowX {
         N = __ldg(n + i);
     }
     __device__ __forceinline__ double diag(int i, int) const { return __ldg(c + i); }
-    __device__ __forceinline__ double div_by_c(double r, int i, int) const { return r / __ldg(c + i); }
+    __device__ __forceinline__ double div_by_c(double r, int i, int) const {
+        return rc ? div_rcp(r, __ldg(c + i), __ldg(rc + i)) : r / __ldg(c + i);
+    }
 };
 
 struct CoefField {
+    static constexpr bool kUnitWE = false, kUnitSN = false;
     const double *c, *w, *e, *s, *n;  // pitched like the level's grid functions
     long long pitch;
     __device__ __forceinline__ void load(int i, int j, double& C, double& W, double& E, double& S,
@@ -126,10 +163,20 @@ __device__ __forceinline__ double stencil_apply(const Coef& A, int i, int j, dou
     double C, W, E, S, N;
     A.load(i, j, C, W, E, S, N);
     double acc = C * xc;
-    acc = acc + W * xw;
-    acc = acc + E * xe;
-    acc = acc + S * xs;
-    acc = acc + N * xn;
+    if constexpr (Coef::kUnitWE) {
+        acc = acc - xw;
+        acc = acc - xe;
+    } else {
+        acc = acc + W * xw;
+        acc = acc + E * xe;
+    }
+    if constexpr (Coef::kUnitSN) {
+        acc = acc - xs;
+        acc = acc - xn;
+    } else {
+        acc = acc + S * xs;
+        acc = acc + N * xn;
+    }
     return acc;
 }
 

@@ -412,6 +412,28 @@ void with_coef(const Lev& L, F&& f) {
     else f(L.cfield);
 }
 
+// Coefficient classes of the warp-strip kernels (large levels): constant rows
+// specialised when their legs are exactly -1 (common.cuh CoefIso / CoefUnitSN).
+template <class F>
+void with_coef_big(const Lev& L, F&& f) {
+    if (L.kind == 0) {
+        const CoefConst& k = L.cconst;
+        if (k.c_pow2 && k.w == -1.0 && k.e == -1.0 && k.s == -1.0 && k.n == -1.0) {
+            CoefIso A;
+            static_cast<CoefConst&>(A) = k;
+            f(A);
+            return;
+        }
+        if (k.s == -1.0 && k.n == -1.0 && (k.c_pow2 || k.rcp_ok)) {
+            CoefUnitSN A;
+            static_cast<CoefConst&>(A) = k;
+            f(A);
+            return;
+        }
+    }
+    with_coef(L, f);
+}
+
 // Once-per-device setup (function attributes apply to the current device only):
 // a (key, device) set guarded by a mutex, so problems on several devices and
 // concurrent creates/solves on different threads each configure their device.
@@ -647,7 +669,7 @@ static const int kRingMinNx = [] {
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
                        double* out, double wd) {
-    if constexpr (std::is_same<Coef, CoefConstP2>::value) {
+    if constexpr (std::is_same<Coef, CoefIso>::value || std::is_same<Coef, CoefUnitSN>::value) {
         switch (s.kind) {
             case S_ZERO: launch_smooth4_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
             case S_U: launch_smooth4_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
@@ -691,19 +713,7 @@ void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const Smooth
 // One launch of M <= 4 Jacobi steps.
 void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, const double* g, double* out,
                    double wd) {
-    if (L.kind == 0 && L.cconst.c_pow2 && L.nx >= kRingMinNx) {  // k_smooth4
-        CoefConstP2 A;
-        static_cast<CoefConst&>(A) = L.cconst;
-        switch (M) {
-            case 0: launch_smooth_src<0>(p, L, A, s, g, out, wd); return;
-            case 1: launch_smooth_src<1>(p, L, A, s, g, out, wd); return;
-            case 2: launch_smooth_src<2>(p, L, A, s, g, out, wd); return;
-            case 3: launch_smooth_src<3>(p, L, A, s, g, out, wd); return;
-            case 4: launch_smooth_src<4>(p, L, A, s, g, out, wd); return;
-            default: throw GmgError{GMG_ERR_LOGIC, "smooth: M > 4"};
-        }
-    }
-    with_coef(L, [&](const auto& A) {
+    auto go = [&](const auto& A) {
         switch (M) {
             case 0: launch_smooth_src<0>(p, L, A, s, g, out, wd); break;
             case 1: launch_smooth_src<1>(p, L, A, s, g, out, wd); break;
@@ -712,7 +722,9 @@ void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, cons
             case 4: launch_smooth_src<4>(p, L, A, s, g, out, wd); break;
             default: throw GmgError{GMG_ERR_LOGIC, "smooth: M > 4"};
         }
-    });
+    };
+    if (L.nx >= kRingMinNx) with_coef_big(L, go);  // k_smooth4
+    else with_coef(L, go);
 }
 
 constexpr int kMaxFuse = 4;
@@ -765,7 +777,7 @@ void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* 
 void launch_resid(gmg_problem* p, const Lev& L, const double* u, const double* e, const double* g,
                   double* dout, double* x0out, double* gc) {
     if (L.nx >= kRingMinNx) {
-        with_coef(L, [&](const auto& A) {
+        with_coef_big(L, [&](const auto& A) {
             if (e)
                 launch_resid4_t<true>(p, L, A, u, e, g, dout, x0out, gc);
             else
@@ -1373,21 +1385,24 @@ struct Driver {
             SrcProlong src{prolong_from(q, l - 1, q->lev(l - 1).buf[uc]), L.nx, L.ny, 0.0};
             double* T0 = q->T;
             double* T1 = q->T + q->lev(q->L).n();
-            with_coef(L, [&](const auto& A) {
-                using C = std::decay_t<decltype(A)>;
-                if (L.nx >= kRingMinNx) {
+            if (L.nx >= kRingMinNx) {
+                with_coef_big(L, [&](const auto& A) {
+                    using C = std::decay_t<decltype(A)>;
                     set_smem(k_omega4<C>, omega4_smem());
                     const int strips = (L.nx + 123) / 124;
                     dim3 g4((strips + kS4W - 1) / kS4W, (L.rows() + seg - 1) / seg);
                     prof_tag("omega terms", l, 26.0 * (double)L.nx * L.rows());
                     launch_k(k_omega4<C>, g4, kS4W * 32, omega4_smem(), q->st, L.grid(), A, src.P, L.buf[DD], T0, T1,
-                                                                          q->nz_cur, seg);
-                } else {
+                             q->nz_cur, seg);
+                });
+            } else {
+                with_coef(L, [&](const auto& A) {
+                    using C = std::decay_t<decltype(A)>;
                     prof_tag("omega terms", l, 26.0 * (double)L.nx * L.rows());
-                    launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, q->st, L.grid(), A, src, L.buf[DD], T0, T1, q->nz_cur,
-                                                                       seg);
-                }
-            });
+                    launch_k(k_omega_terms<kTW, 2, C>, grid, kTW, 0, q->st, L.grid(), A, src, L.buf[DD], T0, T1,
+                             q->nz_cur, seg);
+                });
+            }
             KCHECK();
         }
         g_cur_level = l;
@@ -1864,6 +1879,12 @@ void free_problem(gmg_problem* p) {
     delete p;
 }
 
+// c (and so RN(1/c)) inside the range where div_rcp is exact (common.cuh)
+bool rcp_range_ok(double c) {
+    const double a = std::fabs(c);
+    return std::isnormal(c) && a >= 0x1p-500 && a <= 0x1p500;
+}
+
 double* alloc_pitched(size_t n_buffers, Lev& L) {
     double* m = nullptr;
     CK(dmalloc(&m, n_buffers * L.elems * sizeof(double)));
@@ -1917,20 +1938,30 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         const gmg_host::CoefClass cc = gmg_host::classify(ld.nx, ld.ny, ld.c, ld.n, ld.s, ld.e, ld.w);
         L.kind = cc.kind;
         if (cc.kind == gmg_host::COEF_CONST) {
-            L.cconst = CoefConst{cc.c, cc.w, cc.e, cc.s, cc.n, 0.0, 0};
+            L.cconst = CoefConst{cc.c, cc.w, cc.e, cc.s, cc.n, 0.0, 0, 0, 0.0};
             int ex2;
             const double fr = std::frexp(cc.c, &ex2);
             if (fr == 0.5 && std::isnormal(cc.c)) {
                 L.cconst.c_pow2 = 1;
                 L.cconst.inv_c = std::ldexp(1.0, 1 - ex2);
             }
+            if (rcp_range_ok(cc.c)) {
+                L.cconst.rcp_ok = 1;
+                L.cconst.rcp = 1.0 / cc.c;
+            }
         } else if (cc.kind == gmg_host::COEF_ROWX) {
-            CK(dmalloc(&L.coefmem, 5 * L.nx * sizeof(double)));
-            const std::vector<double>* t[5] = {&cc.rc, &cc.rw, &cc.re, &cc.rs, &cc.rn};
-            for (int q = 0; q < 5; ++q)
+            CK(dmalloc(&L.coefmem, 6 * L.nx * sizeof(double)));
+            std::vector<double> rc(L.nx);
+            bool ok = true;
+            for (int i = 0; i < L.nx; ++i) {
+                ok = ok && rcp_range_ok(cc.rc[i]);
+                rc[i] = 1.0 / cc.rc[i];
+            }
+            const std::vector<double>* t[6] = {&cc.rc, &cc.rw, &cc.re, &cc.rs, &cc.rn, &rc};
+            for (int q = 0; q < 6; ++q)
                 CK(cudaMemcpy(L.coefmem + q * L.nx, t[q]->data(), L.nx * sizeof(double), cudaMemcpyHostToDevice));
-            L.crow = CoefRowX{L.coefmem, L.coefmem + L.nx, L.coefmem + 2 * L.nx, L.coefmem + 3 * L.nx,
-                              L.coefmem + 4 * L.nx};
+            L.crow = CoefRowX{L.coefmem,          L.coefmem + L.nx,     L.coefmem + 2 * L.nx, L.coefmem + 3 * L.nx,
+                              L.coefmem + 4 * L.nx, ok ? L.coefmem + 5 * L.nx : nullptr};
         } else {
             CK(dmalloc(&L.coefmem, 5 * L.elems * sizeof(double)));
             CK(cudaMemset(L.coefmem, 0, 5 * L.elems * sizeof(double)));
@@ -2558,13 +2589,27 @@ int gmg_dev_time_smoother(gmg_problem* p, const gmg_cycle_desc* spec, int varian
     });
 }
 
-int gmg_dev_profile_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int cap, gmg_prof_entry* out, int* count) {
+int gmg_dev_profile_cycle(gmg_problem* p, const gmg_cycle_desc* spec, const double* b_dev, const double* x_dev,
+                          int skip, int cap, gmg_prof_entry* out, int* count) {
     return guarded([&] {
         checked(p);
         std::lock_guard<std::mutex> lk(p->mu);
         check_smoother(*spec);
         const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
         check_cycle(p, *spec);
+        Lev& F = p->lev(p->L);
+        for (auto* q : driver_slabs(p)) {
+            upload(q, F, q->B, b_dev, cudaMemcpyDeviceToDevice);
+            upload(q, F, q->X[0], x_dev, cudaMemcpyDeviceToDevice);
+        }
+        // the solve's prologue (r0 and the first defect cascade seed), then `skip` cycles
+        Driver d0{driver_slabs(p), *spec, sm};
+        d0.initial_resid();
+        int par = 0;
+        if (skip > 0) {
+            auto& ex = get_graphs(p, *spec);
+            for (int k = 0; k < skip; ++k, par = 1 - par) CK(cudaGraphLaunch(ex[par], p->st));
+        }
         std::vector<ProfEntry> prof;
         prof.reserve(4096);
         struct Reset {
@@ -2574,7 +2619,7 @@ int gmg_dev_profile_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int cap, g
         g_prof = &prof;
         try {
             Driver d{driver_slabs(p), *spec, sm};
-            d.cycle(B_X0, B_X1);
+            d.cycle(par == 0 ? B_X0 : B_X1, par == 0 ? B_X1 : B_X0);
             CK(cudaStreamSynchronize(p->st));
         } catch (...) {
             g_prof = nullptr;

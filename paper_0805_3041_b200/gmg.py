@@ -163,8 +163,8 @@ def lib() -> C.CDLL:
         L.gmg_dev_axpy.argtypes = [C.c_void_p, C.c_longlong, C.c_double, _dp, _dp]
         L.gmg_dev_time_smoother.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, C.c_int, _dp, _dp]
         L.gmg_dev_seqsum_stats.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_ulonglong)]
-        L.gmg_dev_profile_cycle.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_int, C.POINTER(_ProfEntry),
-                                            C.POINTER(C.c_int)]
+        L.gmg_dev_profile_cycle.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.c_void_p, C.c_void_p, C.c_int,
+                                            C.c_int, C.POINTER(_ProfEntry), C.POINTER(C.c_int)]
         L.gmg_dev_cycle_kernel_count.argtypes = [C.c_void_p, C.POINTER(_CycleDesc), C.POINTER(C.c_int)]
         L.gmg_host_problem_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                               C.c_int, C.c_double, C.c_double, C.c_int,
@@ -518,12 +518,13 @@ def time_smoother(prob: MultilevelProblem, spec: CycleSpec, variant: int = 0, re
     return float(ms[0]), float(by[0])
 
 
-def profile_cycle(prob: MultilevelProblem, spec: CycleSpec, cap: int = 8192):
-    """One cycle with CUDA events around every launch: list of dicts
-    (kernel, level, bytes = algorithmic bytes, ms)."""
+def profile_cycle(prob: MultilevelProblem, spec: CycleSpec, b_ptr: int, x_ptr: int, skip: int = 0, cap: int = 8192):
+    """Cycle skip+1 of a solve from device arrays b, x with CUDA events around every
+    launch: list of dicts (kernel, level, bytes = algorithmic bytes, ms)."""
     buf = (_ProfEntry * cap)()
     n = C.c_int()
-    _check(lib().gmg_dev_profile_cycle(prob._h, C.byref(spec._c()), cap, buf, C.byref(n)))
+    _check(lib().gmg_dev_profile_cycle(prob._h, C.byref(spec._c()), C.c_void_p(b_ptr), C.c_void_p(x_ptr), skip, cap,
+                                       buf, C.byref(n)))
     return [dict(kernel=buf[k].kernel.decode(), level=buf[k].level, bytes=buf[k].bytes, ms=buf[k].ms)
             for k in range(min(n.value, cap))]
 
