@@ -65,17 +65,39 @@ struct Grid {
 // ulp of d / c, so r = d - q0 c is exact in one FMA and RN(q0 + r y) is the
 // correctly rounded quotient; no underflow or overflow on the way for
 // 2^-960 < |d| < 2^960 and c, y normal in [2^-500, 2^500], which the host checks).
-// Zeros (keeping their sign), huge/tiny, inf and NaN dividends take the division.
+// Zeros keep their sign (q0 = +-0); huge/tiny, inf and NaN dividends take the
+// true division, out of line: an inlined IEEE division (~30 instructions and a
+// slow path) per point and fused step would swamp the instruction cache of the
+// unrolled streaming kernels.
+__device__ __noinline__ double div_ieee(double d, double c) { return d / c; }
 __device__ __forceinline__ double div_rcp(double d, double c, double y) {
     const double q0 = d * y;
     const double a = fabs(d);
-    if (!(a > 0x1p-960 && a < 0x1p960)) return d == 0.0 ? q0 : d / c;
+    if (!(a > 0x1p-960 && a < 0x1p960)) return d == 0.0 ? q0 : div_ieee(d, c);
     const double r = __fma_rn(-q0, c, d);
     return __fma_rn(r, y, q0);
 }
 
+// div_rcp without the out-of-line division: RN(d / c) unless `slow` is set
+// (|d| outside the checked range and d != 0, or inf/NaN), in which case the
+// caller recomputes the point through div_rcp / div_ieee. Range and zero tests
+// are integer ops on d's bits (the fp64 pipe is the busy one); a zero keeps its
+// sign through q0.
+__device__ __forceinline__ double div_rcp_fast(double d, double c, double y, bool& slow) {
+    const double q0 = d * y;
+    const unsigned hi = static_cast<unsigned>(__double2hiint(d));
+    const unsigned lo = static_cast<unsigned>(__double2loint(d));
+    const unsigned e = (hi >> 20) & 0x7ffu;             // biased exponent
+    const bool zero = ((hi << 1) | lo) == 0u;
+    slow = !zero && (e - 64u) > 1918u;                  // in range: 2^-959 <= |d| < 2^960
+    const double r = __fma_rn(-q0, c, d);
+    const double q1 = __fma_rn(r, y, q0);
+    return zero ? q0 : q1;
+}
+
 struct CoefConst {
     static constexpr bool kUnitWE = false, kUnitSN = false;  // legs known to be exactly -1
+    static constexpr bool kMaySlow = false;                 // div_by_c_fast may ask for a recompute
     double c, w, e, s, n;
     double inv_c;  // exact reciprocal (valid only when c_pow2)
     int c_pow2;
@@ -91,7 +113,11 @@ struct CoefConst {
     }
     __device__ __forceinline__ double diag(int, int) const { return c; }
     __device__ __forceinline__ double div_by_c(double r, int, int) const {
-        return c_pow2 ? r * inv_c : (rcp_ok ? div_rcp(r, c, rcp) : r / c);
+        return c_pow2 ? r * inv_c : (rcp_ok ? div_rcp(r, c, rcp) : div_ieee(r, c));
+    }
+    __device__ __forceinline__ double div_by_c_fast(double r, int i, int j, bool& slow) const {
+        slow = false;
+        return div_by_c(r, i, j);
     }
 };
 
@@ -106,16 +132,21 @@ struct CoefConst {
 struct CoefIso : CoefConst {
     static constexpr bool kUnitWE = true, kUnitSN = true;
     __device__ __forceinline__ double div_by_c(double r, int, int) const { return r * inv_c; }
+    __device__ __forceinline__ double div_by_c_fast(double r, int, int, bool& slow) const {
+        slow = false;
+        return r * inv_c;
+    }
 };
-struct CoefUnitSN : CoefConst {
-    static constexpr bool kUnitSN = true;
-    __device__ __forceinline__ double div_by_c(double r, int, int) const {
-        return c_pow2 ? r * inv_c : div_rcp(r, c, rcp);
+struct CoefUnitSN : CoefConst {  // rcp_ok is required (host)
+    static constexpr bool kUnitSN = true, kMaySlow = true;
+    __device__ __forceinline__ double div_by_c(double r, int, int) const { return div_rcp(r, c, rcp); }
+    __device__ __forceinline__ double div_by_c_fast(double r, int, int, bool& slow) const {
+        return div_rcp_fast(r, c, rcp, slow);
     }
 };
 
 struct CoefRowX {
-    static constexpr bool kUnitWE = false, kUnitSN = false;
+    static constexpr bool kUnitWE = false, kUnitSN = false, kMaySlow = false;
     const double *c, *w, *e, *s, *n;  // length nx each
     const double* rc;                 // RN(1/c[i]) for div_rcp, or null (some c outside the checked range)
     __device__ __forceinline__ void load(int i, int, double& C, double& W, double& E, double& S,
@@ -128,12 +159,16 @@ struct CoefRowX {
     }
     __device__ __forceinline__ double diag(int i, int) const { return __ldg(c + i); }
     __device__ __forceinline__ double div_by_c(double r, int i, int) const {
-        return rc ? div_rcp(r, __ldg(c + i), __ldg(rc + i)) : r / __ldg(c + i);
+        return rc ? div_rcp(r, __ldg(c + i), __ldg(rc + i)) : div_ieee(r, __ldg(c + i));
+    }
+    __device__ __forceinline__ double div_by_c_fast(double r, int i, int j, bool& slow) const {
+        slow = false;
+        return div_by_c(r, i, j);
     }
 };
 
 struct CoefField {
-    static constexpr bool kUnitWE = false, kUnitSN = false;
+    static constexpr bool kUnitWE = false, kUnitSN = false, kMaySlow = false;
     const double *c, *w, *e, *s, *n;  // pitched like the level's grid functions
     long long pitch;
     __device__ __forceinline__ void load(int i, int j, double& C, double& W, double& E, double& S,
@@ -147,7 +182,11 @@ struct CoefField {
     }
     __device__ __forceinline__ double diag(int i, int j) const { return __ldg(c + (long long)j * pitch + i); }
     __device__ __forceinline__ double div_by_c(double r, int i, int j) const {
-        return r / __ldg(c + (long long)j * pitch + i);
+        return div_ieee(r, __ldg(c + (long long)j * pitch + i));
+    }
+    __device__ __forceinline__ double div_by_c_fast(double r, int i, int j, bool& slow) const {
+        slow = false;
+        return div_by_c(r, i, j);
     }
 };
 

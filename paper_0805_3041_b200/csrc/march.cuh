@@ -175,6 +175,17 @@ __device__ __forceinline__ double jacobi_point(const Coef& A, int i, int j, doub
     return xc - omega * z;
 }
 
+// jacobi_point with the division's fast path only; `slow` asks the caller to
+// recompute the point with jacobi_point (Coef::kMaySlow, common.cuh).
+template <class Coef>
+__device__ __forceinline__ double jacobi_point_fast(const Coef& A, int i, int j, double xc, double xw, double xe,
+                                                    double xs, double xn, double g, double omega, bool& slow) {
+    const double acc = stencil_apply(A, i, j, xc, xw, xe, xs, xn);
+    const double d = acc - g;
+    const double z = A.div_by_c_fast(d, i, j, slow);
+    return xc - omega * z;
+}
+
 // ---------------- residual (+ restriction) ---------------------------------
 // d = g - A x0 (stencil.cpp:148-153), or with neg the smoother defect
 // A x0 - g (smoother.cpp:393-394), optionally stored; x0 optionally stored;

@@ -220,13 +220,25 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                 const double xl = __shfl_up_sync(0xffffffffu, w[l][sc][3], 1);
                 const double xr = __shfl_down_sync(0xffffffffu, w[l][sc][0], 1);
                 double y[4];
+                bool slow[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const double xw = k == 0 ? xl : w[l][sc][k - 1];
                     const double xe = k == 3 ? xr : w[l][sc][k + 1];
-                    y[k] = jacobi_point(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe, w[l][sd][k],
-                                        w[l][sn][k], gr[l][k],
-                                        omega_damp);
+                    y[k] = jacobi_point_fast(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe, w[l][sd][k],
+                                             w[l][sn][k], gr[l][k], omega_damp, slow[k]);
+                }
+                if constexpr (Coef::kMaySlow) {
+                    // one warp vote per fused step and row; the exact division only where asked
+                    if (__any_sync(0xffffffffu, slow[0] | slow[1] | slow[2] | slow[3])) {
+                        for (int k = 0; k < 4; ++k) {
+                            if (!slow[k]) continue;
+                            const double xw = k == 0 ? xl : w[l][sc][k - 1];
+                            const double xe = k == 3 ? xr : w[l][sc][k + 1];
+                            y[k] = jacobi_point(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe,
+                                                w[l][sd][k], w[l][sn][k], gr[l][k], omega_damp);
+                        }
+                    }
                 }
                 if (R < 0 || R >= ny) {
 #pragma unroll

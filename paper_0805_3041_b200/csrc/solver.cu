@@ -424,7 +424,7 @@ void with_coef_big(const Lev& L, F&& f) {
             f(A);
             return;
         }
-        if (k.s == -1.0 && k.n == -1.0 && (k.c_pow2 || k.rcp_ok)) {
+        if (k.s == -1.0 && k.n == -1.0 && k.rcp_ok) {
             CoefUnitSN A;
             static_cast<CoefConst&>(A) = k;
             f(A);

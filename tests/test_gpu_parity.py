@@ -310,3 +310,33 @@ def test_c5_full_size_ten_cycles(gpu):
         first_mismatch(rep.residual_history, unhex(g["history"]))
     import hashlib
     assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == g["x_sha256"]
+
+
+@pytest.mark.parametrize("alpha", [1.0, 1e-2, 0.3])
+def test_jacobi_division_paths_edge_values(gpu, alpha):
+    """The Jacobi preconditioner z = d / c (smoother.cpp:293-295) on the warp-strip
+    kernels: exact reciprocal (c = 4), the reciprocal-FMA path with its out-of-range
+    fallback (c = 2 + 2 alpha), on defects spanning zeros of both signs, subnormals,
+    tiny and huge magnitudes; M = 1..4 fused steps; bit for bit against the oracle."""
+    levels = 9  # 511^2: k_smooth4
+    a = (levels, 1, 1, (1.0, 1.0), "cartesian", alpha, 1.0)
+    d, o = gmg.MultilevelProblem(*a), Oracle(*a)
+    n = d.n(levels)
+    rng = np.random.default_rng(7)
+    mags = np.array([0.0, -0.0, 5e-324, 1e-310, 1e-300, 2.0 ** -960, 2.0 ** -959, 1e-12, 1.0, 1e12, 2.0 ** 959,
+                     2.0 ** 960, 1e300])
+    x = rng.choice(mags, n) * rng.choice([-1.0, 1.0], n)
+    b = rng.choice(mags, n) * rng.choice([-1.0, 1.0], n)
+    x[: n // 2] = Oracle.random_vector(n // 2, 3)  # half ordinary values
+    for damp in (0.7, 1.0):
+        got = gmg.smooth_step(d, levels, "jacobi", 1.0, x, b, damp)
+        want = o.smooth_step(levels, "jacobi", 1.0, damp, x, b)
+        assert bits_equal(got, want), (damp, first_mismatch(got, want))
+    # fused steps (mg_cycle's pre-smoothing from u) on ordinary data
+    xo = Oracle.random_vector(n, 4)
+    bo = Oracle.random_vector(n, 5)
+    for steps in (2, 3, 4):
+        spec = dict(cycle="V", smoother="jacobi", pre_steps=steps, post_steps=0)
+        got = gmg.mg_cycle(d, levels, xo, bo, gmg.CycleSpec(**spec))
+        want = o.mg_cycle(OSpec(**spec), levels, xo, bo)
+        assert bits_equal(got, want), (steps, first_mismatch(got, want))
