@@ -12,8 +12,10 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "gmg_b200")
-LIB = os.path.join(PKG, "libgmg_b200.so")
+# GMG_LIB_OUT / GMG_BUILD_DIR: an alternative build (e.g. an instrumented -D variant for A/B
+# timing) next to the product library; load it with GMG_LIB_PATH.
+BUILD = os.environ.get("GMG_BUILD_DIR") or os.path.join(ROOT, "build", "gmg_b200")
+LIB = os.environ.get("GMG_LIB_OUT") or os.path.join(PKG, "libgmg_b200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
