@@ -64,7 +64,16 @@ WORKLOADS = {
                     "F-cycle, adaptive omega_l, exact-order reductions"),
     "C1": dict(levels=7, alpha=1.0, beta=1.0, pre=2, post=2, tol=1e-8, seed_x=0,
                desc="127^2 interior (129^2 vertices), 7 levels, isotropic Poisson, jacobi 0.7 2+2"),
+    # BASELINE config 3 (no reference counterpart: the oracle restatement is the checker)
+    "C3": dict(levels=10, alpha=1.0, beta=1.0, pre=2, post=2, tol=1e-8, seed_x=0, coords="polar", cny=2,
+               desc="polar Poisson 1023 (r in [0.1,1], Dirichlet) x 1024 (theta, periodic), 10 levels, "
+                    "jacobi 0.7 2+2, F-cycle, adaptive omega_l, exact-order reductions"),
 }
+
+
+def wl_args(w):
+    """MultilevelProblem / Oracle constructor arguments of a workload."""
+    return (w["levels"], 1, w.get("cny", 1), (1.0, 1.0), w.get("coords", "cartesian"), w["alpha"], w["beta"])
 
 
 def common_config(wl, n):
@@ -204,8 +213,10 @@ def cpu_reference_fcycle(wl, threads=1, cycles=1, seconds_cap=None):
     kind = "reference" if pyoracle.Reference.available() else "port"
     B = pyoracle.Reference if kind == "reference" else pyoracle.Oracle
     w = WORKLOADS[wl]
+    if w.get("coords") == "polar":
+        B, kind = pyoracle.Oracle, "port"
     t0 = time.time()
-    prob = B(w["levels"], 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+    prob = B(*wl_args(w))
     n = prob.n(w["levels"])
     b = B.random_vector(n, 1)
     setup = time.time() - t0
@@ -257,7 +268,10 @@ def run_reference_arm(args):
     import pyoracle
     kind = "reference" if pyoracle.Reference.available() else "port"
     B = pyoracle.Reference if kind == "reference" else pyoracle.Oracle
-    prob = B(w["levels"], 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+    if w.get("coords") == "polar":
+        B = pyoracle.Oracle  # no reference counterpart for polar coordinates: the oracle port
+        kind = "port"
+    prob = B(*wl_args(w))
     n = prob.n(w["levels"])
     b = B.random_vector(n, 1)
     P = usable_threads(n) if args.ref_threads <= 0 else args.ref_threads
@@ -377,7 +391,7 @@ def run_ours(args):
     wl = args.workload
     w = WORKLOADS[wl]
     L = w["levels"]
-    pargs = (L, 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+    pargs = wl_args(w)
     sharded = ws > 1 and args.parallel == "slabs"
     if sharded:
         # one NCCL group for the row slabs; rank 0's unique id travels over the torch group

@@ -64,8 +64,11 @@ enum gmg_smoother_kind {
 };
 /* gmg::CycleType, include/gmg/cycle.hpp:17 */
 enum gmg_cycle_type { GMG_CYCLE_V = 0, GMG_CYCLE_W = 1, GMG_CYCLE_F = 2 };
-/* gmg::CoordinateSystem, include/gmg/mesh.hpp:8 */
-enum gmg_coords { GMG_CARTESIAN = 0, GMG_CYLINDRICAL = 1, GMG_SPHERICAL = 2 };
+/* gmg::CoordinateSystem, include/gmg/mesh.hpp:8; GMG_POLAR has no reference
+ * counterpart (BASELINE config 3: r in [0.1, 1] Dirichlet, theta periodic;
+ * host_setup.h documents the discretisation; only the jacobi and richardson
+ * smoothers, parity against the oracle restatement, unpinned). */
+enum gmg_coords { GMG_CARTESIAN = 0, GMG_CYLINDRICAL = 1, GMG_SPHERICAL = 2, GMG_POLAR = 3 };
 /* how dot products / norms are summed on the device */
 enum gmg_reduction {
     GMG_REDUCE_EXACT = 0, /* bit-identical to the reference's left-to-right sum */
@@ -87,6 +90,10 @@ typedef struct gmg_problem_desc {
     int num_levels;
     const gmg_level_desc* levels; /* levels[0] = level 1 */
     int device;                   /* CUDA ordinal */
+    int periodic_y;               /* 0: the reference's Dirichlet grids. 1: y periodic on every
+                                     level (ny nodes, ny_l = 2 ny_(l-1); y has ny+2 entries whose
+                                     first and last are the wrapped neighbours), the operator's
+                                     s on row 0 and n on row ny-1 couple across the wrap */
 } gmg_problem_desc;
 
 /* gmg::CycleSpec, include/gmg/cycle.hpp:23-39 (+ SmootherSpec) */

@@ -19,10 +19,23 @@ static int fail(int code, const char* msg) {
 const char* orc_last_error(void) { return g_err; }
 
 enum { K_RICH, K_JACOBI, K_GS, K_SOR, K_ILU0, K_TRIX, K_TRIY, K_ADI, K_GSTRIX, K_GSTRIY, K_GSADI };
-enum { CS_CART, CS_CYL, CS_SPH };
+enum { CS_CART, CS_CYL, CS_SPH, CS_POLAR };
+
+/* CS_POLAR has no reference counterpart (the reference has cartesian, cylindrical
+ * and spherical only, mesh.hpp:8): BASELINE config 3's polar Poisson problem,
+ * restated with the reference's own discretisation rules and marked "parity
+ * unpinned". x = r in [0.1, 1] (Dirichlet, graded like the
+ * cylindrical radius), y = theta / (2 pi) in [0, 1) PERIODIC: level l has
+ * coarse_ny * 2^(l-1) nodes y_j = (j+1)/ny (node ny-1 at 1 == 0); y[0] = 0 and
+ * y[ny+1] = (ny+1)/ny are the wrapped neighbours. Flux form as stencil.cpp:49-127
+ * with x-flux face weight r, y-flux face weight 1/(2 pi)^2 and transverse measures
+ * dy and int dr/r = log(r_e/r_w): -(r u_r)_r - (1/r) u_theta theta times the cell.
+ * Every y index wraps (apply, transfers, the level-1 factorization); only the
+ * pointwise smoothers (jacobi, richardson) are defined on it. */
 
 typedef struct {
     int level, nx, ny, coords;
+    int per; /* y periodic (CS_POLAR) */
     double *x, *y; /* nx+2 / ny+2 node coordinates including the boundary */
 } grid_t;
 
@@ -67,7 +80,7 @@ static void axis_range(int cs, int axis, double* lo, double* hi) {
     const double pi = 3.14159265358979323846;
     *lo = 0.0;
     *hi = 1.0;
-    if (cs == CS_CYL && axis == 0) *lo = 0.1;
+    if ((cs == CS_CYL || cs == CS_POLAR) && axis == 0) *lo = 0.1;
     if (cs == CS_SPH) {
         if (axis == 0) {
             *lo = 0.1;
@@ -96,10 +109,15 @@ static int physical_axis(int n, double factor, int cs, int axis, double* p) {
 
 /* ---- assembly: stencil.cpp:49-127 --------------------------------------- */
 
-static double face_weight_x(int cs, double x) { return cs == CS_CART ? 1.0 : (cs == CS_CYL ? x : x * x); }
-static double face_weight_y(int cs, double y) { return cs == CS_SPH ? sin(y) : 1.0; }
+static const double kPolarPi = 3.14159265358979323846;
+static double face_weight_x(int cs, double x) {
+    return cs == CS_CART ? 1.0 : ((cs == CS_CYL || cs == CS_POLAR) ? x : x * x);
+}
+static double face_weight_y(int cs, double y) {
+    return cs == CS_SPH ? sin(y) : (cs == CS_POLAR ? 1.0 / (4.0 * kPolarPi * kPolarPi) : 1.0);
+}
 static double cell_measure_x(int cs, double lo, double hi) {
-    return cs == CS_CYL ? 0.5 * (hi * hi - lo * lo) : hi - lo;
+    return cs == CS_CYL ? 0.5 * (hi * hi - lo * lo) : (cs == CS_POLAR ? log(hi / lo) : hi - lo);
 }
 static double cell_measure_y(int cs, double lo, double hi) {
     return cs == CS_SPH ? cos(lo) - cos(hi) : hi - lo;
@@ -133,8 +151,8 @@ static void assemble(const grid_t* g, double alpha, double beta, op_t* op) {
             op->c[k] = ce + cw + cn + csth;
             if (i + 1 < nx) op->e[k] = -ce;
             if (i > 0) op->w[k] = -cw;
-            if (j + 1 < ny) op->n[k] = -cn;
-            if (j > 0) op->s[k] = -csth;
+            if (j + 1 < ny || g->per) op->n[k] = -cn;
+            if (j > 0 || g->per) op->s[k] = -csth;
         }
     }
 }
@@ -166,8 +184,13 @@ static void op_apply(const grid_t* g, const op_t* A, const double* x, double* y)
             double acc = A->c[k] * x[k];
             if (i > 0) acc += A->w[k] * x[k - 1];
             if (i + 1 < nx) acc += A->e[k] * x[k + 1];
-            if (j > 0) acc += A->s[k] * x[k - nx];
-            if (j + 1 < ny) acc += A->n[k] * x[k + nx];
+            if (g->per) {
+                acc += A->s[k] * x[(size_t)((j + ny - 1) % ny) * nx + i];
+                acc += A->n[k] * x[(size_t)((j + 1) % ny) * nx + i];
+            } else {
+                if (j > 0) acc += A->s[k] * x[k - nx];
+                if (j + 1 < ny) acc += A->n[k] * x[k + nx];
+            }
             y[k] = acc;
         }
 }
@@ -184,16 +207,35 @@ static void op_residual(const grid_t* g, const op_t* A, const double* x, const d
 static int chol_factor(orc_problem* p) {
     const grid_t* g = &p->g[0];
     const op_t* A = &p->op[0];
-    const int n = (int)nlev(g), bw = g->nx, nx = g->nx;
+    const int n = (int)nlev(g), nx = g->nx;
+    const int bw = g->per ? n - 1 : g->nx; /* periodic: the dense lower triangle */
     p->chol_n = n;
     p->chol_bw = bw;
     p->band = dalloc((size_t)(bw + 1) * n);
     double* B = p->band;
 #define ENT(d, k) B[(size_t)(d) * n + (k)]
-    for (int k = 0; k < n; ++k) {
-        ENT(0, k) = A->c[k];
-        if (k % nx != 0) ENT(1, k) = A->w[k];
-        if (k >= nx) ENT(bw, k) = A->s[k];
+    if (g->per) {
+        /* couplings accumulated in apply's order c, w, e, s, n with y wrapped */
+        const int ny = g->ny;
+        double* D = dalloc((size_t)n * n);
+        for (int k = 0; k < n; ++k) {
+            const int i = k % nx, j = k / nx;
+            D[(size_t)k * n + k] = D[(size_t)k * n + k] + A->c[k];
+            if (i > 0) D[(size_t)k * n + k - 1] = D[(size_t)k * n + k - 1] + A->w[k];
+            if (i + 1 < nx) D[(size_t)k * n + k + 1] = D[(size_t)k * n + k + 1] + A->e[k];
+            const int ks = ((j + ny - 1) % ny) * nx + i, kn = ((j + 1) % ny) * nx + i;
+            D[(size_t)k * n + ks] = D[(size_t)k * n + ks] + A->s[k];
+            D[(size_t)k * n + kn] = D[(size_t)k * n + kn] + A->n[k];
+        }
+        for (int k = 0; k < n; ++k)
+            for (int d = 0; d <= k; ++d) ENT(d, k) = D[(size_t)k * n + k - d];
+        free(D);
+    } else {
+        for (int k = 0; k < n; ++k) {
+            ENT(0, k) = A->c[k];
+            if (k % nx != 0) ENT(1, k) = A->w[k];
+            if (k >= nx) ENT(bw, k) = A->s[k];
+        }
     }
     for (int jc = 0; jc < n; ++jc) {
         double d = ENT(0, jc);
@@ -239,14 +281,21 @@ static double odd_weight(const double* xf, const double* xc, int q) {
 }
 
 static int require_nested(const grid_t* c, const grid_t* f) {
-    if (f->level != c->level + 1 || f->nx != 2 * c->nx + 1 || f->ny != 2 * c->ny + 1)
+    const int fny = f->per ? 2 * c->ny : 2 * c->ny + 1;
+    if (f->level != c->level + 1 || f->nx != 2 * c->nx + 1 || f->ny != fny)
         return fail(ORC_ERR_LOGIC, "levels are not parent and child");
     return ORC_OK;
 }
 
+/* periodic y: coarse node 0 is coarse node cny (y = 0 == 1) */
+static double prolong_cv(const grid_t* cg, const double* cv, int qx, int qy) {
+    if (cg->per && qy == 0) qy = cg->ny;
+    if (qx < 1 || qx > cg->nx || qy < 1 || qy > cg->ny) return 0.0;
+    return cv[(size_t)(qy - 1) * cg->nx + (qx - 1)];
+}
+
 static void prolong(const grid_t* cg, const grid_t* fg, const double* cv, double* fv) {
-    const int cnx = cg->nx, cny = cg->ny;
-#define CV(qx, qy) (((qx) < 1 || (qx) > cnx || (qy) < 1 || (qy) > cny) ? 0.0 : cv[(size_t)((qy)-1) * cnx + ((qx)-1)])
+#define CV(qx, qy) prolong_cv(cg, cv, (qx), (qy))
     for (int j = 0; j < fg->ny; ++j) {
         const int pj = j + 1;
         for (int i = 0; i < fg->nx; ++i) {
@@ -291,7 +340,8 @@ static void restrict_(const grid_t* fg, const grid_t* cg, const double* fv, doub
             for (int dj = -1; dj <= 1; ++dj)
                 for (int di = -1; di <= 1; ++di)
                     acc += wx[di + 1] * wy[dj + 1] *
-                           fv[(size_t)(2 * qj + dj - 1) * fnx + (2 * qi + di - 1)];
+                           fv[(size_t)(fg->per ? (2 * qj + dj - 1) % fg->ny : 2 * qj + dj - 1) * fnx +
+                              (2 * qi + di - 1)];
             cv[(size_t)(qj - 1) * cg->nx + (qi - 1)] = acc / (sx * sy);
         }
     }
@@ -463,6 +513,8 @@ static int sm_setup(smoother_t* s, int kind, double omega, const grid_t* g, cons
     memset(s, 0, sizeof *s);
     int st = check_omega(kind, omega);
     if (st) return st;
+    if (g->per && kind != K_JACOBI && kind != K_RICH)
+        return fail(ORC_ERR_INVALID, "smoother: periodic (polar) grids support jacobi and richardson only");
     s->kind = kind;
     s->omega = omega;
     s->g = g;
@@ -641,6 +693,15 @@ orc_problem* orc_problem_create(int levels, int cnx, int cny, double fx, double 
     if (cnx < 1 || cny < 1) { fail(ORC_ERR_INVALID, "coarse_n: interior counts must be >= 1"); return NULL; }
     if (!(fx > 0.0) || !(fy > 0.0)) { fail(ORC_ERR_INVALID, "grading: factors must be > 0"); return NULL; }
     if (!(alpha > 0.0) || !(beta > 0.0)) { fail(ORC_ERR_INVALID, "alpha/beta must be > 0"); return NULL; }
+    if (coords < CS_CART || coords > CS_POLAR) { fail(ORC_ERR_INVALID, "coords: unknown coordinate system"); return NULL; }
+    if (coords == CS_POLAR && fy != 1.0) {
+        fail(ORC_ERR_INVALID, "grading_y: the periodic polar theta axis must be uniform");
+        return NULL;
+    }
+    if (coords == CS_POLAR && cny < 2) {
+        fail(ORC_ERR_INVALID, "coarse_n: the periodic polar theta axis needs >= 2 nodes");
+        return NULL;
+    }
     orc_problem* p = (orc_problem*)calloc(1, sizeof *p);
     p->L = levels;
     p->g = (grid_t*)calloc((size_t)levels, sizeof(grid_t));
@@ -649,25 +710,33 @@ orc_problem* orc_problem_create(int levels, int cnx, int cny, double fx, double 
     grid_t* f = &p->g[levels - 1];
     f->level = levels;
     f->nx = ((cnx + 1) << (levels - 1)) - 1;
-    f->ny = ((cny + 1) << (levels - 1)) - 1;
+    f->ny = coords == CS_POLAR ? cny << (levels - 1) : ((cny + 1) << (levels - 1)) - 1;
     f->coords = coords;
+    f->per = coords == CS_POLAR;
     f->x = dalloc((size_t)f->nx + 2);
     f->y = dalloc((size_t)f->ny + 2);
-    if (physical_axis(f->nx, fx, coords, 0, f->x) || physical_axis(f->ny, fy, coords, 1, f->y)) {
+    if (physical_axis(f->nx, fx, coords, 0, f->x) ||
+        (!f->per && physical_axis(f->ny, fy, coords, 1, f->y))) {
         orc_problem_destroy(p);
         return NULL;
     }
+    if (f->per)
+        for (int q = 0; q <= f->ny + 1; ++q) f->y[q] = (double)q / (double)f->ny;
     for (int l = levels - 1; l >= 1; --l) {
         const grid_t* fg = &p->g[l];
         grid_t* cg = &p->g[l - 1];
         cg->level = l;
         cg->nx = (fg->nx - 1) / 2;
-        cg->ny = (fg->ny - 1) / 2;
+        cg->ny = fg->per ? fg->ny / 2 : (fg->ny - 1) / 2;
         cg->coords = coords;
+        cg->per = fg->per;
         cg->x = dalloc((size_t)cg->nx + 2);
         cg->y = dalloc((size_t)cg->ny + 2);
         for (int q = 0; q < cg->nx + 2; ++q) cg->x[q] = fg->x[2 * q];
-        for (int q = 0; q < cg->ny + 2; ++q) cg->y[q] = fg->y[2 * q];
+        if (cg->per)
+            for (int q = 0; q <= cg->ny + 1; ++q) cg->y[q] = (double)q / (double)cg->ny;
+        else
+            for (int q = 0; q < cg->ny + 2; ++q) cg->y[q] = fg->y[2 * q];
     }
     /* MultilevelProblem, cycle.cpp:25-30 */
     for (int l = 0; l < levels; ++l) assemble(&p->g[l], alpha, beta, &p->op[l]);

@@ -23,7 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libgmg_ref_capi.so")
 
-COORDS = {"cartesian": 0, "cylindrical": 1, "spherical": 2}
+COORDS = {"cartesian": 0, "cylindrical": 1, "spherical": 2, "polar": 3}  # polar: oracle and device only (no reference)
 SMOOTHERS = ["richardson", "jacobi", "gauss_seidel", "sor", "ilu0", "tri_x", "tri_y",
              "adi", "gstri_x", "gstri_y", "gsadi"]
 CYCLES = {"V": 0, "W": 1, "F": 2}

@@ -38,12 +38,21 @@ constexpr int kWarp = 32;
 // Rows [w0, w1) are the rows a kernel produces (the whole grid, or one rank's
 // slab of it when a level is sharded); domain tests always use the
 // full [0, ny).
+// per: the level is periodic in y (polar theta, BASELINE config 3): every row
+// index wraps modulo ny, and no row is outside the domain.
 struct Grid {
     int nx, ny;
     long long pitch;
     int w0 = 0, w1 = 0;
-    __host__ __device__ long long at(int i, int j) const { return (long long)j * pitch + i; }
-    __host__ __device__ bool inside(int i, int j) const { return i >= 0 && i < nx && j >= 0 && j < ny; }
+    int per = 0;
+    __host__ __device__ int wrap(int j) const {
+        if (!per) return j;
+        const int r = j % ny;
+        return r < 0 ? r + ny : r;
+    }
+    __host__ __device__ bool row_ok(int j) const { return per || (j >= 0 && j < ny); }
+    __host__ __device__ long long at(int i, int j) const { return (long long)wrap(j) * pitch + i; }
+    __host__ __device__ bool inside(int i, int j) const { return i >= 0 && i < nx && row_ok(j); }
 };
 
 // ---------------------------------------------------------------------------

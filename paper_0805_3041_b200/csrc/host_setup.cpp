@@ -37,7 +37,7 @@ std::vector<double> graded_unit_axis(int n, double ratio) {
 // axis_range (mesh.cpp:25-36) then physical_axis (mesh.cpp:79-93).
 std::vector<double> mapped_axis(int n, double ratio, int coords, int axis) {
     double lo = 0.0, hi = 1.0;
-    if (coords == 1 && axis == 0) lo = 0.1;
+    if ((coords == 1 || coords == 3) && axis == 0) lo = 0.1;
     if (coords == 2) {
         lo = 0.1;
         if (axis == 1) hi = kPi - 0.1;
@@ -52,11 +52,22 @@ std::vector<double> mapped_axis(int n, double ratio, int coords, int axis) {
     return p;
 }
 
-// Flux-form coefficients (stencil.cpp:49-73).
-double face_x(int cs, double x) { return cs == 0 ? 1.0 : (cs == 1 ? x : x * x); }
-double face_y(int cs, double y) { return cs == 2 ? std::sin(y) : 1.0; }
-double measure_x(int cs, double a, double b) { return cs == 1 ? 0.5 * (b * b - a * a) : b - a; }
+// Flux-form coefficients (stencil.cpp:49-73); polar (cs 3) as in host_setup.h.
+const double kPolarThetaWeight = 1.0 / (4.0 * kPi * kPi);
+double face_x(int cs, double x) { return cs == 0 ? 1.0 : ((cs == 1 || cs == 3) ? x : x * x); }
+double face_y(int cs, double y) { return cs == 2 ? std::sin(y) : (cs == 3 ? kPolarThetaWeight : 1.0); }
+double measure_x(int cs, double a, double b) {
+    return cs == 1 ? 0.5 * (b * b - a * a) : (cs == 3 ? std::log(b / a) : b - a);
+}
 double measure_y(int cs, double a, double b) { return cs == 2 ? std::cos(a) - std::cos(b) : b - a; }
+
+// y = theta / (2 pi) on a periodic axis of ny nodes: y[q] = q / ny for q = 0 .. ny+1
+// (q = 0 and ny+1 are the wrapped neighbours of the first and last node).
+std::vector<double> periodic_axis(int ny) {
+    std::vector<double> y(static_cast<std::size_t>(ny) + 2);
+    for (int q = 0; q <= ny + 1; ++q) y[q] = static_cast<double>(q) / static_cast<double>(ny);
+    return y;
+}
 
 void assemble_level(Level& L, int cs, double alpha, double beta) {
     const int nx = L.nx, ny = L.ny;
@@ -86,8 +97,8 @@ void assemble_level(Level& L, int cs, double alpha, double beta) {
             L.c[k] = fe + fw + fn + fs;
             if (i + 1 < nx) L.e[k] = -fe;
             if (i > 0) L.w[k] = -fw;
-            if (j + 1 < ny) L.n[k] = -fn;
-            if (j > 0) L.s[k] = -fs;
+            if (j + 1 < ny || L.periodic) L.n[k] = -fn;
+            if (j > 0 || L.periodic) L.s[k] = -fs;
         }
     }
 }
@@ -101,8 +112,32 @@ std::vector<Level> build_problem(int num_levels, int cnx, int cny, double gx, do
     if (num_levels < 1) throw std::invalid_argument("levels: must be >= 1");
     if (cnx < 1 || cny < 1) throw std::invalid_argument("coarse_n: interior counts must be >= 1");
     if (!(gx > 0.0) || !(gy > 0.0)) throw std::invalid_argument("grading: factors must be > 0");
-    if (coords < 0 || coords > 2) throw std::invalid_argument("coords: unknown coordinate system");
+    if (coords < 0 || coords > 3) throw std::invalid_argument("coords: unknown coordinate system");
     if (!(alpha > 0.0) || !(beta > 0.0)) throw std::invalid_argument("alpha/beta must be > 0");
+    if (coords == 3) {
+        if (gy != 1.0) throw std::invalid_argument("grading_y: the periodic polar theta axis must be uniform");
+        if (cny < 2) throw std::invalid_argument("coarse_n: the periodic polar theta axis needs >= 2 nodes");
+        std::vector<Level> lv(static_cast<std::size_t>(num_levels));
+        Level& f = lv.back();
+        f.level = num_levels;
+        f.nx = ((cnx + 1) << (num_levels - 1)) - 1;
+        f.x = mapped_axis(f.nx, gx, coords, 0);
+        for (int l = num_levels; l >= 1; --l) {
+            Level& L = lv[l - 1];
+            L.level = l;
+            L.periodic = true;
+            L.ny = cny << (l - 1);
+            L.y = periodic_axis(L.ny);
+            if (l < num_levels) {
+                const Level& fine = lv[l];
+                L.nx = (fine.nx - 1) / 2;
+                L.x.resize(static_cast<std::size_t>(L.nx) + 2);
+                for (std::size_t q = 0; q < L.x.size(); ++q) L.x[q] = fine.x[2 * q];
+            }
+        }
+        for (Level& L : lv) assemble_level(L, coords, alpha, beta);
+        return lv;
+    }
     std::vector<Level> lv(static_cast<std::size_t>(num_levels));
     Level& f = lv.back();
     f.level = num_levels;
@@ -153,7 +188,7 @@ std::vector<double> cholesky_band(const double* c, const double* w, const double
 }
 
 CoefClass classify(int nx, int ny, const double* c, const double* n, const double* s, const double* e,
-                   const double* w) {
+                   const double* w, bool periodic) {
     CoefClass cc;
     const std::size_t N = static_cast<std::size_t>(nx) * ny;
     // reference interior values (the row/column that has the neighbour)
@@ -166,8 +201,8 @@ CoefClass classify(int nx, int ny, const double* c, const double* n, const doubl
     for (std::size_t k = 0; k < N && isconst; ++k) {
         const int i = static_cast<int>(k % nx), j = static_cast<int>(k / nx);
         isconst = same_bits(c[k], C) && same_bits(w[k], i > 0 ? W : 0.0) &&
-                  same_bits(e[k], i + 1 < nx ? E : 0.0) && same_bits(s[k], j > 0 ? S : 0.0) &&
-                  same_bits(n[k], j + 1 < ny ? Nn : 0.0);
+                  same_bits(e[k], i + 1 < nx ? E : 0.0) && same_bits(s[k], (j > 0 || periodic) ? S : 0.0) &&
+                  same_bits(n[k], (j + 1 < ny || periodic) ? Nn : 0.0);
     }
     if (isconst) {
         cc.kind = COEF_CONST;
@@ -185,7 +220,8 @@ CoefClass classify(int nx, int ny, const double* c, const double* n, const doubl
             const std::size_t k = static_cast<std::size_t>(j) * nx + i;
             const double Si = ny > 1 ? s[static_cast<std::size_t>(nx) + i] : 0.0;
             rowx = same_bits(c[k], c[i]) && same_bits(w[k], w[i]) && same_bits(e[k], e[i]) &&
-                   same_bits(s[k], j > 0 ? Si : 0.0) && same_bits(n[k], j + 1 < ny ? n[i] : 0.0);
+                   same_bits(s[k], (j > 0 || periodic) ? Si : 0.0) &&
+                   same_bits(n[k], (j + 1 < ny || periodic) ? n[i] : 0.0);
         }
     if (rowx) {
         cc.kind = COEF_ROWX;
@@ -224,7 +260,57 @@ void restrict_weights(const std::vector<double>& xf, const std::vector<double>& 
     }
 }
 
+double polar_theta_weight() { return kPolarThetaWeight; }
+
+std::vector<double> cholesky_periodic(const double* c, const double* w, const double* e, const double* s,
+                                      const double* n, int nx, int ny) {
+    const int N = nx * ny, bw = N - 1;
+    // dense lower triangle of A (row k, column m < k), couplings accumulated in
+    // the order c, w, e, s, n of apply (stencil.cpp:133-137) with y wrapped
+    std::vector<double> A(static_cast<std::size_t>(N) * N, 0.0);
+    auto at = [&](int r, int q) -> double& { return A[static_cast<std::size_t>(r) * N + q]; };
+    for (int k = 0; k < N; ++k) {
+        const int i = k % nx, j = k / nx;
+        at(k, k) = at(k, k) + c[k];
+        if (i > 0) at(k, k - 1) = at(k, k - 1) + w[k];
+        if (i + 1 < nx) at(k, k + 1) = at(k, k + 1) + e[k];
+        const int js = (j + ny - 1) % ny, jn = (j + 1) % ny;
+        at(k, js * nx + i) = at(k, js * nx + i) + s[k];
+        at(k, jn * nx + i) = at(k, jn * nx + i) + n[k];
+    }
+    std::vector<double> band(static_cast<std::size_t>(bw + 1) * N, 0.0);
+    auto B = [&](int d, int k) -> double& { return band[static_cast<std::size_t>(d) * N + k]; };
+    for (int k = 0; k < N; ++k)
+        for (int d = 0; d <= k; ++d) B(d, k) = at(k, k - d);
+    for (int col = 0; col < N; ++col) {
+        double d = B(0, col);
+        for (int m = std::max(0, col - bw); m < col; ++m) {
+            const double l = B(col - m, col);
+            d -= l * l;
+        }
+        if (!(d > 0.0)) throw std::runtime_error("BandedCholesky: matrix not positive definite");
+        const double piv = std::sqrt(d);
+        B(0, col) = piv;
+        for (int row = col + 1; row <= std::min(N - 1, col + bw); ++row) {
+            double a = B(row - col, row);
+            for (int m = std::max(0, row - bw); m < col; ++m) a -= B(row - m, row) * B(col - m, col);
+            B(row - col, row) = a / piv;
+        }
+    }
+    return band;
+}
+
 std::string check_nested(const Level& coarse, const Level& fine) {
+    if (fine.periodic != coarse.periodic) return "levels are not parent and child";
+    if (fine.periodic) {
+        if (fine.level != coarse.level + 1 || fine.nx != 2 * coarse.nx + 1 || fine.ny != 2 * coarse.ny)
+            return "levels are not parent and child";
+        for (int q = 0; q < coarse.nx + 2; ++q)
+            if (std::abs(coarse.x[q] - fine.x[2 * q]) > 1e-14) return "grids are not nested";
+        for (int q = 0; q <= coarse.ny; ++q)
+            if (std::abs(coarse.y[q] - fine.y[2 * q]) > 1e-14) return "grids are not nested";
+        return "";
+    }
     if (fine.level != coarse.level + 1 || fine.nx != 2 * coarse.nx + 1 || fine.ny != 2 * coarse.ny + 1)
         return "levels are not parent and child";
     for (int q = 0; q < coarse.nx + 2; ++q)

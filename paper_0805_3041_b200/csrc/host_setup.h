@@ -12,18 +12,30 @@ namespace gmg_host {
 
 struct Level {
     int level = 1, nx = 0, ny = 0;
+    bool periodic = false;                  // y periodic (polar theta): ny nodes, no y boundary
     std::vector<double> x, y;               // nx+2 / ny+2 node coordinates
     std::vector<double> c, n, s, e, w;      // nx*ny each, reference layout
 };
 
 // gmg::build_hierarchy + gmg::assemble (mesh.cpp:48-138, stencil.cpp:49-127).
 // Throws std::invalid_argument with the reference's messages.
+// coords 3 (polar, no reference counterpart, BASELINE
+// config 3): x = r in [0.1, 1] (Dirichlet, graded like cylindrical), y = theta
+// / (2 pi) in [0, 1) periodic with coarse_ny * 2^(l-1) nodes on level l at
+// y_j = (j+1)/ny (node ny-1 sits at 1 == 0); the reference's flux form with
+// x-flux face weight r, y-flux face weight 1/(2 pi)^2 and transverse measures
+// dy and int dr/r = log(r_e / r_w): the polar Laplacian times r, i.e. the
+// variable-coefficient 5-point stencil with coefficients r and 1/r.
 std::vector<Level> build_problem(int num_levels, int coarse_nx, int coarse_ny, double grading_x,
                                  double grading_y, int coords, double alpha, double beta);
 
 // BandedCholesky ctor (stencil.cpp:155-188): band[d*n + k] = L(k, k-d),
 // half bandwidth nx. Throws std::runtime_error if not SPD.
 std::vector<double> cholesky_band(const double* c, const double* w, const double* s, int nx, int ny);
+// The same factorization for a y-periodic level: the dense lower triangle
+// (half bandwidth n-1, the wrap couplings of rows 0 and ny-1 included).
+std::vector<double> cholesky_periodic(const double* c, const double* w, const double* e, const double* s,
+                                      const double* n, int nx, int ny);
 
 // Operator classification (see common.cuh).
 enum CoefKind { COEF_CONST = 0, COEF_ROWX = 1, COEF_FIELD = 2 };
@@ -32,8 +44,9 @@ struct CoefClass {
     double c = 0, w = 0, e = 0, s = 0, n = 0;            // CONST
     std::vector<double> rc, rw, re, rs, rn;              // ROWX tables (length nx)
 };
+// periodic: y-periodic level (s on row 0 and n on the last row couple across the wrap).
 CoefClass classify(int nx, int ny, const double* c, const double* n, const double* s,
-                   const double* e, const double* w);
+                   const double* e, const double* w, bool periodic = false);
 
 // odd_weight (transfer.cpp:26-28) tables.
 // Prolongation (fine level f from coarse cx): tx[i] for fine column i (odd node i+1).
@@ -43,6 +56,9 @@ void restrict_weights(const std::vector<double>& xf, const std::vector<double>& 
                       std::vector<double>& ww, std::vector<double>& we, std::vector<double>& sw);
 // require_nested (transfer.cpp:10-22); returns an error message or "".
 std::string check_nested(const Level& coarse, const Level& fine);
+
+// Polar face weight of the theta flux, 1/(2 pi)^2 (coords 3).
+double polar_theta_weight();
 
 // factor_ilu0 (smoother.cpp:187-210) on the reference arrays: lw, ls, d
 // (nx*ny each; ue/un are the operator's e/n). Throws std::runtime_error

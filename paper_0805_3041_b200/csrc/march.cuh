@@ -77,6 +77,10 @@ struct ProlongRaw {
 };
 __device__ __forceinline__ ProlongRaw prolong_fetch(const Prolong& P, int i, int j, int fnx, int fny) {
     ProlongRaw r{0.0, 0.0, 0.0, 0.0, 0.0};
+    if (P.cg.per) {  // periodic y (fine rows 2 ny_c): wrap first, the coarse rows wrap in cval
+        j %= fny;
+        if (j < 0) j += fny;
+    }
     if (i < 0 || i >= fnx || j < 0 || j >= fny) return r;
     const int pi = i + 1, pj = j + 1;
     const int ci = (pi & 1) ? (pi - 1) / 2 - 1 : pi / 2 - 1;  // left/only coarse column
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
     for (int p = 0; p < PF; ++p) {
         const int Jf = Jbeg + p;
         q[p] = src.fetch(i, Jf);
-        gq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(g + fg.at(i, Jf - 1)) : 0.0;
+        gq[p] = (col_in && fg.row_ok(Jf - 1)) ? __ldg(g + fg.at(i, Jf - 1)) : 0.0;
     }
     for (int Jb = Jbeg; Jb <= Jend; Jb += PF) {
 #pragma unroll
@@ -237,10 +241,10 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
             {
                 const int Jf = J + PF;
                 q[p] = src.fetch(i, Jf);
-                gq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(g + fg.at(i, Jf - 1)) : 0.0;
+                gq[p] = (col_in && fg.row_ok(Jf - 1)) ? __ldg(g + fg.at(i, Jf - 1)) : 0.0;
             }
-            const bool row_in = J >= 0 && J < fg.ny;
-            const double x0 = (col_in && row_in) ? src.make(raw, i, J) : 0.0;
+            const bool row_in = fg.row_ok(J);
+            const double x0 = (col_in && row_in) ? src.make(raw, i, fg.wrap(J)) : 0.0;
             if (STORE_X0 && owner && J >= j0 && J < j1) x0out[fg.at(i, J)] = x0;
             a = b;
             b = c;
@@ -250,8 +254,8 @@ __global__ void __launch_bounds__(TW) k_resid(Grid fg, Coef A, Src src, const do
             const double xr = t < TW - 1 ? xs[(J - 1) & 1][t + 1] : 0.0;
             xs[J & 1][t] = x0;
             double d = 0.0;
-            if (col_in && R >= 0 && R < fg.ny) {
-                const double ax = stencil_apply(A, cix(i, fg.nx), R, b, xl, xr, a, c);
+            if (col_in && fg.row_ok(R)) {
+                const double ax = stencil_apply(A, cix(i, fg.nx), fg.wrap(R), b, xl, xr, a, c);
                 d = neg ? ax - gR : gR - ax;  // smoother defect (Ax - g) or residual (g - Ax)
             }
             if (STORE_D && owner && R >= j0 && R < j1) dout[fg.at(i, R)] = d;
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(TW) k_omega_terms(Grid fg, Coef A, SrcProlong 
     for (int p = 0; p < PF; ++p) {
         const int Jf = Jbeg + p;
         q[p] = src.fetch(i, Jf);
-        dq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(d + fg.at(i, Jf - 1)) : 0.0;
+        dq[p] = (col_in && fg.row_ok(Jf - 1)) ? __ldg(d + fg.at(i, Jf - 1)) : 0.0;
     }
     for (int Jb = Jbeg; Jb <= Jend; Jb += PF) {
 #pragma unroll
@@ -319,9 +323,9 @@ __global__ void __launch_bounds__(TW) k_omega_terms(Grid fg, Coef A, SrcProlong 
             {
                 const int Jf = J + PF;
                 q[p] = src.fetch(i, Jf);
-                dq[p] = (col_in && Jf - 1 >= 0 && Jf - 1 < fg.ny) ? __ldg(d + fg.at(i, Jf - 1)) : 0.0;
+                dq[p] = (col_in && fg.row_ok(Jf - 1)) ? __ldg(d + fg.at(i, Jf - 1)) : 0.0;
             }
-            const double cj = (col_in && J >= 0 && J < fg.ny) ? src.make(raw, i, J) : 0.0;
+            const double cj = (col_in && fg.row_ok(J)) ? src.make(raw, i, fg.wrap(J)) : 0.0;
             a = b;
             b = c;
             c = cj;

@@ -14,7 +14,7 @@ namespace gmg_dev {
 // (i even) pair at row j, zeros outside the interior
 __device__ __forceinline__ double2 ld_pair(const double* a, const Grid& g, int i, int j) {
     double2 r = make_double2(0.0, 0.0);
-    if (j < 0 || j >= g.ny) return r;
+    if (!g.row_ok(j)) return r;
     const double* p = a + g.at(i, j);
     if (i >= 0 && i + 1 < g.nx) return __ldg(reinterpret_cast<const double2*>(p));
     if (i >= 0 && i < g.nx) r.x = __ldg(p);
@@ -52,6 +52,10 @@ struct Pair2Raw {
 };
 __device__ __forceinline__ Pair2Raw prolong2_fetch(const Prolong& P, int i, int j, int fny) {
     Pair2Raw r{0.0, 0.0, 0.0, 0.0, 0.0};
+    if (P.cg.per) {  // periodic y (fine rows 2 ny_c): wrap first, the coarse rows wrap in cval
+        j %= fny;
+        if (j < 0) j += fny;
+    }
     if (j < 0 || j >= fny) return r;
     const int m = i / 2;  // i even (may be negative only on the halo, handled by cval)
     const int pj = j + 1;
@@ -169,8 +173,8 @@ __global__ void __launch_bounds__(TW) k_smooth2(Grid fg, Coef A, Src src, OmegaS
             const double2 gnew = gq[p];
             q[p] = src.fetch(i, J + PF);
             gq[p] = M > 0 ? ld_pair(g, fg, i, J + PF) : make_double2(0.0, 0.0);
-            const bool row_in = J >= 0 && J < fg.ny;
-            double2 nv = row_in ? src.make(raw, i, J) : make_double2(0.0, 0.0);
+            const bool row_in = fg.row_ok(J);
+            double2 nv = row_in ? src.make(raw, i, fg.wrap(J)) : make_double2(0.0, 0.0);
             if (!in0) nv.x = 0.0;
             if (!in1) nv.y = 0.0;
             if constexpr (M == 0) {
@@ -194,11 +198,11 @@ __global__ void __launch_bounds__(TW) k_smooth2(Grid fg, Coef A, Src src, OmegaS
                     const double xl = t > 0 ? sh[pb][l][t - 1].y : 0.0;
                     const double xr = t < TW - 1 ? sh[pb][l][t + 1].x : 0.0;
                     const double2 c = win[l][1], dn = win[l][0], up = win[l][2];
-                    const int Rc = cix(R, fg.ny);
+                    const int Rc = fg.per ? fg.wrap(R) : cix(R, fg.ny);
                     const double y0 = jacobi_point(A, cix(i, fg.nx), Rc, c.x, xl, c.y, dn.x, up.x, gring[l].x, omega_damp);
                     const double y1 =
                         jacobi_point(A, cix(i + 1, fg.nx), Rc, c.y, c.x, xr, dn.y, up.y, gring[l].y, omega_damp);
-                    const bool rin = R >= 0 && R < fg.ny;
+                    const bool rin = fg.row_ok(R);
                     nv = make_double2((rin && in0) ? y0 : 0.0, (rin && in1) ? y1 : 0.0);
                 }
                 const int RM = J - M;

@@ -169,7 +169,10 @@ struct Lev {
     double* scr[2] = {nullptr, nullptr};  // smoother scratch (adi/gsadi/ilu0), allocated on demand
     double* scrmem = nullptr;
     int w0 = 0, w1 = 0;  // owned rows; [0, ny) unless the level is sharded
-    Grid grid() const { return Grid{nx, ny, pitch, w0, w1}; }
+    int per = 0;         // periodic in y (polar theta): rows wrap (common.cuh Grid)
+    // the warp-strip kernels (march4.cuh) march non-periodic rows only
+    bool strips() const;
+    Grid grid() const { return Grid{nx, ny, pitch, w0, w1, per}; }
     int rows() const { return w1 - w0; }
     long long n() const { return (long long)nx * ny; }
 };
@@ -666,6 +669,7 @@ static const int kRingMinNx = [] {
     const char* e = getenv("GMG_RING_MIN_NX");
     return e ? atoi(e) : 255;
 }();
+bool Lev::strips() const { return nx >= kRingMinNx && !per; }
 template <int M, class Coef>
 void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const SmoothSrc& s, const double* g,
                        double* out, double wd) {
@@ -678,7 +682,7 @@ void launch_smooth_src(gmg_problem* p, const Lev& L, const Coef& A, const Smooth
             default: throw GmgError{GMG_ERR_LOGIC, "smooth: bad source"};
         }
     } else {
-    if (L.nx >= kRingMinNx) {
+    if (L.strips()) {
         switch (s.kind) {
             case S_ZERO: launch_smooth4_t<M, K3_ZERO>(p, L, A, nullptr, nullptr, s.om, g, out, wd); return;
             case S_U: launch_smooth4_t<M, K3_U>(p, L, A, s.u, nullptr, s.om, g, out, wd); return;
@@ -723,7 +727,7 @@ void launch_smooth(gmg_problem* p, const Lev& L, int M, const SmoothSrc& s, cons
             default: throw GmgError{GMG_ERR_LOGIC, "smooth: M > 4"};
         }
     };
-    if (L.nx >= kRingMinNx) with_coef_big(L, go);  // k_smooth4
+    if (L.strips()) with_coef_big(L, go);  // k_smooth4
     else with_coef(L, go);
 }
 
@@ -776,7 +780,7 @@ void launch_resid4_t(gmg_problem* p, const Lev& L, const Coef& A, const double* 
 // residual of (u, or x+e when e != null) against g; optional outputs.
 void launch_resid(gmg_problem* p, const Lev& L, const double* u, const double* e, const double* g,
                   double* dout, double* x0out, double* gc) {
-    if (L.nx >= kRingMinNx) {
+    if (L.strips()) {
         with_coef_big(L, [&](const auto& A) {
             if (e)
                 launch_resid4_t<true>(p, L, A, u, e, g, dout, x0out, gc);
@@ -1293,6 +1297,7 @@ struct Driver {
             v.ny = L.ny;
             v.pitch = L.pitch;
             v.kind = L.kind;
+            v.per = L.per;
             v.cc = L.cconst;
             v.cr = L.crow;
             v.cf = L.cfield;
@@ -1385,7 +1390,7 @@ struct Driver {
             SrcProlong src{prolong_from(q, l - 1, q->lev(l - 1).buf[uc]), L.nx, L.ny, 0.0};
             double* T0 = q->T;
             double* T1 = q->T + q->lev(q->L).n();
-            if (L.nx >= kRingMinNx) {
+            if (L.strips()) {
                 with_coef_big(L, [&](const auto& A) {
                     using C = std::decay_t<decltype(A)>;
                     set_smem(k_omega4<C>, omega4_smem());
@@ -1561,6 +1566,13 @@ void check_smoother(const gmg_cycle_desc& sp) {
         default:
             throw std::invalid_argument("smoother: unknown kind");
     }
+}
+
+// Periodic (polar) levels define the pointwise smoothers only: the lexicographic
+// and line sweeps would need wrap-around recurrences.
+void check_periodic_kind(const gmg_problem* p, int kind) {
+    if (p->lv[0].per && kind != GMG_SMOOTHER_JACOBI && kind != GMG_SMOOTHER_RICHARDSON)
+        throw std::invalid_argument("smoother: periodic (polar) grids support jacobi and richardson only");
 }
 
 // checks the reference performs inside mg_cycle / smooth_step (cycle.cpp:75-76, smoother.cpp:391)
@@ -1765,6 +1777,7 @@ void solve_core(gmg_problem* p, const gmg_cycle_desc& sp, gmg_solve_report* rep,
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
     check_smoother(sp);
+    check_periodic_kind(p, sp.smoother_kind);
     if (p->dist && sp.smoother_kind != GMG_SMOOTHER_JACOBI)
         throw GmgError{GMG_ERR_UNSUPPORTED, "row slabs: only the jacobi smoother is sharded"};
     const SmSetup* sm = ensure_smoother(p, sp.smoother_kind, sp.smoother_omega);
@@ -1914,6 +1927,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         h.level = l;
         h.nx = ld.nx;
         h.ny = ld.ny;
+        h.periodic = d->periodic_y != 0;
         h.x.assign(ld.x, ld.x + ld.nx + 2);
         h.y.assign(ld.y, ld.y + ld.ny + 2);
         if (l >= 2) {
@@ -1935,7 +1949,8 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         CK(cudaMemset(L.mem, 0, NBUF * L.elems * sizeof(double)));
         for (int b = 0; b < NBUF; ++b) L.buf[b] = L.mem + b * L.elems + L.off0;
         // operator
-        const gmg_host::CoefClass cc = gmg_host::classify(ld.nx, ld.ny, ld.c, ld.n, ld.s, ld.e, ld.w);
+        L.per = d->periodic_y != 0;
+        const gmg_host::CoefClass cc = gmg_host::classify(ld.nx, ld.ny, ld.c, ld.n, ld.s, ld.e, ld.w, L.per != 0);
         L.kind = cc.kind;
         if (cc.kind == gmg_host::COEF_CONST) {
             L.cconst = CoefConst{cc.c, cc.w, cc.e, cc.s, cc.n, 0.0, 0, 0, 0.0};
@@ -2013,9 +2028,11 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
     // level-1 factorization (MultilevelProblem ctor, cycle.cpp:29)
     {
         const gmg_level_desc& ld = d->levels[0];
-        std::vector<double> band = gmg_host::cholesky_band(ld.c, ld.w, ld.s, ld.nx, ld.ny);
+        const bool per = d->periodic_y != 0;
+        std::vector<double> band = per ? gmg_host::cholesky_periodic(ld.c, ld.w, ld.e, ld.s, ld.n, ld.nx, ld.ny)
+                                       : gmg_host::cholesky_band(ld.c, ld.w, ld.s, ld.nx, ld.ny);
         p->cn = ld.nx * ld.ny;
-        p->cbw = ld.nx;
+        p->cbw = per ? p->cn - 1 : ld.nx;
         CK(dmalloc(&p->band, band.size() * sizeof(double)));
         CK(cudaMemcpy(p->band, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice));
         CK(dmalloc(&p->cscr, std::max(1, p->cn) * sizeof(double)));
@@ -2079,6 +2096,7 @@ DistCtx::~DistCtx() {
 // a multi-process (one GPU per rank) NCCL group.
 void create_slabs(const gmg_problem_desc* d, const gmg_slab_desc* sl, gmg_problem** out) {
     if (!sl || sl->world < 1) throw std::invalid_argument("slabs: world must be >= 1");
+    if (d && d->periodic_y) throw std::invalid_argument("slabs: periodic (polar) levels are not sharded");
     const bool local = sl->rank < 0;
     if (!local && (sl->rank >= sl->world || !sl->nccl_id)) throw std::invalid_argument("slabs: bad rank or id");
     const int nloc = local ? sl->world : 1;
@@ -2271,6 +2289,7 @@ int gmg_dev_mg_cycle(gmg_problem* p, const gmg_cycle_desc* spec, int level, cons
         std::lock_guard<std::mutex> lk(p->mu);
         check_level(p, level, "mg_cycle");
         check_smoother(*spec);
+        check_periodic_kind(p, spec->smoother_kind);
         const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
         check_cycle(p, *spec);
         Lev& L = p->lev(level);
@@ -2313,6 +2332,7 @@ int gmg_dev_make_start_vector(gmg_problem* p, const gmg_cycle_desc* spec, int ki
         } else {
             for (int l = L; l >= 2; --l) launch_restrict(p, l, p->lev(l).buf[DCAS], p->lev(l - 1).buf[DCAS]);
             check_smoother(*spec);
+            check_periodic_kind(p, spec->smoother_kind);
             const SmSetup* sm = ensure_smoother(p, spec->smoother_kind, spec->smoother_omega);
             if (!(spec->smoothing_omega > 0.0)) throw std::invalid_argument("omega: damping must be > 0");
             // u = coarse_solver().solve(rhs[1]); per level u = smooth_step(P u, rhs[l])
@@ -2381,6 +2401,7 @@ int gmg_dev_smooth_step(gmg_problem* p, int level, int kind, double somega, doub
         sp.smoother_kind = kind;
         sp.smoother_omega = somega;
         check_smoother(sp);
+        check_periodic_kind(p, kind);
         const SmSetup* sm = ensure_smoother(p, kind, somega);
         if (!(omega_damp > 0.0)) throw std::invalid_argument("omega: damping must be > 0");
         Lev& L = p->lev(level);
@@ -2699,7 +2720,7 @@ int gmg_host_problem_create(int num_levels, int cnx, int cny, double gx, double 
                                   lv[q].c.data(), lv[q].n.data(), lv[q].s.data(), lv[q].e.data(),
                                   lv[q].w.data()};
         }
-        gmg_problem_desc pd{num_levels, d.data(), device};
+        gmg_problem_desc pd{num_levels, d.data(), device, coords == GMG_POLAR ? 1 : 0};
         create_problem(&pd, out);
     });
 }
@@ -2714,7 +2735,7 @@ int gmg_host_problem_create_slabs(int num_levels, int cnx, int cny, double gx, d
                                   lv[q].c.data(), lv[q].n.data(), lv[q].s.data(), lv[q].e.data(),
                                   lv[q].w.data()};
         }
-        gmg_problem_desc pd{num_levels, d.data(), device};
+        gmg_problem_desc pd{num_levels, d.data(), device, coords == GMG_POLAR ? 1 : 0};
         create_slabs(&pd, slabs, out);
     });
 }

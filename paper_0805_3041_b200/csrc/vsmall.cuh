@@ -26,6 +26,7 @@ constexpr size_t kVSmemMax = 200 * 1024;
 
 struct VLev {
     int nx, ny;
+    int per;  // y periodic (polar): row neighbours and transfer rows wrap
     long long pitch;
     int kind;  // 0 CONST, 1 ROWX, 2 FIELD
     CoefConst cc;
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
                 for (int k = t; k < n; k += kVThreads) {
                     const int i = k % nx, j = k / nx;
                     const double xw = i > 0 ? a[k - 1] : 0.0, xe = i + 1 < nx ? a[k + 1] : 0.0;
-                    const double xs = j > 0 ? a[k - nx] : 0.0, xn = j + 1 < ny ? a[k + nx] : 0.0;
+                    const double xs = j > 0 ? a[k - nx] : (L.per ? a[k + (ny - 1) * nx] : 0.0);
+                    const double xn = j + 1 < ny ? a[k + nx] : (L.per ? a[i] : 0.0);
                     b[k] = jacobi_point(A, i, j, a[k], xw, xe, xs, xn, g[k], P.damp);
                 }
             });
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
             if (P.uc && P.top > 1) {
                 const VLev& C = P.lv[P.top - 1];
                 v = prolong_dense(L.tx, L.ty, i, j, [&](int ci, int cj) {
+                    if (C.per && cj < 0) cj += C.ny;  // coarse node 0 == coarse node ny_c
                     return (ci >= 0 && ci < C.nx && cj >= 0 && cj < C.ny) ? P.uc[(long long)cj * C.pitch + ci] : 0.0;
                 });
             }
@@ -149,7 +152,8 @@ __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
             for (int k = t; k < n; k += kVThreads) {
                 const int i = k % nx, j = k / nx;
                 const double xw = i > 0 ? u[k - 1] : 0.0, xe = i + 1 < nx ? u[k + 1] : 0.0;
-                const double xs = j > 0 ? u[k - nx] : 0.0, xn = j + 1 < ny ? u[k + nx] : 0.0;
+                const double xs = j > 0 ? u[k - nx] : (L.per ? u[k + (ny - 1) * nx] : 0.0);
+                const double xn = j + 1 < ny ? u[k + nx] : (L.per ? u[i] : 0.0);
                 d[k] = g[k] - stencil_apply(A, i, j, u[k], xw, xe, xs, xn);
             }
         });
@@ -161,7 +165,8 @@ __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
         for (int k = t; k < cn; k += kVThreads) {
             const int Pc = k % C.nx, Qc = k / C.nx;
             gc[k] = restrict_at(C.rw, Pc, Qc, [&](int di, int dj) {
-                return d[(2 * Qc + 1 + dj) * nx + 2 * Pc + 1 + di];
+                const int r = 2 * Qc + 1 + dj;  // < ny, or == ny on a periodic level: row 0
+                return d[(r < ny ? r : r - ny) * nx + 2 * Pc + 1 + di];
             });
             ucz[k] = 0.0;
         }
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
         for (int k = t; k < n; k += kVThreads) {
             const int i = k % nx, j = k / nx;
             T[k] = prolong_dense(L.tx, L.ty, i, j, [&](int ci, int cj) {
+                if (C.per && cj < 0) cj += C.ny;  // coarse node 0 == coarse node ny_c
                 return (ci >= 0 && ci < C.nx && cj >= 0 && cj < C.ny) ? uc[cj * C.nx + ci] : 0.0;
             });
         }
@@ -221,7 +227,8 @@ __global__ void __launch_bounds__(kVThreads) k_vsmall(VParams P) {
                     const int i = k % nx, j = k / nx;
                     const double b = T[k];
                     const double xw = i > 0 ? T[k - 1] : 0.0, xe = i + 1 < nx ? T[k + 1] : 0.0;
-                    const double xs = j > 0 ? T[k - nx] : 0.0, xn = j + 1 < ny ? T[k + nx] : 0.0;
+                    const double xs = j > 0 ? T[k - nx] : (L.per ? T[k + (ny - 1) * nx] : 0.0);
+                    const double xn = j + 1 < ny ? T[k + nx] : (L.per ? T[i] : 0.0);
                     X[k] = stencil_apply(A, i, j, b, xw, xe, xs, xn) * b;
                     d[k] = d[k] * b;
                     any |= (b * b) != 0.0;

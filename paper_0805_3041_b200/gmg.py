@@ -39,7 +39,7 @@ GMG_OK, GMG_ERR_LOGIC, GMG_ERR_INVALID, GMG_ERR_RUNTIME, GMG_DIVERGED, GMG_ERR_C
 SMOOTHERS = ["richardson", "jacobi", "gauss_seidel", "sor", "ilu0", "tri_x", "tri_y", "adi",
              "gstri_x", "gstri_y", "gsadi"]
 CYCLES = {"V": 0, "W": 1, "F": 2}
-COORDS = {"cartesian": 0, "cylindrical": 1, "spherical": 2}
+COORDS = {"cartesian": 0, "cylindrical": 1, "spherical": 2, "polar": 3}  # polar: BASELINE C3, no reference
 REDUCTIONS = {"exact": 0, "fast": 1}
 UNLIMITED = (1 << 64) - 1
 
@@ -103,7 +103,8 @@ class _LevelDesc(C.Structure):
 
 
 class _ProblemDesc(C.Structure):
-    _fields_ = [("num_levels", C.c_int), ("levels", C.POINTER(_LevelDesc)), ("device", C.c_int)]
+    _fields_ = [("num_levels", C.c_int), ("levels", C.POINTER(_LevelDesc)), ("device", C.c_int),
+                ("periodic_y", C.c_int)]
 
 
 class _SlabDesc(C.Structure):
@@ -304,7 +305,7 @@ class MultilevelProblem:
             arrs = {k: _arr(L[k]) for k in ("x", "y", "c", "n", "s", "e", "w")}
             keep.append(arrs)
             descs[q] = _LevelDesc(q + 1, L["nx"], L["ny"], *[_p(arrs[k]) for k in ("x", "y", "c", "n", "s", "e", "w")])
-        pd = _ProblemDesc(len(levels), descs, device)
+        pd = _ProblemDesc(len(levels), descs, device, 0)
         h = C.c_void_p()
         _check(lib().gmg_dev_problem_create(C.byref(pd), C.byref(h)))
         obj = cls.__new__(cls)

@@ -23,7 +23,7 @@ ap.add_argument("--skips", default="0,4,8,11,15,19")
 ap.add_argument("--reduction", default="exact")
 a = ap.parse_args()
 w = bench.WORKLOADS[a.workload]
-p = gmg.MultilevelProblem(w["levels"], 1, 1, (1.0, 1.0), "cartesian", w["alpha"], w["beta"])
+p = gmg.MultilevelProblem(*bench.wl_args(w))
 n = p.n(w["levels"])
 b = torch.from_numpy(gmg.random_vector(n, 1)).cuda()
 x0 = np.zeros(n) if not w["seed_x"] else gmg.random_vector(n, w["seed_x"])
