@@ -94,6 +94,13 @@ typedef struct gmg_problem_desc {
                                      level (ny nodes, ny_l = 2 ny_(l-1); y has ny+2 entries whose
                                      first and last are the wrapped neighbours), the operator's
                                      s on row 0 and n on row ny-1 couple across the wrap */
+    /* Optional: the physics the operators were assembled from (AnisotropySpec and
+     * LevelGrid::coords, cycle.hpp:62-78). With alpha > 0, levels whose arrays are
+     * not constant or x-only are rebuilt on the fly from 1-D tables (0 B/DOF of
+     * coefficient traffic) when the tables reproduce every given coefficient bit
+     * for bit; otherwise (alpha <= 0, or a mismatch) the five arrays are streamed. */
+    double alpha, beta;
+    int coords;                   /* gmg_coords */
 } gmg_problem_desc;
 
 /* gmg::CycleSpec, include/gmg/cycle.hpp:23-39 (+ SmootherSpec) */
@@ -149,7 +156,8 @@ int gmg_dev_problem_create(const gmg_problem_desc* desc, gmg_problem** out);
 int gmg_dev_problem_destroy(gmg_problem* p);
 int gmg_dev_num_levels(const gmg_problem* p);
 int gmg_dev_level_shape(const gmg_problem* p, int level, int* nx, int* ny);
-/* operator storage chosen at create: 0 = constant 5-point, 1 = x-varying rows, 2 = full field */
+/* operator storage chosen at create: 0 = constant 5-point, 1 = x-varying rows, 2 = full
+ * field (five streamed arrays), 3 = computed on the fly from 1-D axis tables */
 int gmg_dev_level_coef_kind(const gmg_problem* p, int level);
 /* Row-slab problems (see gmg_slab_desc). Only gmg_dev_solve / _solve_devptr and
  * the queries below accept such a handle; the Jacobi smoother is sharded. */

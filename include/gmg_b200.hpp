@@ -112,7 +112,9 @@ inline gmg_problem* create(const gmg::MultilevelProblem& prob, int device) {
         lv[l - 1] = gmg_level_desc{l,          g.nx,       g.ny,       g.x.data(), g.y.data(),
                                    A.c.data(), A.n.data(), A.s.data(), A.e.data(), A.w.data()};
     }
-    const gmg_problem_desc desc{prob.num_levels(), lv.data(), device};
+    // the physics lets the library rebuild graded / spherical operators on the fly (checked bit for bit)
+    const gmg_problem_desc desc{prob.num_levels(), lv.data(), device, 0, prob.anisotropy().alpha,
+                                prob.anisotropy().beta, static_cast<int>(prob.grid(1).coords)};
     gmg_problem* p = nullptr;
     check(gmg_dev_problem_create(&desc, &p));
     return p;

@@ -199,17 +199,64 @@ struct CoefField {
     }
 };
 
+// AXES: the general graded / spherical operator computed on the fly from 1-D
+// tables of the hierarchy, exactly as assemble builds it (stencil.cpp:77-127):
+//   ce = ((alpha fw(x_e)) my) / h_e,   cw = ((alpha fw(x_w)) my) / h_w,
+//   cn = ((beta fw(y_n)) mx) / h_n,    cs = ((beta fw(y_s)) mx) / h_s,
+//   c = ((ce + cw) + cn) + cs; e, w, n, s = -ce, -cw, -cn, -cs (0 toward the boundary).
+// Per column i: ae = alpha fw(x_e), aw, he, hw, mx (the transverse measure) and the
+// reciprocals rhe, rhw; per row j: bn, bs, hn, hs, my, rhn, rhs. The host builds
+// them with the reference's expressions and checks every coefficient against the
+// given arrays bit for bit before choosing this class; the divisions are div_rcp
+// (the IEEE quotient). 0 B/DOF instead of FIELD's 40.
+struct CoefAxes {
+    static constexpr bool kUnitWE = false, kUnitSN = false, kMaySlow = false;
+    const double *ae, *aw, *he, *hw, *mx, *rhe, *rhw;  // length nx each
+    const double *bn, *bs, *hn, *hs, *my, *rhn, *rhs;  // length ny each
+    int nx, ny;
+    __device__ __forceinline__ void fluxes(int i, int j, double& ce, double& cw, double& cn, double& cs) const {
+        const double yj = __ldg(my + j), xi = __ldg(mx + i);
+        ce = div_rcp(__ldg(ae + i) * yj, __ldg(he + i), __ldg(rhe + i));
+        cw = div_rcp(__ldg(aw + i) * yj, __ldg(hw + i), __ldg(rhw + i));
+        cn = div_rcp(__ldg(bn + j) * xi, __ldg(hn + j), __ldg(rhn + j));
+        cs = div_rcp(__ldg(bs + j) * xi, __ldg(hs + j), __ldg(rhs + j));
+    }
+    __device__ __forceinline__ void load(int i, int j, double& C, double& W, double& E, double& S,
+                                         double& N) const {
+        double ce, cw, cn, cs;
+        fluxes(i, j, ce, cw, cn, cs);
+        C = ((ce + cw) + cn) + cs;
+        E = i + 1 < nx ? -ce : 0.0;
+        W = i > 0 ? -cw : 0.0;
+        N = j + 1 < ny ? -cn : 0.0;
+        S = j > 0 ? -cs : 0.0;
+    }
+    __device__ __forceinline__ double diag(int i, int j) const {
+        double ce, cw, cn, cs;
+        fluxes(i, j, ce, cw, cn, cs);
+        return ((ce + cw) + cn) + cs;
+    }
+    __device__ __forceinline__ double div_by_c(double r, int i, int j) const { return div_ieee(r, diag(i, j)); }
+    __device__ __forceinline__ double div_by_c_loaded(double r, double C, int, int) const { return div_ieee(r, C); }
+    __device__ __forceinline__ double div_by_c_fast(double r, int i, int j, bool& slow) const {
+        slow = false;
+        return div_by_c(r, i, j);
+    }
+};
+
 // Coefficient index clamp for points a streaming kernel evaluates outside the
 // grid (halo columns/rows whose results are discarded): ROWX/FIELD tables are
 // only read in bounds; for interior points the clamp is the identity.
 __device__ __forceinline__ int cix(int v, int n) { return v < 0 ? 0 : (v >= n ? n - 1 : v); }
 
 // y = (A x)(i,j) in the reference's order c, w, e, s, n (stencil.cpp:133-137).
+// Cout: the diagonal the stencil used (for the preconditioner's division).
 template <class Coef>
-__device__ __forceinline__ double stencil_apply(const Coef& A, int i, int j, double xc, double xw,
-                                                double xe, double xs, double xn) {
+__device__ __forceinline__ double stencil_apply_c(const Coef& A, int i, int j, double xc, double xw, double xe,
+                                                  double xs, double xn, double& Cout) {
     double C, W, E, S, N;
     A.load(i, j, C, W, E, S, N);
+    Cout = C;
     double acc = C * xc;
     if constexpr (Coef::kUnitWE) {
         acc = acc - xw;
@@ -226,6 +273,24 @@ __device__ __forceinline__ double stencil_apply(const Coef& A, int i, int j, dou
         acc = acc + N * xn;
     }
     return acc;
+}
+template <class Coef>
+__device__ __forceinline__ double stencil_apply(const Coef& A, int i, int j, double xc, double xw, double xe,
+                                                double xs, double xn) {
+    double C;
+    return stencil_apply_c(A, i, j, xc, xw, xe, xs, xn, C);
+}
+
+// z = r / c given the diagonal c the stencil just loaded: classes that compute
+// their coefficients (CoefAxes) divide by it instead of recomputing it.
+template <class Coef>
+__device__ __forceinline__ auto div_loaded(const Coef& A, double r, double C, int i, int j)
+    -> decltype(A.div_by_c_loaded(r, C, i, j)) {
+    return A.div_by_c_loaded(r, C, i, j);
+}
+template <class Coef, class... Ignored>
+__device__ __forceinline__ double div_loaded(const Coef& A, double r, double, int i, int j, Ignored...) {
+    return A.div_by_c(r, i, j);
 }
 
 // ---------------------------------------------------------------------------

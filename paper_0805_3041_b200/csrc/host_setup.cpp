@@ -262,6 +262,56 @@ void restrict_weights(const std::vector<double>& xf, const std::vector<double>& 
 
 double polar_theta_weight() { return kPolarThetaWeight; }
 
+bool axis_tables(const Level& L, int cs, double alpha, double beta, const double* c, const double* n,
+                 const double* s, const double* e, const double* w, AxisTables& T) {
+    if (cs < 0 || cs > 2 || !(alpha > 0.0) || !(beta > 0.0) || L.periodic) return false;
+    const int nx = L.nx, ny = L.ny;
+    T = AxisTables{};
+    for (int i = 0; i < nx; ++i) {
+        const double xw = 0.5 * (L.x[i] + L.x[i + 1]);
+        const double xe = 0.5 * (L.x[i + 1] + L.x[i + 2]);
+        const double dxw = L.x[i + 1] - L.x[i];
+        const double dxe = L.x[i + 2] - L.x[i + 1];
+        T.ae.push_back(alpha * face_x(cs, xe));
+        T.aw.push_back(alpha * face_x(cs, xw));
+        T.he.push_back(dxe);
+        T.hw.push_back(dxw);
+        T.mx.push_back(measure_x(cs, xw, xe));
+        T.rhe.push_back(1.0 / dxe);
+        T.rhw.push_back(1.0 / dxw);
+    }
+    for (int j = 0; j < ny; ++j) {
+        const double ys = 0.5 * (L.y[j] + L.y[j + 1]);
+        const double yn = 0.5 * (L.y[j + 1] + L.y[j + 2]);
+        const double dys = L.y[j + 1] - L.y[j];
+        const double dyn = L.y[j + 2] - L.y[j + 1];
+        T.bn.push_back(beta * face_y(cs, yn));
+        T.bs.push_back(beta * face_y(cs, ys));
+        T.hn.push_back(dyn);
+        T.hs.push_back(dys);
+        T.my.push_back(measure_y(cs, ys, yn));
+        T.rhn.push_back(1.0 / dyn);
+        T.rhs.push_back(1.0 / dys);
+    }
+    // the reciprocal path (div_rcp) needs normal spacings in [2^-500, 2^500]
+    for (const std::vector<double>* v : {&T.he, &T.hw, &T.hn, &T.hs})
+        for (double h : *v)
+            if (!std::isnormal(h) || std::fabs(h) < 0x1p-500 || std::fabs(h) > 0x1p500) return false;
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            const double ce = (T.ae[i] * T.my[j]) / T.he[i];
+            const double cw = (T.aw[i] * T.my[j]) / T.hw[i];
+            const double cn = (T.bn[j] * T.mx[i]) / T.hn[j];
+            const double cs_ = (T.bs[j] * T.mx[i]) / T.hs[j];
+            const std::size_t k = static_cast<std::size_t>(j) * nx + i;
+            if (!same_bits(c[k], ((ce + cw) + cn) + cs_) || !same_bits(e[k], i + 1 < nx ? -ce : 0.0) ||
+                !same_bits(w[k], i > 0 ? -cw : 0.0) || !same_bits(n[k], j + 1 < ny ? -cn : 0.0) ||
+                !same_bits(s[k], j > 0 ? -cs_ : 0.0))
+                return false;
+        }
+    return true;
+}
+
 std::vector<double> cholesky_periodic(const double* c, const double* w, const double* e, const double* s,
                                       const double* n, int nx, int ny) {
     const int N = nx * ny, bw = N - 1;

@@ -38,7 +38,21 @@ std::vector<double> cholesky_periodic(const double* c, const double* w, const do
                                       const double* n, int nx, int ny);
 
 // Operator classification (see common.cuh).
-enum CoefKind { COEF_CONST = 0, COEF_ROWX = 1, COEF_FIELD = 2 };
+enum CoefKind { COEF_CONST = 0, COEF_ROWX = 1, COEF_FIELD = 2, COEF_AXES = 3 };
+
+// 1-D tables of the on-the-fly operator (common.cuh CoefAxes): per column i
+// ae = alpha fw(x_e), aw = alpha fw(x_w), he, hw, mx and 1/he, 1/hw; per row j
+// bn, bs, hn, hs, my and 1/hn, 1/hs, with assemble's expressions
+// (stencil.cpp:49-127).
+struct AxisTables {
+    std::vector<double> ae, aw, he, hw, mx, rhe, rhw;
+    std::vector<double> bn, bs, hn, hs, my, rhn, rhs;
+};
+// Builds the tables of a level of coordinate system cs and checks that the
+// coefficients computed from them reproduce c, n, s, e, w bit for bit (the
+// reference's arrays); false if they do not (the level then streams FIELD).
+bool axis_tables(const Level& L, int cs, double alpha, double beta, const double* c, const double* n,
+                 const double* s, const double* e, const double* w, AxisTables& T);
 struct CoefClass {
     CoefKind kind = COEF_FIELD;
     double c = 0, w = 0, e = 0, s = 0, n = 0;            // CONST

@@ -173,9 +173,10 @@ template <class Coef>
 __device__ __forceinline__ double jacobi_point(const Coef& A, int i, int j, double xc, double xw,
                                                double xe, double xs, double xn, double g,
                                                double omega) {
-    const double acc = stencil_apply(A, i, j, xc, xw, xe, xs, xn);
+    double C;
+    const double acc = stencil_apply_c(A, i, j, xc, xw, xe, xs, xn, C);
     const double d = acc - g;
-    const double z = A.div_by_c(d, i, j);
+    const double z = div_loaded(A, d, C, i, j);
     return xc - omega * z;
 }
 

@@ -246,10 +246,11 @@ __device__ __forceinline__ void cpa_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
-// stage one coarse value (zeros outside the coarse interior)
+// stage one coarse value (zeros outside the coarse interior). The warp-strip
+// kernels march non-periodic levels only (Lev::strips), so no row wrap here.
 __device__ __forceinline__ void stage_coarse(double* dst, const double* uc, const Grid& cg, int ci, int cj) {
-    const bool in = cg.inside(ci, cj);
-    cpa8(dst, in ? uc + cg.at(ci, cj) : uc, in ? 8 : 0);
+    const bool in = ci >= 0 && ci < cg.nx && cj >= 0 && cj < cg.ny;
+    cpa8(dst, in ? uc + (long long)cj * cg.pitch + ci : uc, in ? 8 : 0);
 }
 
 enum SrcKind3 { K3_ZERO = 0, K3_U = 1, K3_PROLONG = 2, K3_CORRECT = 3 };

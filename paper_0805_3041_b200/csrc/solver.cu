@@ -161,6 +161,8 @@ struct Lev {
     CoefConst cconst{};
     CoefRowX crow{};
     CoefField cfield{};
+    CoefAxes caxes{};
+    gmg_host::AxisTables axt;  // host copy of the AXES tables (kind 3)
     double* coefmem = nullptr;
     double *tx = nullptr, *ty = nullptr;  // prolongation weights (this level as fine)
     RestrictW rw{};                       // restriction weights (this level as coarse)
@@ -412,6 +414,7 @@ template <class F>
 void with_coef(const Lev& L, F&& f) {
     if (L.kind == 0) f(L.cconst);
     else if (L.kind == 1) f(L.crow);
+    else if (L.kind == 3) f(L.caxes);
     else f(L.cfield);
 }
 
@@ -1301,6 +1304,7 @@ struct Driver {
             v.cc = L.cconst;
             v.cr = L.crow;
             v.cf = L.cfield;
+            v.ca = L.caxes;
             v.tx = L.tx;
             v.ty = L.ty;
             v.rw = L.rw;
@@ -1616,6 +1620,21 @@ int fetch_status(gmg_problem* p) {
 void host_coefs(gmg_problem* p, const Lev& L, std::vector<double> (&a)[5]) {
     const size_t N = (size_t)L.n();
     for (auto& v : a) v.assign(N, 0.0);
+    if (L.kind == 3) {  // the AXES expressions (common.cuh CoefAxes), on the host
+        const gmg_host::AxisTables& T = L.axt;
+        for (int j = 0; j < L.ny; ++j)
+            for (int i = 0; i < L.nx; ++i) {
+                const size_t k = (size_t)j * L.nx + i;
+                const double ce = (T.ae[i] * T.my[j]) / T.he[i], cw = (T.aw[i] * T.my[j]) / T.hw[i];
+                const double cn = (T.bn[j] * T.mx[i]) / T.hn[j], cs = (T.bs[j] * T.mx[i]) / T.hs[j];
+                a[0][k] = ((ce + cw) + cn) + cs;
+                a[1][k] = i > 0 ? -cw : 0.0;
+                a[2][k] = i + 1 < L.nx ? -ce : 0.0;
+                a[3][k] = j > 0 ? -cs : 0.0;
+                a[4][k] = j + 1 < L.ny ? -cn : 0.0;
+            }
+        return;
+    }
     if (L.kind == 2) {
         for (int q = 0; q < 5; ++q)
             download(p, L, a[q].data(), L.coefmem + q * L.elems + L.off0, cudaMemcpyDeviceToHost);
@@ -1977,6 +1996,25 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
                 CK(cudaMemcpy(L.coefmem + q * L.nx, t[q]->data(), L.nx * sizeof(double), cudaMemcpyHostToDevice));
             L.crow = CoefRowX{L.coefmem,          L.coefmem + L.nx,     L.coefmem + 2 * L.nx, L.coefmem + 3 * L.nx,
                               L.coefmem + 4 * L.nx, ok ? L.coefmem + 5 * L.nx : nullptr};
+        } else if (gmg_host::axis_tables(h, d->coords, d->alpha, d->beta, ld.c, ld.n, ld.s, ld.e, ld.w, L.axt)) {
+            // AXES: coefficients on the fly from 1-D tables (checked bit for bit on the host)
+            L.kind = 3;
+            const gmg_host::AxisTables& T = L.axt;
+            const std::vector<double>* tx[7] = {&T.ae, &T.aw, &T.he, &T.hw, &T.mx, &T.rhe, &T.rhw};
+            const std::vector<double>* ty[7] = {&T.bn, &T.bs, &T.hn, &T.hs, &T.my, &T.rhn, &T.rhs};
+            CK(dmalloc(&L.coefmem, 7 * ((size_t)L.nx + L.ny) * sizeof(double)));
+            const double* px[7];
+            const double* py[7];
+            for (int q = 0; q < 7; ++q) {
+                double* dx = L.coefmem + (size_t)q * L.nx;
+                double* dy = L.coefmem + 7 * (size_t)L.nx + (size_t)q * L.ny;
+                CK(cudaMemcpy(dx, tx[q]->data(), L.nx * sizeof(double), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(dy, ty[q]->data(), L.ny * sizeof(double), cudaMemcpyHostToDevice));
+                px[q] = dx;
+                py[q] = dy;
+            }
+            L.caxes = CoefAxes{px[0], px[1], px[2], px[3], px[4], px[5], px[6],
+                               py[0], py[1], py[2], py[3], py[4], py[5], py[6], L.nx, L.ny};
         } else {
             CK(dmalloc(&L.coefmem, 5 * L.elems * sizeof(double)));
             CK(cudaMemset(L.coefmem, 0, 5 * L.elems * sizeof(double)));
@@ -1989,6 +2027,7 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
             }
             L.cfield = CoefField{dst[0], dst[1], dst[2], dst[3], dst[4], L.pitch};
         }
+
     }
     // transfer tables: tx, ty (fine side); restriction weights (coarse side)
     for (int l = 1; l <= p->L; ++l) {
@@ -2720,7 +2759,7 @@ int gmg_host_problem_create(int num_levels, int cnx, int cny, double gx, double 
                                   lv[q].c.data(), lv[q].n.data(), lv[q].s.data(), lv[q].e.data(),
                                   lv[q].w.data()};
         }
-        gmg_problem_desc pd{num_levels, d.data(), device, coords == GMG_POLAR ? 1 : 0};
+        gmg_problem_desc pd{num_levels, d.data(), device, coords == GMG_POLAR ? 1 : 0, alpha, beta, coords};
         create_problem(&pd, out);
     });
 }
@@ -2735,7 +2774,7 @@ int gmg_host_problem_create_slabs(int num_levels, int cnx, int cny, double gx, d
                                   lv[q].c.data(), lv[q].n.data(), lv[q].s.data(), lv[q].e.data(),
                                   lv[q].w.data()};
         }
-        gmg_problem_desc pd{num_levels, d.data(), device, coords == GMG_POLAR ? 1 : 0};
+        gmg_problem_desc pd{num_levels, d.data(), device, coords == GMG_POLAR ? 1 : 0, alpha, beta, coords};
         create_slabs(&pd, slabs, out);
     });
 }

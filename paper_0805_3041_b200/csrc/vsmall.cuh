@@ -32,6 +32,7 @@ struct VLev {
     CoefConst cc;
     CoefRowX cr;
     CoefField cf;
+    CoefAxes ca;
     const double *tx, *ty;  // prolongation weights (this level as fine)
     RestrictW rw;           // restriction weights (this level as coarse)
     int off;                // shared-memory offset (doubles) of U, G, D (each nx*ny)
@@ -53,6 +54,7 @@ template <class F>
 __device__ __forceinline__ void with_vcoef(const VLev& L, F&& f) {
     if (L.kind == 0) f(L.cc);
     else if (L.kind == 1) f(L.cr);
+    else if (L.kind == 3) f(L.ca);
     else f(L.cf);
 }
 

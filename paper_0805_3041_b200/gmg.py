@@ -104,7 +104,7 @@ class _LevelDesc(C.Structure):
 
 class _ProblemDesc(C.Structure):
     _fields_ = [("num_levels", C.c_int), ("levels", C.POINTER(_LevelDesc)), ("device", C.c_int),
-                ("periodic_y", C.c_int)]
+                ("periodic_y", C.c_int), ("alpha", C.c_double), ("beta", C.c_double), ("coords", C.c_int)]
 
 
 class _SlabDesc(C.Structure):
@@ -305,7 +305,7 @@ class MultilevelProblem:
             arrs = {k: _arr(L[k]) for k in ("x", "y", "c", "n", "s", "e", "w")}
             keep.append(arrs)
             descs[q] = _LevelDesc(q + 1, L["nx"], L["ny"], *[_p(arrs[k]) for k in ("x", "y", "c", "n", "s", "e", "w")])
-        pd = _ProblemDesc(len(levels), descs, device, 0)
+        pd = _ProblemDesc(len(levels), descs, device, 0, 0.0, 0.0, 0)  # no physics: arrays as given
         h = C.c_void_p()
         _check(lib().gmg_dev_problem_create(C.byref(pd), C.byref(h)))
         obj = cls.__new__(cls)
@@ -337,7 +337,7 @@ class MultilevelProblem:
         return a.value, b.value
 
     def coef_kind(self, level: int) -> str:
-        return {0: "const", 1: "rowx", 2: "field"}.get(lib().gmg_dev_level_coef_kind(self._h, level), "?")
+        return {0: "const", 1: "rowx", 2: "field", 3: "axes"}.get(lib().gmg_dev_level_coef_kind(self._h, level), "?")
 
     def close(self):
         if getattr(self, "_h", None):

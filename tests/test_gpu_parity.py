@@ -39,9 +39,32 @@ def problems(gpu):
 def test_operator_classes(problems):
     kinds = [p.coef_kind(p.num_levels) for p, _ in problems]
     assert kinds[0] == "const"  # dyadic uniform grid: bit-exact constant stencil
-    assert kinds[1] in ("const", "rowx", "field")  # 23 x 31 cells: h = 1/24 is not dyadic
+    assert kinds[1] in ("const", "rowx", "field", "axes")  # 23 x 31 cells: h = 1/24 is not dyadic
     assert kinds[2] == "rowx"
-    assert kinds[3] == "field"
+    assert kinds[3] == "axes"  # graded spherical: rebuilt on the fly from 1-D tables (0 B/DOF)
+
+
+@pytest.mark.parametrize("gi", [3, 4], ids=["spherical_graded", "wide_graded"])
+def test_axes_and_field_storage_agree(problems, gi):
+    """The same graded operator stored as five streamed arrays (FIELD: built from the
+    arrays alone, without the physics) and computed on the fly (AXES): every level's
+    smoother and whole solves bit for bit (stencil.cpp:77-127)."""
+    d, o = problems[gi]
+    levels = [dict(nx=o.shapes[l][0], ny=o.shapes[l][1], **dict(zip(("x", "y"), o.coords(l))), **o.operator(l))
+              for l in range(1, d.num_levels + 1)]
+    f = gmg.MultilevelProblem.from_levels(levels)
+    L = d.num_levels
+    assert f.coef_kind(L) == "field" and d.coef_kind(L) == "axes"
+    x = Oracle.random_vector(d.n(L), 5)
+    b = Oracle.random_vector(d.n(L), 6)
+    for l in range(1, L + 1):
+        xl, bl = Oracle.random_vector(d.n(l), 7), Oracle.random_vector(d.n(l), 8)
+        assert bits_equal(gmg.smooth_step(d, l, "jacobi", 1.0, xl, bl, 0.7), gmg.smooth_step(f, l, "jacobi", 1.0, xl, bl, 0.7))
+        assert bits_equal(gmg.apply(d, l, xl), gmg.apply(f, l, xl))
+    spec = gmg.CycleSpec(smoother="jacobi", tolerance=1e-9, max_cycles=20)
+    xa, xf = x.copy(), x.copy()
+    ra, rf = gmg.solve(d, b, spec, xa), gmg.solve(f, b, spec, xf)
+    assert ra.residual_history == rf.residual_history and bits_equal(xa, xf)
 
 
 @pytest.mark.parametrize("gi", range(len(GEOMS)), ids=GIDS)
