@@ -68,12 +68,18 @@ WORKLOADS = {
     "C3": dict(levels=10, alpha=1.0, beta=1.0, pre=2, post=2, tol=1e-8, seed_x=0, coords="polar", cny=2,
                desc="polar Poisson 1023 (r in [0.1,1], Dirichlet) x 1024 (theta, periodic), 10 levels, "
                     "jacobi 0.7 2+2, F-cycle, adaptive omega_l, exact-order reductions"),
+    # SURVEY.md §8(e) weak-scaling family: coarse 15 x (2P-1), 11 levels -> 16383 x (2048P-1) interior
+    # (P = 8: exactly the C5 grid, with a 225-unknown level-1 factor); C5's physics and smoother
+    "W": dict(levels=11, alpha=1e-2, beta=1.0, pre=3, post=3, tol=1e-30, seed_x=2, cnx=15, cny_per_rank=True,
+              desc="weak-scaling family 16383 x (2048P-1) interior, coarse 15 x (2P-1), 11 levels, eps=1e-2, "
+                   "jacobi 0.7 3+3, F-cycle, adaptive omega_l, exact-order reductions"),
 }
 
 
-def wl_args(w):
-    """MultilevelProblem / Oracle constructor arguments of a workload."""
-    return (w["levels"], 1, w.get("cny", 1), (1.0, 1.0), w.get("coords", "cartesian"), w["alpha"], w["beta"])
+def wl_args(w, world=1):
+    """MultilevelProblem / Oracle constructor arguments of a workload (world: ranks, for W)."""
+    cny = 2 * world - 1 if w.get("cny_per_rank") else w.get("cny", 1)
+    return (w["levels"], w.get("cnx", 1), cny, (1.0, 1.0), w.get("coords", "cartesian"), w["alpha"], w["beta"])
 
 
 def common_config(wl, n):
@@ -113,6 +119,9 @@ def maybe_spawn(args):
         return
     if args.gpus is None or args.gpus <= 1 or args.impl == "reference":
         return
+    import torch
+    if torch.cuda.device_count() < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {torch.cuda.device_count()}")
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
@@ -271,7 +280,7 @@ def run_reference_arm(args):
     if w.get("coords") == "polar":
         B = pyoracle.Oracle  # no reference counterpart for polar coordinates: the oracle port
         kind = "port"
-    prob = B(*wl_args(w))
+    prob = B(*wl_args(w, ws if ws > 1 else (args.gpus or 1)))
     n = prob.n(w["levels"])
     b = B.random_vector(n, 1)
     P = usable_threads(n) if args.ref_threads <= 0 else args.ref_threads
@@ -391,7 +400,7 @@ def run_ours(args):
     wl = args.workload
     w = WORKLOADS[wl]
     L = w["levels"]
-    pargs = wl_args(w)
+    pargs = wl_args(w, ws)
     sharded = ws > 1 and args.parallel == "slabs"
     if sharded:
         # one NCCL group for the row slabs; rank 0's unique id travels over the torch group
@@ -521,7 +530,8 @@ def run_ours(args):
         line = {
             "metric": "fine-grid DOF*F-cycles/s (fp64)", "value": value, "unit": "DOF*cycles/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if sharded and not w.get("cny_per_rank") else "weak",
+            "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded U[-1,1] rhs from std::mt19937, as the reference tests)",
             "config": common_config(wl, n),
