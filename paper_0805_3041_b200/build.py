@@ -26,6 +26,7 @@ NVFLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "--expt-relax
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall"]
 
 SOURCES_CU = ["solver.cu"]
+INST_GROUPS = [1, 2, 3, 4]  # inst.cu, once per group of inst.h
 SOURCES_CPP = ["host_setup.cpp"]
 def _deps():
     """Every header the sources may include (all of csrc/ plus the C ABI)."""
@@ -54,15 +55,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     log = os.path.join(BUILD, "build.log")
     deps = _deps()
     objs = []
+    extra = os.environ.get("GMG_EXTRA_NVFLAGS", "").split()  # e.g. -DGMG_KDEBUG (debug builds)
+    jobs = []  # (name, command, object): the CUDA translation units compile in parallel
     for src in SOURCES_CU:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if force or _newer(o, [s, *deps]):
-            if verbose:
-                print("nvcc", src, flush=True)
-            extra = os.environ.get("GMG_EXTRA_NVFLAGS", "").split()  # e.g. -DGMG_KDEBUG (debug builds)
-            _run([NVCC, *NVFLAGS, *extra, "-c", s, "-o", o], o + ".log")
+            jobs.append((src, [NVCC, *NVFLAGS, *extra, "-c", s, "-o", o], o))
         objs.append(o)
+    for g in INST_GROUPS:
+        s = os.path.join(CSRC, "inst.cu")
+        o = os.path.join(BUILD, f"inst{g}.o")
+        if force or _newer(o, [s, *deps]):
+            jobs.append((f"inst.cu[{g}]", [NVCC, *NVFLAGS, *extra, f"-DGMG_INST_GROUP={g}", "-c", s, "-o", o], o))
+        objs.append(o)
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+        if verbose:
+            print("nvcc", ", ".join(j[0] for j in jobs), flush=True)
+        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            list(ex.map(lambda j: _run(j[1], j[2] + ".log"), jobs))
     for src in SOURCES_CPP:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")

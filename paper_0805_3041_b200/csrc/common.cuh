@@ -78,7 +78,7 @@ struct Grid {
 // true division, out of line: an inlined IEEE division (~30 instructions and a
 // slow path) per point and fused step would swamp the instruction cache of the
 // unrolled streaming kernels.
-__device__ __noinline__ double div_ieee(double d, double c) { return d / c; }
+static __device__ __noinline__ double div_ieee(double d, double c) { return d / c; }
 __device__ __forceinline__ double div_rcp(double d, double c, double y) {
     const double q0 = d * y;
     const double a = fabs(d);

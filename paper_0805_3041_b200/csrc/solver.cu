@@ -36,6 +36,7 @@
 #include "march.cuh"
 #include "march2.cuh"
 #include "march4.cuh"
+#include "inst.h"
 #include "seqsum.cuh"
 #include "vsmall.cuh"
 
