@@ -28,7 +28,12 @@ template <int SK>
 struct Smooth4Smem {
     static constexpr bool HAS_U = SK == K3_U || SK == K3_CORRECT;
     static constexpr bool HAS_C = SK == K3_PROLONG || SK == K3_CORRECT;
-    static constexpr int D = 4;
+    // ring depth: rows in flight per warp = D-1 (a deeper ring, 8, for the sources with one
+    // streamed array measured 25% slower in the cycle)
+#ifndef GMG_S4_DEEP
+#define GMG_S4_DEEP 4
+#endif
+    static constexpr int D = HAS_U ? 4 : GMG_S4_DEEP;
     // [slot][half][lane]: lane's columns 4l..4l+1 in half 0, 4l+2..4l+3 in half 1
     // (16-B lane stride: conflict-free 128-bit accesses)
     double2 g[D][2][32];
@@ -36,63 +41,72 @@ struct Smooth4Smem {
     double c[HAS_C ? D : 1][68];  // coarse rows, slot = coarse row & (D-1)
 };
 
-template <int M, int SK, class Coef>
-__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
-    k_smooth4(Grid fg, Coef A, const double* __restrict__ u, Prolong P, OmegaSrc om, const double* __restrict__ g,
-              double* __restrict__ out, double omega_damp, int seg) {
-    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
-    pdl_trigger();
+// The march of one warp strip. BND = false: the strip and every row it touches
+// (staged rows included) lie inside the domain with both coarse parents present,
+// so no bounds predicate, zero-fill byte count or masking select is issued — the
+// common case (all but the first/last strips and row segments). BND = true: the
+// general path with domain masks. Same arithmetic per point in both.
+template <int M, int SK, class Coef, bool BND>
+__device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg, const Coef& A,
+                                              const double* __restrict__ u, const Prolong& P, double omega,
+                                              const double* __restrict__ g, double* __restrict__ out,
+                                              double omega_damp, int i0, int j0, int j1) {
     using SM = Smooth4Smem<SK>;
     constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C;
     constexpr int D = SM::D;
     constexpr int H = (M + 1) & ~1;  // halo columns, even: 16-B aligned strips
-    constexpr int OW = 128 - 2 * H;  // columns each strip produces
     constexpr int ML = M > 0 ? M : 1;
-    extern __shared__ __align__(16) unsigned char sm4raw[];
-    SM& S = reinterpret_cast<SM*>(sm4raw)[threadIdx.x >> 5];
-
+    // coarse columns are staged from the even column mS = m0 - COFF (16-B pairs)
+    constexpr int COFF = (H == 2) ? 0 : 1;
     const int lane = threadIdx.x & 31;
-    const int strip = blockIdx.x * kS4W + (threadIdx.x >> 5);
-    const int i0 = strip * OW - H;
-    if (i0 + H >= fg.nx) return;  // warp-uniform; the kernel has no block barriers
     const int i = i0 + 4 * lane;
     const int nx = fg.nx, ny = fg.ny;
-    const int j0 = fg.w0 + blockIdx.y * seg;
-    const int j1 = min(j0 + seg, fg.w1);
-    const bool edge = i0 < 0 || i0 + 128 > nx;
+    const bool edge = BND && (i0 < 0 || i0 + 128 > nx);
     bool cin[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cin[k] = i + k >= 0 && i + k < nx;
-    const int m0 = i0 / 2 - 1;  // first coarse column staged (i0 even)
+    for (int k = 0; k < 4; ++k) cin[k] = !BND || (i + k >= 0 && i + k < nx);
+    const int m0 = i0 / 2 - 1;  // first coarse column needed (i0 even)
     const double tX0 = (HAS_C && cin[0]) ? __ldg(P.tx + i) : 0.0;
     const double tX2 = (HAS_C && cin[2]) ? __ldg(P.tx + i + 2) : 0.0;
-    double omega = 0.0;
-    if constexpr (SK == K3_CORRECT) omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0);
 
     const int Jbeg = j0 - M;
     const int Jend = j1 - 1 + M;
     auto slot_of = [](int J) { return (J + 8) & (D - 1); };
     auto chunk_bytes = [&](int c) { return (c >= 0 && c < nx) ? (c + 1 < nx ? 16 : 8) : 0; };
-    const int cb0 = chunk_bytes(i), cb1 = chunk_bytes(i + 2);
+    const int cb0 = BND ? chunk_bytes(i) : 16, cb1 = BND ? chunk_bytes(i + 2) : 16;
     // running pointers of the next row to stage / the next row to store
     const long long pitch = fg.pitch;
     long long soff = (long long)Jbeg * pitch + i;
     long long roff = soff;
+    const long long cpitch = P.cg.pitch;
     auto stage_crow = [&](int q) {
         double* dst = S.c[(q + 8) & (D - 1)];
-        stage_coarse(dst + 2 * lane, P.uc, P.cg, m0 + 2 * lane, q);
-        stage_coarse(dst + 2 * lane + 1, P.uc, P.cg, m0 + 2 * lane + 1, q);
-        if (lane == 0) stage_coarse(dst + 64, P.uc, P.cg, m0 + 64, q);
+        if constexpr (BND) {
+            stage_coarse(dst + COFF + 2 * lane, P.uc, P.cg, m0 + 2 * lane, q);
+            stage_coarse(dst + COFF + 2 * lane + 1, P.uc, P.cg, m0 + 2 * lane + 1, q);
+            if (lane == 0) stage_coarse(dst + COFF + 64, P.uc, P.cg, m0 + 64, q);
+        } else {
+            // all of [m0, m0 + 64] x {q} is inside the coarse grid: aligned pairs
+            const double* src = P.uc + (long long)q * cpitch + (m0 - COFF);
+            cpa16(dst + 2 * lane, src + 2 * lane, 16);
+            if (lane == 0) cpa8(dst + COFF + 64, src + COFF + 64, 8);
+            if (COFF && lane == 1) cpa8(dst + 64, src + 64, 8);
+        }
     };
     auto stage = [&](int J) {
         const int sl = slot_of(J);
-        const bool row_in = J >= 0 && J < ny;
+        const bool row_in = !BND || (J >= 0 && J < ny);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const int bytes = row_in ? (h ? cb1 : cb0) : 0;
-            const long long o = bytes ? soff + 2 * h : 0;
-            cpa16(&S.g[sl][h][lane], g + o, bytes);
-            if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], u + o, bytes);
+            if constexpr (BND) {
+                const int bytes = row_in ? (h ? cb1 : cb0) : 0;
+                const long long o = bytes ? soff + 2 * h : 0;
+                cpa16(&S.g[sl][h][lane], g + o, bytes);
+                if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], u + o, bytes);
+            } else {
+                cpa16(&S.g[sl][h][lane], g + soff + 2 * h, 16);
+                if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], u + soff + 2 * h, 16);
+            }
         }
         soff += pitch;
         if constexpr (HAS_C) {
@@ -106,7 +120,7 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
     auto source = [&](int J, int sl, double (&nv)[4]) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) nv[k] = 0.0;
-        if (J < 0 || J >= ny) return;
+        if (BND && (J < 0 || J >= ny)) return;
         if constexpr (SK == K3_U) {
             const double2 a = S.u[sl][0][lane];
             const double2 b = S.u[sl][1][lane];
@@ -118,20 +132,20 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
         if constexpr (HAS_C) {
             const int qf = (J + 8) / 2 - 4;  // floor(J/2)
             const bool even = ((J + 8) & 1) == 0;
-            const double* ca = &S.c[((even ? qf - 1 : qf) + 8) & (D - 1)][2 * lane];
-            const double* cb = &S.c[(qf + 8) & (D - 1)][2 * lane];
+            const double* ca = &S.c[((even ? qf - 1 : qf) + 8) & (D - 1)][COFF + 2 * lane];
+            const double* cb = &S.c[(qf + 8) & (D - 1)][COFF + 2 * lane];
             Pair2Raw r;
             r.ty = ((J + 1) & 1) ? __ldg(P.ty + J) : 0.0;
             r.a = ca[0];
             r.b = ca[1];
             r.c = cb[0];
             r.d = cb[1];
-            const double2 p0 = prolong2_make(r, i, J, nx, tX0);
+            const double2 p0 = prolong2_make(r, BND ? i : 0, J, BND ? nx : 4, tX0);
             r.a = ca[1];
             r.b = ca[2];
             r.c = cb[1];
             r.d = cb[2];
-            const double2 p1 = prolong2_make(r, i + 2, J, nx, tX2);
+            const double2 p1 = prolong2_make(r, BND ? i + 2 : 0, J, BND ? nx : 4, tX2);
             if constexpr (SK == K3_PROLONG) {
                 nv[0] = p0.x;
                 nv[1] = p0.y;
@@ -152,8 +166,16 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                 if (!cin[k]) nv[k] = 0.0;
         }
     };
+    // lanes 0 and 31 hold the halo columns: with H = 2 each still produces one pair
+    const bool st_lo = lane > 0 && (H == 2 || lane < 31);   // columns 4l, 4l+1
+    const bool st_hi = lane < 31 && (H == 2 || lane > 0);   // columns 4l+2, 4l+3
     auto store = [&](long long off, const double (&v)[4]) {
         double* o = out + off;
+        if constexpr (!BND && H > 0) {
+            if (st_lo) *reinterpret_cast<double2*>(o) = make_double2(v[0], v[1]);
+            if (st_hi) *reinterpret_cast<double2*>(o + 2) = make_double2(v[2], v[3]);
+            return;
+        }
         if (!edge && lane > 0 && lane < 31) {  // all four columns are produced here
             *reinterpret_cast<double2*>(o) = make_double2(v[0], v[1]);
             *reinterpret_cast<double2*>(o + 2) = make_double2(v[2], v[3]);
@@ -178,15 +200,22 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
     cpa_wait<D - 2>();
     __syncwarp();
 
+    // register windows: w[l] = rows J-l, J-l-1, J-l-2 of step l's input; gw = the
+    // right-hand side of rows J, J-1, .. J-M. Slots are named by PH = (J - Jbeg) mod 3
+    // (w) so the unrolled-by-3 row loop rotates them by renaming; gw is a 3-slot ring
+    // as well when M <= 2, else a shifted window.
     double w[ML][3][4];
-    double gr[ML][4];
+    constexpr bool GRING = M <= 2 && !BND;
+    constexpr int GS = GRING ? 3 : ML + 1;
+    double gw[GS][4];
 #pragma unroll
     for (int l = 0; l < ML; ++l)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            w[l][0][k] = w[l][1][k] = w[l][2][k] = 0.0;
-            gr[l][k] = 0.0;
-        }
+        for (int k = 0; k < 4; ++k) w[l][0][k] = w[l][1][k] = w[l][2][k] = 0.0;
+#pragma unroll
+    for (int q = 0; q < GS; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gw[q][k] = 0.0;
 
     // one row J; PH = (J - Jbeg) mod 3 names the window slots statically
     auto row = [&](int J, auto ph) {
@@ -200,20 +229,28 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
         if constexpr (M == 0) {
             if (J >= j0 && J < j1) store(rJ, nv);
         } else {
-            double gn[4];
+            // g of row J into its slot (ring: slot PH; shifted window: slot 0 after the shift)
+            constexpr int gJ = GRING ? PH : 0;
+            if constexpr (!GRING) {
+#pragma unroll
+                for (int q = GS - 1; q > 0; --q)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) gw[q][k] = gw[q - 1][k];
+            }
             {
                 const double2 a = S.g[sl][0][lane];
                 const double2 b = S.g[sl][1][lane];
-                gn[0] = a.x;
-                gn[1] = a.y;
-                gn[2] = b.x;
-                gn[3] = b.y;
+                gw[gJ][0] = a.x;
+                gw[gJ][1] = a.y;
+                gw[gJ][2] = b.x;
+                gw[gJ][3] = b.y;
             }
 #pragma unroll
             for (int l = 0; l < M; ++l) {
                 const int sn = (PH - l + 30) % 3;      // newest row J-l
                 const int sc = (PH - l - 1 + 30) % 3;  // centre row J-l-1
                 const int sd = (PH - l - 2 + 30) % 3;  // row J-l-2
+                const int gs = GRING ? (PH - l - 1 + 30) % 3 : l + 1;  // g of row J-l-1
 #pragma unroll
                 for (int k = 0; k < 4; ++k) w[l][sn][k] = nv[k];
                 const int R = J - l - 1;
@@ -226,7 +263,7 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                     const double xw = k == 0 ? xl : w[l][sc][k - 1];
                     const double xe = k == 3 ? xr : w[l][sc][k + 1];
                     y[k] = jacobi_point_fast(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe, w[l][sd][k],
-                                             w[l][sn][k], gr[l][k], omega_damp, slow[k]);
+                                             w[l][sn][k], gw[gs][k], omega_damp, slow[k]);
                 }
                 if constexpr (Coef::kMaySlow) {
                     // one warp vote per fused step and row; the exact division only where asked
@@ -236,41 +273,88 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
                             const double xw = k == 0 ? xl : w[l][sc][k - 1];
                             const double xe = k == 3 ? xr : w[l][sc][k + 1];
                             y[k] = jacobi_point(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe,
-                                                w[l][sd][k], w[l][sn][k], gr[l][k], omega_damp);
+                                                w[l][sd][k], w[l][sn][k], gw[gs][k], omega_damp);
                         }
                     }
                 }
-                if (R < 0 || R >= ny) {
+                if constexpr (BND) {
+                    if (R < 0 || R >= ny) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) y[k] = 0.0;
-                } else if (edge) {
+                        for (int k = 0; k < 4; ++k) y[k] = 0.0;
+                    } else if (edge) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (!cin[k]) y[k] = 0.0;
+                        for (int k = 0; k < 4; ++k)
+                            if (!cin[k]) y[k] = 0.0;
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) nv[k] = y[k];
             }
             const int RM = J - M;
-            if (RM >= j0 && RM < j1) store(rJ - M * pitch, nv);
-#pragma unroll
-            for (int l = ML - 1; l > 0; --l)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) gr[l][k] = gr[l - 1][k];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) gr[0][k] = gn[k];
+            if (RM >= j0 && (!BND || RM < j1)) store(rJ - M * pitch, nv);
         }
         cpa_wait<D - 2>();  // row J+1 has landed (for this lane)
         __syncwarp();       // ... for every lane; slot of row J is free again
     };
-    for (int J = Jbeg; J <= Jend; J += 3) {
-        row(J, std::integral_constant<int, 0>{});
-        if (J + 1 > Jend) break;
-        row(J + 1, std::integral_constant<int, 1>{});
-        if (J + 2 > Jend) break;
-        row(J + 2, std::integral_constant<int, 2>{});
+    if constexpr (BND && M >= 3) {
+        // the rare path (first/last strips and row segments) stays small in the instruction
+        // cache: one row body, the windows shifted by moves (slot names of PH = 0)
+#pragma unroll 1
+        for (int J = Jbeg; J <= Jend; ++J) {
+            row(J, std::integral_constant<int, 0>{});
+#pragma unroll
+            for (int l = 0; l < M; ++l) {
+                const int sn = (30 - l) % 3, sc = (29 - l) % 3, sd = (28 - l) % 3;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    w[l][sd][k] = w[l][sc][k];
+                    w[l][sc][k] = w[l][sn][k];
+                }
+            }
+        }
+    } else {
+        for (int J = Jbeg; J <= Jend; J += 3) {
+            row(J, std::integral_constant<int, 0>{});
+            if (J + 1 > Jend) break;
+            row(J + 1, std::integral_constant<int, 1>{});
+            if (J + 2 > Jend) break;
+            row(J + 2, std::integral_constant<int, 2>{});
+        }
     }
     cpa_wait<0>();
+}
+
+template <int M, int SK, class Coef>
+__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
+    k_smooth4(Grid fg, Coef A, const double* __restrict__ u, Prolong P, OmegaSrc om, const double* __restrict__ g,
+              double* __restrict__ out, double omega_damp, int seg) {
+    pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
+    pdl_trigger();
+    using SM = Smooth4Smem<SK>;
+    constexpr int H = (M + 1) & ~1;  // halo columns, even: 16-B aligned strips
+    constexpr int OW = 128 - 2 * H;  // columns each strip produces
+    extern __shared__ __align__(16) unsigned char sm4raw[];
+    SM& S = reinterpret_cast<SM*>(sm4raw)[threadIdx.x >> 5];
+
+    const int strip = blockIdx.x * kS4W + (threadIdx.x >> 5);
+    const int i0 = strip * OW - H;
+    if (i0 + H >= fg.nx) return;  // warp-uniform; the kernel has no block barriers
+    const int j0 = fg.w0 + blockIdx.y * seg;
+    const int j1 = min(j0 + seg, fg.w1);
+    double omega = 0.0;
+    if constexpr (SK == K3_CORRECT) omega = om.get(blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0);
+    // interior: the strip's 128 columns, every row it stages (j0-M .. j1-1+M+D-1) and their
+    // coarse parents (rows >= 2 and <= ny-3 have both) are inside the domain
+    bool interior = i0 >= 4 && i0 + 128 <= fg.nx && j0 - M >= 2 && j1 + M + SM::D <= fg.ny - 2;
+    if constexpr (SM::HAS_C)  // ... which the nested grids guarantee (fine n = 2 coarse n + 1); checked anyway
+        interior = interior && i0 / 2 + 63 < P.cg.nx && (j1 + M + SM::D) / 2 < P.cg.ny;
+    // The split pays for M >= 3 (C5's 3+3: -18% on the finest level; the one-path loop is
+    // instruction-cache bound there). For M <= 2 the single general loop measured faster
+    // (C4 finest post-smoother 0.336 vs 0.354 ms), so every strip takes it.
+    if (M >= 3 && interior)
+        smooth4_march<M, SK, Coef, false>(S, fg, A, u, P, omega, g, out, omega_damp, i0, j0, j1);
+    else
+        smooth4_march<M, SK, Coef, true>(S, fg, A, u, P, omega, g, out, omega_damp, i0, j0, j1);
 }
 
 // ---------------------------------------------------------------------------

@@ -767,140 +767,202 @@ __device__ double warp_walk(const TG& tg, int s, double sv, long long k0, long l
     return sv;
 }
 
-// grid (NS); block kSsT; dynamic smem 2 * kSsBatch records. Warp 0 replays,
-// warps 1.. stage the next batch.
+// Shared memory of the chain (dynamic): two batches of records (the next batch is
+// staged while the current one replays), the serial step's operands of both
+// batches, and the state entering every record of the current batch.
+struct ChainOps {
+    long long d[kSsBatch];  // run step on the sum's bit pattern (see chain_decode)
+    double pb[kSsBatch];    // break term (-0.0: none)
+    int ft[kSsBatch];       // parity handling: bit 0 = f, bit 1 = t (see chain_decode)
+};
+struct ChainSmem {
+    gmg_ss::Rec buf[2][kSsBatch];
+    ChainOps op[2];
+    double before[kSsBatch];
+    double ltile[kSsLitTile];  // literal re-sum staging
+};
+
+// Operands of one record's serial step. In a valid run the sum keeps its binade
+// and sign, so s + Q*u is the integer add of D = +-Q to the double's bit pattern
+// (the magnitude grows by Q for a positive sum, by -Q for a negative one). Q has
+// one value per parity of the state entering the run (ties, seqsum_core.h), at
+// most one unit apart; the step is written branch-free as
+//     bits += d + ((bits ^ f) & t),
+// d = the smaller of the two steps, t = 1 if they differ, f = 1 if the even
+// state takes the larger one. An empty run adds 0; a record without a break
+// element adds -0.0 afterwards (the exact identity). `ok` = false (never seen;
+// the variants would have to differ by more than a unit) forces the fallback.
+__device__ __forceinline__ void chain_decode(const gmg_ss::Rec& r, long long& d, int& ft, double& pb, bool& ok) {
+    const uint32_t meta = r.meta;
+    const bool brk = (meta >> 12) & 1u, ne = (meta >> 15) & 1u, negr = (meta >> 11) & 1u;
+    const long long D0 = ne ? (negr ? -r.Q[0] : r.Q[0]) : 0;
+    const long long D1 = ne ? (negr ? -r.Q[1] : r.Q[1]) : 0;
+    d = D0 < D1 ? D0 : D1;
+    ft = (D0 != D1 ? 2 : 0) | (D0 > D1 ? 1 : 0);
+    ok = D0 - D1 <= 1 && D1 - D0 <= 1;
+    pb = brk ? r.pb : -0.0;
+}
+
+// Is record r valid from the exact state `before` entering it? (seg_valid on the
+// double's bits; literal and bad records never are.)
+__device__ __forceinline__ bool chain_valid(const gmg_ss::Rec& r, double before) {
+    const uint32_t meta = r.meta;
+    const bool lit = (meta >> 14) & 1u, ne = (meta >> 15) & 1u;
+    const uint64_t Er = meta & 0x7ffu;
+    const bool negr = (meta >> 11) & 1u, badr = (meta >> 13) & 1u;
+    const uint64_t bits = gmg_ss::dbits(before);
+    const uint64_t E = (bits >> 52) & 0x7ffu;
+    const bool v = (bits & 1u) != 0;
+    const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
+    const long long mni = v ? r.mn[1] : r.mn[0], mxi = v ? r.mx[1] : r.mx[0];
+    const bool neg = bits >> 63;
+    const long long lo_v = neg ? mant - mxi : mant + mni;
+    const long long hi_v = neg ? mant - mni : mant + mxi;
+    const bool ok_run = E >= (uint64_t)gmg_ss::kEMin && E <= (uint64_t)gmg_ss::kEMax && E == Er && neg == negr &&
+                        lo_v >= gmg_ss::kLo && hi_v <= gmg_ss::kHi;
+    return !lit && !badr && (!ne || ok_run);
+}
+
+// The serial replay of records [q0, cnt) of a decoded batch by one warp, from
+// state sv: per record an integer add on the sum's bits (run step) and one fp64
+// add (break term) — the only serial dependence is on the sum itself; the
+// operands of 32 records sit one per lane and are broadcast by shuffles, off the
+// chain. The state entering each record is kept for the validation that
+// follows. Nothing is validated here: the caller checks every record against
+// before[] afterwards and resumes from the first failure.
+__device__ __forceinline__ double chain_serial(const ChainOps& op, double* before, int q0, int cnt, double sv) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    for (int g = q0; g < cnt; g += 32) {
+        const int gn = min(32, cnt - g);
+        const int q = g + (lane < gn ? lane : 0);
+        const long long d = op.d[q];
+        const double pb = op.pb[q];
+        const int ft = op.ft[q];
+        double x = sv, bf = sv;
+        auto step = [&](int k) {
+            const long long dk = __shfl_sync(full, d, k);
+            const double pk = __shfl_sync(full, pb, k);
+            const unsigned ftk = (unsigned)__shfl_sync(full, ft, k);
+            const unsigned tk = ftk >> 1;
+            if (lane == k) bf = x;
+            const uint64_t bits = gmg_ss::dbits(x);
+            const unsigned e = ((unsigned)bits ^ ftk) & tk;
+            x = gmg_ss::bitsd(bits + (uint64_t)dk + e) + pk;
+        };
+        if (gn == 32) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) step(k);
+        } else {
+            for (int k = 0; k < gn; ++k) step(k);
+        }
+        if (lane < gn) before[g + lane] = bf;
+        sv = x;
+    }
+    return sv;
+}
+
+// grid (NS); block kSsT; dynamic smem ss_chain_smem(). Per batch of kSsBatch records:
+// warp 0 replays the batch serially (chain_serial) while warps 1.. stage and decode the
+// next one; then all threads validate the batch in parallel against the states warp 0
+// recorded. From the first record that fails (a wrong speculation, a literal chunk) the
+// results are discarded: that record's element range is re-summed literally from the
+// true state, and the replay resumes after it.
 template <class TG>
 __device__ __forceinline__ void ss_chain_body(const TG& tg, long long n, const SsState& S, int s,
                                               double* __restrict__ out, const double* __restrict__ start,
                                               unsigned char* smraw) {
-    gmg_ss::Rec* buf = reinterpret_cast<gmg_ss::Rec*>(smraw);
-    __shared__ longlong2 cD[32];  // per record of the current group: signed run steps (parity 0, 1)
-    __shared__ double2 cPB[32];   // break term (-0.0 if none), tie flag
-    __shared__ double ltile[kSsLitTile];  // literal re-sum staging
+    ChainSmem& M = *reinterpret_cast<ChainSmem*>(smraw);
+    __shared__ int s_fail;
+    __shared__ double s_sv;
+    __shared__ unsigned long long s_nbrk;
     const int t = threadIdx.x;
     const int total = *S.total;
     const int nb = (total + kSsBatch - 1) / kSsBatch;
-
-    for (int q = t; q < min(total, kSsBatch); q += kSsT) buf[q] = S.recs2[q];
+    unsigned n_brk = 0;  // break records this thread staged (stats)
+    auto stage_batch = [&](int b, int t0, int nt) {
+        const int cn = min(kSsBatch, total - b * kSsBatch);
+        const gmg_ss::Rec* src = S.recs2 + (long long)b * kSsBatch;
+        gmg_ss::Rec* B = M.buf[b & 1];
+        ChainOps& O = M.op[b & 1];
+        for (int q = t0; q < cn; q += nt) {
+            gmg_ss::Rec r = src[q];
+            n_brk += (r.meta >> 12) & 1u;
+            bool ok;
+            chain_decode(r, O.d[q], O.ft[q], O.pb[q], ok);
+            if (!ok) r.meta |= 1u << 13;  // bad: re-summed literally
+            B[q] = r;
+        }
+    };
+    if (nb > 0) stage_batch(0, t, kSsT);
+    if (t == 0) s_nbrk = 0ull;
     __syncthreads();
 
-    // Exact running sum kept as a double. While a record's run validates, the
-    // sum stays inside one binade whose spacing is u = 2^(E-1075), so
-    // s + Q*u is exact (Q*u: power-of-two scaling; the result is representable)
-    // and the integer state is M = s * 2^(1075-E), also exact.
     double sv = start ? start[s] : 0.0;  // exact state entering this range (earlier row slabs)
-    long long prev = -1;  // global index of the last element consumed
-    unsigned long long n_brk = 0, n_lit = 0, n_litterms = 0, cyc_lit = 0, n_dense = 0, cyc_dense = 0;
+    long long prev = -1;                 // global index of the last element consumed
+    unsigned long long n_lit = 0, n_litterms = 0, cyc_lit = 0, n_dense = 0, cyc_dense = 0;
     const long long cyc0 = clock64();
     for (int b = 0; b < nb; ++b) {
-        const gmg_ss::Rec* A = buf + (b & 1) * kSsBatch;
+        const gmg_ss::Rec* A = M.buf[b & 1];
+        const ChainOps& O = M.op[b & 1];
         const int cnt = min(kSsBatch, total - b * kSsBatch);
-        if (t < 32) {
-            // Speculate serially, validate in parallel. For 32 records at a time:
-            //  (1) each lane decodes one record into the state-independent operands of
-            //      its fast step: in a valid run the sum keeps its binade and sign, so
-            //      s + Q*u is the integer add bits + D on the representation (D = +-Q,
-            //      one value per tie parity), then the break's real add (+(-0.0), the
-            //      exact identity, for a record without a break);
-            //  (2) the warp applies the 32 fast steps in order (~7 instructions each,
-            //      the only serial dependence is on the sum's bits);
-            //  (3) each lane validates its record against the state it was applied to;
-            //      from the first failure on, results are discarded, that record is
-            //      re-summed exactly from the true state and speculation resumes.
-            const int lane = t;
-            int q0 = 0;
-            while (q0 < cnt) {
-                const int gn = min(32, cnt - q0);
-                const bool act = lane < gn;
-                const gmg_ss::Rec& r = A[q0 + (act ? lane : 0)];
-                const uint32_t meta = r.meta;
-                const bool brk = (meta >> 12) & 1u, lit = (meta >> 14) & 1u, ne = (meta >> 15) & 1u;
-                const uint64_t Er = meta & 0x7ffu;
-                const bool negr = (meta >> 11) & 1u, badr = (meta >> 13) & 1u;
-                const bool ties = (r.Q[0] != r.Q[1]) | (r.mn[0] != r.mn[1]) | (r.mx[0] != r.mx[1]);
-                const long long D0 = ne ? (negr ? -r.Q[0] : r.Q[0]) : 0;
-                const long long D1 = ne ? (negr ? -r.Q[1] : r.Q[1]) : 0;
-                const long long kbl = r.kb;
-                cD[lane] = make_longlong2(D0, D1);
-                cPB[lane] = make_double2(brk ? r.pb : -0.0, __longlong_as_double(ties ? 1ll : 0ll));
-                __syncwarp();
-                double x = sv, before = sv;
-                if (!__any_sync(0xffffffffu, act && ties)) {
-                    // no tie in the group: one parity variant, the chain is integer add + fp64 add
-#pragma unroll 8
-                    for (int k = 0; k < gn; ++k) {
-                        if (lane == k) before = x;
-                        x = gmg_ss::bitsd(gmg_ss::dbits(x) + (uint64_t)cD[k].x) + cPB[k].x;
-                    }
-                } else {
-#pragma unroll 4
-                    for (int k = 0; k < gn; ++k) {
-                        if (lane == k) before = x;
-                        const longlong2 dd = cD[k];
-                        const double2 pt = cPB[k];
-                        const uint64_t bits = gmg_ss::dbits(x);
-                        const long long D = (bits & (uint64_t)__double_as_longlong(pt.y)) ? dd.y : dd.x;
-                        x = gmg_ss::bitsd(bits + (uint64_t)D) + pt.x;
-                    }
-                }
-                // (3) validation of record lane against `before`
-                bool ok = true;
-                if (act) {
-                    const uint64_t bits = gmg_ss::dbits(before);
-                    const uint64_t E = (bits >> 52) & 0x7ffu;
-                    const bool v = ties && (bits & 1u);
-                    const long long mant = (long long)((bits & ((1ull << 52) - 1)) | (1ull << 52));
-                    const long long mni = v ? r.mn[1] : r.mn[0], mxi = v ? r.mx[1] : r.mx[0];
-                    const bool neg = bits >> 63;
-                    const long long lo_v = neg ? mant - mxi : mant + mni;
-                    const long long hi_v = neg ? mant - mni : mant + mxi;
-                    const bool ok_run = E >= (uint64_t)gmg_ss::kEMin && E <= (uint64_t)gmg_ss::kEMax && E == Er &&
-                                        neg == negr && lo_v >= gmg_ss::kLo && hi_v <= gmg_ss::kHi;
-                    ok = !lit && !badr && (!ne || ok_run);
-                }
-                const unsigned fail = __ballot_sync(0xffffffffu, !ok);
-                const unsigned brkm = __ballot_sync(0xffffffffu, act && brk);
-                __syncwarp();
-                if (!fail) {
-                    sv = x;
-                    prev = __shfl_sync(0xffffffffu, kbl, gn - 1);
-                    n_brk += __popc(brkm);
-                    q0 += gn;
-                    continue;
-                }
-                const int f = __ffs(fail) - 1;
-                n_brk += __popc(brkm & ((2u << f) - 1u));
-                sv = __shfl_sync(0xffffffffu, before, f);
-                const long long pf = f > 0 ? __shfl_sync(0xffffffffu, kbl, f - 1) : prev;
-                const gmg_ss::Rec& rf = A[q0 + f];
+        int q0 = 0;
+        bool staged = false;
+        while (q0 < cnt) {
+            if (t < 32) {
+                const double r = chain_serial(O, M.before, q0, cnt, sv);
+                if (t == 0) s_sv = r;
+            } else if (!staged && b + 1 < nb) {
+                stage_batch(b + 1, t - 32, kSsT - 32);
+            }
+            staged = true;
+            if (t == 0) s_fail = cnt;
+            __syncthreads();
+            // validation of records [q0, cnt) against the states they were applied to
+            int f = cnt;
+            for (int q = q0 + t; q < cnt; q += kSsT)
+                if (!chain_valid(A[q], M.before[q])) f = min(f, q);
+            if (f < cnt) atomicMin(&s_fail, f);
+            __syncthreads();
+            f = s_fail;
+            if (f == cnt) {
+                sv = s_sv;
+                prev = A[cnt - 1].kb;
+                q0 = cnt;
+            } else {
+                // re-sum the failed record's range exactly from the true state (the break
+                // element, if any, is applied after; otherwise kb is inclusive): plain
+                // left-to-right adds — a failed record sits where the sum crosses binades
+                // often, and there the literal chain (~6 cycles/term) beats an integer walk
+                const gmg_ss::Rec& rf = A[f];
                 const bool brk_f = (rf.meta >> 12) & 1u, lit_f = (rf.meta >> 14) & 1u;
                 const long long kb_f = rf.kb;
-                // re-walk the failed record's range exactly from the true state (the break
-                // element, if any, is applied below; otherwise kb is inclusive)
+                const long long pf = f > 0 ? (long long)A[f - 1].kb : prev;
                 const long long k1 = min(brk_f ? kb_f : kb_f + 1, n);
-                const long long c0 = clock64();
-                // plain left-to-right adds: a failed record sits where the sum crosses
-                // binades often, and there the literal chain (~6 cycles/term) beats the
-                // warp's integer walk, which restarts at every break
-                (void)lit_f;
-                const double s1 = literal_sum(tg, s, sv, pf + 1, k1, ltile);
-                cyc_lit += clock64() - c0;
-                ++n_lit;
-                n_litterms += k1 - (pf + 1);
-                if (lit_f) {
-                    ++n_dense;
-                    cyc_dense += clock64() - c0;
+                double s1 = M.before[f];
+                if (t < 32) {
+                    const long long c0 = clock64();
+                    s1 = literal_sum(tg, s, s1, pf + 1, k1, M.ltile);
+                    cyc_lit += clock64() - c0;
+                    ++n_lit;
+                    n_litterms += k1 - (pf + 1);
+                    if (lit_f) {
+                        ++n_dense;
+                        cyc_dense += clock64() - c0;
+                    }
+                    if (t == 0) s_sv = brk_f ? s1 + rf.pb : s1;
                 }
-                sv = brk_f ? s1 + rf.pb : s1;
+                __syncthreads();
+                sv = s_sv;
                 prev = kb_f;
-                q0 += f + 1;
+                q0 = f + 1;
             }
-        } else if (b + 1 < nb) {
-            gmg_ss::Rec* B = buf + ((b + 1) & 1) * kSsBatch;
-            const int cn = min(kSsBatch, total - (b + 1) * kSsBatch);
-            const gmg_ss::Rec* src = S.recs2 + (long long)(b + 1) * kSsBatch;
-            for (int q = t - 32; q < cn; q += kSsT - 32) B[q] = src[q];
+            __syncthreads();  // s_fail / s_sv / before[] are rewritten by the next round
         }
+    }
+    if (S.stats) {
+        n_brk = __reduce_add_sync(0xffffffffu, n_brk);
+        if ((t & 31) == 0 && n_brk) atomicAdd(&s_nbrk, (unsigned long long)n_brk);
         __syncthreads();
     }
     if (t == 0) {
@@ -910,7 +972,7 @@ __device__ __forceinline__ void ss_chain_body(const TG& tg, long long n, const S
             atomicAdd(S.stats + 1, (unsigned long long)total);
             atomicAdd(S.stats + 2, (unsigned long long)(clock64() - cyc0));
             atomicAdd(S.stats + 3, cyc_lit);
-            atomicAdd(S.stats + 4, n_brk);
+            atomicAdd(S.stats + 4, s_nbrk);
             atomicAdd(S.stats + 5, n_lit);
             atomicAdd(S.stats + 6, n_litterms);
             atomicAdd(S.stats + 14, n_dense);
@@ -1006,7 +1068,7 @@ __global__ void __launch_bounds__(kSsT) k_ss_partial(TG tg, long long n, double*
 
 template <int EPT>
 constexpr size_t ss_walk_smem() { return sizeof(double) * (kSsWT * EPT + kSsWT * EPT / 32); }
-constexpr size_t ss_chain_smem() { return sizeof(gmg_ss::Rec) * 2 * kSsBatch; }
+constexpr size_t ss_chain_smem() { return sizeof(ChainSmem); }
 
 // ---- term generators ----------------------------------------------------------
 // row index j = k / nx without an integer division: fp64 estimate + exact fix-up
