@@ -837,6 +837,7 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
     CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
     if (g_debug_sync) dbg_sync(__LINE__);
     set_smem(k_gs_wave<Pol>, gs_smem());
+    prof_tag("gs wavefront", L.l, (Pol::UPDATE ? 24.0 : 16.0) * (double)L.nx * L.ny);
     launch_k(k_gs_wave<Pol>, blocks, kGsWarps * 32, gs_smem(), p->st, L.grid(), pol, d, x, xo, damp, p->gs_edge,
                                                                  p->gs_prog);
     KCHECK();

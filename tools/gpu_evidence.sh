@@ -9,16 +9,19 @@ for tool in racecheck synccheck memcheck; do
 done
 # the bench's launch list (C4; serialised, cold-cache: shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -c 1300 --csv --log-file gpurun_out/r02_c4_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+  -c 1300 --csv --log-file gpurun_out/r02b_c4_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
   --no-c5 --no-per-level --e2e-steps 1 > gpurun_out/ncu_launch.log 2>&1
 # full captures (one launch each)
-bash tools/ncu_capture.sh r02_walk_norm k_ss_walk 0 python tools/profile_cycle.py --cycles 1
-bash tools/ncu_capture.sh r02_walk_arr k_ss_walk 29 python tools/profile_cycle.py --cycles 1
-bash tools/ncu_capture.sh r02_scan_chain k_ss_scan_chain 0 python tools/profile_cycle.py --cycles 1
-bash tools/ncu_capture.sh r02_resid4 k_resid4 0 python tools/profile_cycle.py --cycles 1
-bash tools/ncu_capture.sh r02_smooth4_correct k_smooth4 0 python tools/smoother_probe.py --levels 13 --alphas 1 --steps 2 --variants 1 --reps 1
-bash tools/ncu_capture.sh r02_smooth4_pe k_smooth4 0 python tools/smoother_probe.py --levels 13 --alphas 1 --steps 2 --variants 0 --reps 1
-bash tools/ncu_capture.sh r02_smooth4_c5_m3 k_smooth4 0 python tools/smoother_probe.py --levels 14 --alphas 1e-2 --steps 3 --variants 1 --reps 1
-bash tools/ncu_capture.sh r02_omega4 k_omega4 0 python tools/profile_cycle.py --cycles 1
-rm -f gpurun_out/*.sass.csv
+bash tools/ncu_capture.sh r02b_walk_norm k_ss_walk 0 python tools/profile_cycle.py --cycles 1
+bash tools/ncu_capture.sh r02b_walk_arr k_ss_walk 29 python tools/profile_cycle.py --cycles 1
+bash tools/ncu_capture.sh r02b_scan_chain k_ss_scan_chain 0 python tools/profile_cycle.py --cycles 1
+bash tools/ncu_capture.sh r02b_resid4 k_resid4 0 python tools/profile_cycle.py --cycles 1
+bash tools/ncu_capture.sh r02b_smooth4_correct k_smooth4 0 python tools/smoother_probe.py --levels 13 --alphas 1 --steps 2 --variants 1 --reps 1
+bash tools/ncu_capture.sh r02b_smooth4_pe k_smooth4 0 python tools/smoother_probe.py --levels 13 --alphas 1 --steps 2 --variants 0 --reps 1
+bash tools/ncu_capture.sh r02b_smooth4_c5_m3 k_smooth4 0 python tools/smoother_probe.py --levels 14 --alphas 1e-2 --steps 3 --variants 1 --reps 1
+bash tools/ncu_capture.sh r02b_omega4 k_omega4 0 python tools/profile_cycle.py --cycles 1
+
 ls -la gpurun_out
+bash tools/ncu_capture.sh r02b_gs_wave k_gs_wave 0 python tools/gs_step.py 10 1e-2
+
+rm -f gpurun_out/*.sass.csv; ls gpurun_out | head -80
