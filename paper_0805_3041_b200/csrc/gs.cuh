@@ -10,80 +10,114 @@
 //
 // Mapping: lane r of warp w owns row j = 32w + r and, at step tau, handles
 // column i = tau - r, one column behind the row above. z(i,j-1) comes from
-// lane r-1 by a warp shuffle (computed on the previous step).
+// lane r-1 by a warp shuffle (computed on the previous step). With one warp per
+// scheduler the sweep is bound by the latency of everything a step issues, so
+// the step is kept to the recurrence itself:
 //   * Operands: each warp stages its 32 rows of d and x through shared memory,
-//     32 columns at a time with coalesced cp.async copies, three blocks deep,
-//     so the sequential loop only ever touches shared memory.
-//   * The row above a warp (lane 31 of the warp before) arrives through a
-//     shared-memory ring with block-scope progress counters inside a CTA, and
-//     through global memory with release/acquire flags between CTAs.
+//     32 columns at a time in coalesced 16-byte cp.async chunks, three blocks
+//     deep; results go back into the same slots and leave as 16-byte stores a
+//     block at a time. The sequential loop touches shared memory only.
+//   * The row above a warp (lane 31 of the warp before) arrives through global
+//     memory as 16-byte {value, generation} words, one per column, stored with a
+//     single relaxed vector store and fetched 16 columns at a time one window
+//     ahead of use: no flags, fences, progress counters or shared rings. The
+//     generation (one per launch) tells a fresh value from the previous sweep's.
+//     A window that is not complete yet is polled when it is needed (start-up
+//     only: the consumer then trails the producer far enough).
+//   * Coefficients and the finishing operand of the next column are fetched one
+//     step ahead (table/field operators, ILU factors).
 //   * All CTAs are co-resident (grid <= 148 CTAs of kGsWarps warps), so the
-//     spin-waits on predecessors always make progress.
-// The critical path per anti-diagonal is one division by c (a multiplication
-// when c is a power of two) + two multiply-subtracts + one shuffle. The same
-// kernel runs ILU(0)'s two triangular solves (policies below).
+//     polls on predecessors always make progress.
+// The critical path per anti-diagonal is one shuffle + two multiply-subtracts +
+// the division by c (a multiplication when c is a power of two, div_rcp from the
+// host-rounded reciprocal otherwise). The same kernel runs ILU(0)'s two
+// triangular solves (policies below).
 #pragma once
 
 #include "common.cuh"
 
 namespace gmg_dev {
 
-constexpr int kGsWarps = 4;     // warps (x 32 rows) per CTA
-constexpr int kGsRing = 128;    // intra-CTA edge ring (columns)
-constexpr int kGsPub = 4;       // progress published every kGsPub columns
-constexpr int kGsWin = 8;       // edge values fetched per refill
+constexpr int kGsWarps = 4;     // warps (x 32 rows) per CTA: one per scheduler
+constexpr int kGsWin = 16;      // edge values fetched per window
 constexpr int kGsBlk = 32;      // staged column block
 constexpr int kGsSlots = 3;     // staged blocks in flight
-constexpr int kGsStride = kGsBlk * kGsSlots + 2;  // even row stride: conflict-free diagonal reads
+constexpr int kGsCols = kGsBlk * kGsSlots;
+constexpr int kGsStride = kGsCols + 2;  // even row stride: conflict-free diagonal reads, 16-B chunks
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+__device__ __forceinline__ void cp_async16z(double* smem, const double* gmem, int bytes) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+// edge words {z bits, generation}: one relaxed 16-byte store / load (value and tag travel together)
+__device__ __forceinline__ void edge_store(longlong2* p, double z, long long gen) {
+    asm volatile("st.relaxed.gpu.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(__double_as_longlong(z)), "l"(gen)
+                 : "memory");
+}
+__device__ __forceinline__ longlong2 edge_load(const longlong2* p) {
+    longlong2 r;
+    asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+    return r;
+}
+
+__device__ __forceinline__ double lds64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void sts64(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
 // The recurrence a wave solves, z_k = finish(rhs_k - a1_k*z_left - a2_k*z_up):
 //   Gauss-Seidel/SOR   a1 = om*w, a2 = om*s, finish = /c        (smoother.cpp:297-309)
 //   ILU(0) forward     a1 = lw,   a2 = ls,   finish = identity  (smoother.cpp:318-325)
 //   ILU(0) backward    reversed order, a1 = e, a2 = n, finish = /d (smoother.cpp:326-334)
-// A policy gives a1/a2/finish at physical (i, j). REV runs the wave from the
-// last node backwards (logical (i, j) = physical (nx-1-i, ny-1-j)); UPDATE
+// A policy loads a1/a2 and its finishing operand f at physical (i, j) — one
+// step ahead of use — and finishes a point from them. REV runs the wave from
+// the last node backwards (logical (i, j) = physical (nx-1-i, ny-1-j)); UPDATE
 // writes x - damp*z, otherwise z itself.
-template <class Coef>
+struct GsOps {
+    double a1, a2, f;
+};
+
+// FIN: how z = acc / c is formed for constant operators (chosen on the host, common.cuh):
+// 0 = the class's own div_by_c, 1 = exact reciprocal multiply (c a power of two),
+// 2 = div_rcp from the host-rounded reciprocal.
+template <class Coef, int FIN = 0>
 struct GsPolicy {
     static constexpr bool REV = false, UPDATE = true;
     Coef A;
     double om;
-    __device__ __forceinline__ void coefs(int i, int j, double& a1, double& a2) const {
+    __device__ __forceinline__ void load(int i, int j, GsOps& o) const {
         double C, Wc, E, S, N;
         A.load(i, j, C, Wc, E, S, N);
-        a1 = om * Wc;
-        a2 = om * S;
+        o.a1 = om * Wc;
+        o.a2 = om * S;
+        o.f = C;
     }
-    __device__ __forceinline__ double finish(double acc, int i, int j) const { return A.div_by_c(acc, i, j); }
+    __device__ __forceinline__ double finish(double acc, const GsOps& o, int i, int j) const {
+        if constexpr (FIN == 1) return acc * A.inv_c;
+        else if constexpr (FIN == 2) return div_rcp(acc, A.c, A.rcp);
+        else return div_loaded(A, acc, o.f, i, j);
+    }
 };
 
 struct IluFwdPolicy {
     static constexpr bool REV = false, UPDATE = false;
     const double *lw, *ls;
     long long pitch;
-    __device__ __forceinline__ void coefs(int i, int j, double& a1, double& a2) const {
-        a1 = __ldg(lw + (long long)j * pitch + i);
-        a2 = __ldg(ls + (long long)j * pitch + i);
+    __device__ __forceinline__ void load(int i, int j, GsOps& o) const {
+        o.a1 = __ldg(lw + (long long)j * pitch + i);
+        o.a2 = __ldg(ls + (long long)j * pitch + i);
+        o.f = 0.0;
     }
-    __device__ __forceinline__ double finish(double acc, int, int) const { return acc; }
+    __device__ __forceinline__ double finish(double acc, const GsOps&, int, int) const { return acc; }
 };
 
 template <class Coef>
@@ -92,142 +126,244 @@ struct IluBwdPolicy {
     Coef A;
     const double* dp;
     long long pitch;
-    __device__ __forceinline__ void coefs(int i, int j, double& a1, double& a2) const {
+    __device__ __forceinline__ void load(int i, int j, GsOps& o) const {
         double C, Wc, E, S, N;
         A.load(i, j, C, Wc, E, S, N);
-        a1 = E;
-        a2 = N;
+        o.a1 = E;
+        o.a2 = N;
+        o.f = __ldg(dp + (long long)j * pitch + i);
     }
-    __device__ __forceinline__ double finish(double acc, int i, int j) const {
-        return acc / __ldg(dp + (long long)j * pitch + i);
-    }
+    __device__ __forceinline__ double finish(double acc, const GsOps& o, int, int) const { return acc / o.f; }
 };
 
-// dynamic smem: kGsWarps * 2 * 32 * kGsStride doubles
+// dynamic smem: kGsWarps * 2 * 32 * kGsStride doubles. gedge: [warps][epitch] edge words
+// (epitch >= nx), gstate: {generation, finished-CTA count}; both zero at allocation.
 template <class Pol>
 __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, const double* __restrict__ d,
                                                            const double* __restrict__ x, double* __restrict__ xo,
-                                                           double damp, double* __restrict__ gedge,
-                                                           int* __restrict__ gprog) {
+                                                           double damp, longlong2* __restrict__ gedge, int epitch,
+                                                           long long* __restrict__ gstate) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
     pdl_trigger();
-    extern __shared__ double stg[];
-    __shared__ double ring[kGsWarps][kGsRing];
-    __shared__ volatile int prog[kGsWarps];  // columns of row 32w+31 available in ring[w]
-    __shared__ volatile int cons[kGsWarps];  // columns of ring[w-1] consumed by warp w
+    extern __shared__ __align__(16) double stg[];
+    __shared__ long long s_gen;
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const int W = blockIdx.x * kGsWarps + w;  // global warp index
-    if (lane == 0) {
-        prog[w] = 0;
-        cons[w] = 0;
-    }
+    // This launch's generation = gstate[0] + 1, read once per CTA; the CTA that finishes its
+    // warp 0 last (gstate[1] counts them) advances gstate[0] for the next launch. A device
+    // counter, not a kernel argument: launches replayed from a CUDA graph get fresh tags too.
+    if (threadIdx.x == 0) s_gen = *reinterpret_cast<volatile long long*>(gstate) + 1;
     __syncthreads();
-    if (W * 32 >= g.ny) return;  // warp entirely below the grid
-    const int j = W * 32 + lane;
-    const bool row_ok = j < g.ny;
-    const int nx = g.nx;
+    const long long gen = s_gen;
+    if (W * 32 >= g.ny) return;  // warp entirely below the grid (no block barriers from here on)
+    const int nx = g.nx, ny = g.ny;
+    const int j = W * 32 + lane;  // logical row
+    const bool row_ok = j < ny;
+    const int pj = Pol::REV ? ny - 1 - j : j;
     const unsigned full = 0xffffffffu;
-    const bool from_global = (w == 0 && W > 0);
-    const bool to_global = (w == kGsWarps - 1) && (W + 1) * 32 < g.ny;
-    const bool to_ring = (w + 1 < kGsWarps) && (W + 1) * 32 < g.ny;
+    const bool has_up = W > 0;
+    const bool has_down = (W + 1) * 32 < ny;
     double* sd = stg + (size_t)w * 2 * 32 * kGsStride;
-    double* sx = sd + 32 * kGsStride;
-    const int rows = min(32, g.ny - W * 32);
+    double* sr = Pol::UPDATE ? sd + 32 * kGsStride : sd;  // where results are kept until the flush
+    const int rows = min(32, ny - W * 32);
+    const int nblk = (nx + kGsBlk - 1) / kGsBlk;
+    // REV walks the physical blocks from the last one down; the wave's clock is shifted so
+    // that lane 0 still enters a new physical block every 32 steps (i' = i + shift)
+    const int shift = Pol::REV ? nblk * kGsBlk - nx : 0;
+    const longlong2* ein = gedge + (long long)(W - 1) * epitch;
+    longlong2* eout = gedge + (long long)W * epitch;
 
-    // stage column block b of this warp's rows (lane = column within the block)
-    auto stage = [&](int b) {
-        const int col = b * kGsBlk + lane;
-        if (col < nx) {
-            const int slot = (b % kGsSlots) * kGsBlk + lane;
-            for (int rr = 0; rr < rows; ++rr) {
-                const int jr = W * 32 + rr;
-                const long long k = Pol::REV ? g.at(nx - 1 - col, g.ny - 1 - jr) : g.at(col, jr);
-                cp_async8(sd + rr * kGsStride + slot, d + k);
-                if (Pol::UPDATE) cp_async8(sx + rr * kGsStride + slot, x + k);
+    // The k-th block in sweep order covers physical columns [32 pb, 32 pb + 32), pb = k or
+    // nblk-1-k (REV), kept in slot group pb % 3 at its physical position. This lane moves the
+    // 16-byte chunks (row rr0 + 2m, column pair pp) of a block, m = 0..15.
+    const int pp = lane & 15, rr0 = lane >> 4;
+    auto chunk_row = [&](int rr) { return Pol::REV ? ny - 1 - (W * 32 + rr) : W * 32 + rr; };
+    auto stage = [&](int k) {
+        if (k < nblk) {
+            const int pb = Pol::REV ? nblk - 1 - k : k;
+            const int col = pb * kGsBlk + 2 * pp;
+            const int bytes = col + 1 < nx ? 16 : (col < nx ? 8 : 0);
+            const int slot = (pb % kGsSlots) * kGsBlk + 2 * pp;
+            if (bytes) {
+#pragma unroll 4
+                for (int m = 0; m < 16; ++m) {
+                    const int rr = rr0 + 2 * m;
+                    if (rr < rows) {
+                        const long long kk = (long long)chunk_row(rr) * g.pitch + col;
+                        cp_async16z(sd + rr * kGsStride + slot, d + kk, bytes);
+                        if (Pol::UPDATE) cp_async16z(sd + (32 + rr) * kGsStride + slot, x + kk, bytes);
+                    }
+                }
             }
         }
         cp_commit();
     };
+    // results of the k-th block (complete in shared memory) -> xo
+    auto flush = [&](int k) {
+        const int pb = Pol::REV ? nblk - 1 - k : k;
+        const int col = pb * kGsBlk + 2 * pp;
+        const int slot = (pb % kGsSlots) * kGsBlk + 2 * pp;
+        if (col < nx) {
+#pragma unroll 4
+            for (int m = 0; m < 16; ++m) {
+                const int rr = rr0 + 2 * m;
+                if (rr < rows) {
+                    const double2 v = *reinterpret_cast<const double2*>(sr + rr * kGsStride + slot);
+                    double* o = xo + (long long)chunk_row(rr) * g.pitch + col;
+                    if (col + 1 < nx) *reinterpret_cast<double2*>(o) = v;
+                    else *o = v.x;
+                }
+            }
+        }
+    };
+    // the window of edge values [c0, c0 + kGsWin) from the warp above (lanes < kGsWin)
+    auto edge_fetch = [&](int c0, double& v, bool& ok) {
+        ok = true;
+        v = 0.0;
+        if (lane < kGsWin && c0 + lane >= 0 && c0 + lane < nx) {
+            const longlong2 wd = edge_load(ein + c0 + lane);
+            v = __longlong_as_double(wd.x);
+            ok = wd.y == gen;
+        }
+    };
+
     stage(0);
     stage(1);
+    double up = 0.0, upn = 0.0;  // edge windows: current, next
+    bool upn_ok = true;
+    if (has_up) {
+        bool ok;
+        edge_fetch(-shift, up, ok);
+        while (!__all_sync(full, ok)) {
+            __nanosleep(100);
+            edge_fetch(-shift, up, ok);
+        }
+    }
     cp_wait<1>();
     __syncwarp();
 
-    double zl = 0.0, zprev = 0.0, up = 0.0;
-    int ebase = -64;
-    const int steps = nx + 31;
-    for (int tau = 0; tau < steps; ++tau) {
-        if ((tau & (kGsBlk - 1)) == 0 && tau > 0) {
-            // block tau/32 must be resident; prefetch the one after it
-            stage(tau / kGsBlk + 1);
-            cp_wait<1>();
+    // The step loop is written to compile to straight-line predicated code (one warp per
+    // scheduler pays the latency of every instruction and branch it issues): every lane
+    // executes every step on an always-valid shared-memory slot; only the result store, the
+    // edge store and the slot advance are predicated on the lane being inside its row.
+    GsOps cur{0.0, 0.0, 1.0}, nxt{0.0, 0.0, 1.0};
+    const int pjc = row_ok ? pj : (Pol::REV ? 0 : ny - 1);  // rows below the grid load row ny-1's operands
+    auto load_ops = [&](int ii, GsOps& o) {  // operands of logical column ii (clamped into the row)
+        const int ic = min(max(ii, 0), nx - 1);
+        pol.load(Pol::REV ? nx - 1 - ic : ic, pjc, o);
+    };
+    int i = -lane - shift;  // logical column of this lane at step 0
+    load_ops(i, cur);
+    double zl = 0.0, zprev = 0.0;
+    // byte offset of the logical column in hand within the lane's shared-memory row (column 0
+    // first): cyclic over kGsCols slots, forwards (backwards for REV)
+    int off;
+    {
+        const int pi = Pol::REV ? nx - 1 : 0;
+        off = 8 * (((pi / kGsBlk) % kGsSlots) * kGsBlk + (pi & (kGsBlk - 1)));
+    }
+    const unsigned a_d = static_cast<unsigned>(__cvta_generic_to_shared(sd + lane * kGsStride));
+    const unsigned a_x = static_cast<unsigned>(__cvta_generic_to_shared(sd + (32 + lane) * kGsStride));
+    const unsigned a_r = Pol::UPDATE ? a_x : a_d;
+    const bool down31 = has_down && lane == 31;
+    const bool jpos = j > 0;
+    const int steps = nx + shift + 31;
+    for (int t0 = 0; t0 < steps; t0 += kGsWin) {
+        if ((t0 & (kGsBlk - 1)) == 0 && t0 > 0) {
+            // lane 0 enters block t0/32: it must be resident; every lane has left block
+            // t0/32 - 2, whose results go out before its slots take block t0/32 + 1
+            const int kb = t0 / kGsBlk;
+            cp_wait<0>();
             __syncwarp();
+            if (kb >= 2) flush(kb - 2);
+            __syncwarp();
+            stage(kb + 1);
         }
-        const int i = tau - lane;
-        double zup = __shfl_up_sync(full, zprev, 1);
-        if (W > 0 && tau < nx) {
-            if (tau >= ebase + kGsWin) {
-                ebase = tau;
-                const int need = min(tau + kGsWin, nx);
-                if (from_global) {
-                    if (lane < kGsWin) {
-                        while (ld_acquire(gprog + (W - 1)) < need) __nanosleep(32);
-                        up = (ebase + lane < nx) ? __ldcg(gedge + (long long)(W - 1) * nx + ebase + lane) : 0.0;
-                    }
-                } else {
-                    if (lane == 0) {
-                        while (prog[w - 1] < need) __nanosleep(16);
-                    }
-                    __syncwarp();
-                    up = (lane < kGsWin && ebase + lane < nx)
-                             ? reinterpret_cast<volatile double*>(ring[w - 1])[(ebase + lane) % kGsRing]
-                             : 0.0;
-                    __syncwarp();
-                    if (lane == 0) cons[w] = ebase;  // everything before ebase has been read
+        const int c0 = t0 - shift;  // lane 0's logical column at step t0
+        if (has_up && c0 < nx) {
+            if (t0 > 0) {
+                // the window fetched one window ago; poll only if the producer was not there yet
+                while (!__all_sync(full, upn_ok)) {
+                    __nanosleep(100);
+                    edge_fetch(c0, upn, upn_ok);
                 }
-                __syncwarp();
+                up = upn;
             }
-            const double e = __shfl_sync(full, up, tau - ebase);
-            if (lane == 0) zup = e;
+            if (c0 + kGsWin < nx) edge_fetch(c0 + kGsWin, upn, upn_ok);
         }
-        double z = 0.0;
-        if (row_ok && i >= 0 && i < nx) {
-            const int slot = ((i / kGsBlk) % kGsSlots) * kGsBlk + (i & (kGsBlk - 1));
-            const double dk = sd[lane * kGsStride + slot];
-            const int pi = Pol::REV ? nx - 1 - i : i, pj = Pol::REV ? g.ny - 1 - j : j;
-            double a1, a2;
-            pol.coefs(pi, pj, a1, a2);
-            double acc = dk;
-            if (i > 0) acc = acc - a1 * zl;
-            if (j > 0) acc = acc - a2 * zup;
-            z = pol.finish(acc, pi, pj);
-            if (Pol::UPDATE) {
-                const double xk = sx[lane * kGsStride + slot];
-                xo[g.at(pi, pj)] = xk - damp * z;
-            } else {
-                xo[g.at(pi, pj)] = z;
+        // Steady windows (every lane inside its row on a column > 0 for all 16 steps; almost all
+        // of the sweep): no activity selects at all. The first and last windows take the general
+        // body. Rows without a left / upper neighbour skip that term as the reference does
+        // (i > 0, j > 0): in the steady body only lane 0 of warp 0 has none, and it subtracts
+        // a2 * (0 with a2's sign) = +0, the exact identity.
+        const bool steady = rows == 32 && c0 >= 32 && c0 + kGsWin <= nx;
+        if (steady) {
+#pragma unroll
+            for (int u = 0; u < kGsWin; ++u) {
+                const double zs = __shfl_up_sync(full, zprev, 1);
+                double e = __shfl_sync(full, up, u);
+                if (!has_up) e = copysign(0.0, cur.a2);
+                const double zup = lane == 0 ? e : zs;
+                load_ops(i + 1, nxt);  // next column's operands, one step ahead
+                const double dk = lds64(a_d + off);
+                const double t1 = cur.a1 * zl;
+                const double t2 = cur.a2 * zup;
+                const double acc = (dk - t1) - t2;
+                const double z = pol.finish(acc, cur, Pol::REV ? nx - 1 - i : i, pjc);
+                double res = z;
+                if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
+                sts64(a_r + off, res);
+                if (down31) edge_store(eout + i, z, gen);
+                if (Pol::REV) off = off == 0 ? 8 * (kGsCols - 1) : off - 8;
+                else off = off == 8 * (kGsCols - 1) ? 0 : off + 8;
+                zl = z;
+                zprev = z;
+                cur = nxt;
+                ++i;
             }
-            zl = z;
-            if (lane == 31) {
-                if (to_ring) {
-                    // back-pressure: never overwrite a slot warp w+1 has not read yet
-                    while (i - kGsRing >= cons[w + 1]) __nanosleep(16);
-                    ring[w][i % kGsRing] = z;
-                    if ((i + 1) % kGsPub == 0 || i == nx - 1) {
-                        __threadfence_block();
-                        prog[w] = i + 1;
-                    }
-                }
-                if (to_global) {
-                    gedge[(long long)W * nx + i] = z;
-                    if ((i + 1) % kGsWin == 0 || i == nx - 1) st_release(gprog + W, i + 1);
-                }
+        } else {
+#pragma unroll 1
+            for (int u = 0; u < kGsWin; ++u) {
+                const double zs = __shfl_up_sync(full, zprev, 1);
+                const double e = __shfl_sync(full, up, u);  // (0 without a warp above: unused, j == 0)
+                const double zup = lane == 0 ? e : zs;
+                const bool act = row_ok && static_cast<unsigned>(i) < static_cast<unsigned>(nx);
+                load_ops(i + 1, nxt);
+                const double dk = lds64(a_d + off);
+                double acc = dk;
+                if (i > 0) acc = acc - cur.a1 * zl;
+                if (jpos) acc = acc - cur.a2 * zup;
+                double z = pol.finish(acc, cur, Pol::REV ? nx - 1 - i : i, pjc);
+                z = act ? z : 0.0;
+                double res = z;
+                if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
+                if (act) sts64(a_r + off, res);
+                if (act && down31) edge_store(eout + i, z, gen);
+                if (Pol::REV) off = act ? (off == 0 ? 8 * (kGsCols - 1) : off - 8) : off;
+                else off = act ? (off == 8 * (kGsCols - 1) ? 0 : off + 8) : off;
+                zl = z;
+                zprev = z;
+                cur = nxt;
+                ++i;
             }
         }
-        zprev = z;
     }
     cp_wait<0>();
+    __syncwarp();
+    // the last blocks still in shared memory
+    {
+        const int kb_max = (steps - 1) / kGsBlk;  // last block boundary the loop passed (it flushed up to kb_max - 2)
+        for (int k = max(0, kb_max - 1); k < nblk; ++k) flush(k);
+    }
+    if (w == 0 && lane == 0) {
+        __threadfence();
+        if (atomicAdd(reinterpret_cast<unsigned long long*>(gstate) + 1, 1ull) == gridDim.x - 1) {
+            gstate[1] = 0;
+            __threadfence();
+            atomicAdd(reinterpret_cast<unsigned long long*>(gstate), 1ull);
+        }
+    }
 }
 
 constexpr size_t gs_smem() { return sizeof(double) * kGsWarps * 2 * 32 * kGsStride; }

@@ -254,8 +254,9 @@ struct gmg_problem {
     int nz_next = 0;
     int* nz_cur = nullptr;
     unsigned long long* ss_stats = nullptr;  // [16] exact-sum engine counters (seqsum.cuh)
-    double* gs_edge = nullptr;               // Gauss-Seidel wavefront warp-edge rows
-    int* gs_prog = nullptr;                  // and their progress counters
+    longlong2* gs_edge = nullptr;            // Gauss-Seidel wavefront warp-edge rows: {value, generation} words
+    long long* gs_state = nullptr;           // {generation, finished-CTA count} (gs.cuh)
+    int gs_epitch = 0;
     int gs_warps = 0;
     double* sums = nullptr;  // [0..1] omega sums, [2] residual norm^2, [3] misc
     int* nz = nullptr;
@@ -834,18 +835,23 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
     if (warps > p->gs_warps) throw GmgError{GMG_ERR_LOGIC, "gs: workspace too small"};
     const int blocks = (warps + kGsWarps - 1) / kGsWarps;
     if (blocks > 148) throw GmgError{GMG_ERR_UNSUPPORTED, "gs: more rows than one co-resident wavefront"};
-    CK(cudaMemsetAsync(p->gs_prog, 0, warps * sizeof(int), p->st));
-    if (g_debug_sync) dbg_sync(__LINE__);
     set_smem(k_gs_wave<Pol>, gs_smem());
     prof_tag("gs wavefront", L.l, (Pol::UPDATE ? 24.0 : 16.0) * (double)L.nx * L.ny);
     launch_k(k_gs_wave<Pol>, blocks, kGsWarps * 32, gs_smem(), p->st, L.grid(), pol, d, x, xo, damp, p->gs_edge,
-                                                                 p->gs_prog);
+             p->gs_epitch, p->gs_state);
     KCHECK();
 }
 
 // One lexicographic Gauss-Seidel/SOR smooth_step: x' = x - damp * (D + om L)^{-1} (A x - g).
 void launch_gs_wave(gmg_problem* p, const Lev& L, const double* d, const double* x, double* xo, double om,
                     double damp) {
+    if (L.kind == 0) {  // constant operator: the division form is chosen here, not per point
+        const CoefConst& A = L.cconst;
+        if (A.c_pow2) launch_wave(p, L, GsPolicy<CoefConst, 1>{A, om}, d, x, xo, damp);
+        else if (A.rcp_ok) launch_wave(p, L, GsPolicy<CoefConst, 2>{A, om}, d, x, xo, damp);
+        else launch_wave(p, L, GsPolicy<CoefConst, 0>{A, om}, d, x, xo, damp);
+        return;
+    }
     with_coef(L, [&](const auto& A) {
         using C = std::decay_t<decltype(A)>;
         launch_wave(p, L, GsPolicy<C>{A, om}, d, x, xo, damp);
@@ -1901,7 +1907,7 @@ void free_problem(gmg_problem* p) {
     dfree(p->recs2);
     dfree(p->ss_stats);
     dfree(p->gs_edge);
-    dfree(p->gs_prog);
+    dfree(p->gs_state);
     dfree(p->sums);
     dfree(p->nz);
     dfree(p->nz_slots);
@@ -2110,8 +2116,11 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
             maxnx = std::max(maxnx, Lq.nx);
         }
         p->gs_warps = (maxny + 31) / 32;
-        CK(dmalloc(&p->gs_edge, (size_t)p->gs_warps * maxnx * sizeof(double)));
-        CK(dmalloc(&p->gs_prog, p->gs_warps * sizeof(int)));
+        p->gs_epitch = (maxnx + 31) / 32 * 32;
+        CK(dmalloc(&p->gs_edge, (size_t)p->gs_warps * p->gs_epitch * sizeof(longlong2)));
+        CK(cudaMemset(p->gs_edge, 0, (size_t)p->gs_warps * p->gs_epitch * sizeof(longlong2)));
+        CK(dmalloc(&p->gs_state, 2 * sizeof(long long)));
+        CK(cudaMemset(p->gs_state, 0, 2 * sizeof(long long)));
         CK(dmalloc(&p->linebuf, 2 * (size_t)std::max(maxnx, maxny) * sizeof(double)));
         CK(cudaMemset(p->ss_stats, 0, 16 * sizeof(unsigned long long)));
         CK(dmalloc(&p->sums, 8 * sizeof(double)));
