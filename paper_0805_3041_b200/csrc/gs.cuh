@@ -13,14 +13,20 @@
 // lane r-1 by a warp shuffle (computed on the previous step). With one warp per
 // scheduler the sweep is bound by the latency of everything a step issues, so
 // the step is kept to the recurrence itself:
-//   * Operands: each warp stages its 32 rows of d and x through shared memory,
+//   * Operands: the 32 rows of d and x of a warp pass through shared memory,
 //     32 columns at a time in coalesced 16-byte cp.async chunks, three blocks
 //     deep; results go back into the same slots and leave as 16-byte stores a
-//     block at a time. The sequential loop touches shared memory only.
-//   * The row above a warp (lane 31 of the warp before) arrives through global
+//     block at a time. The sequential loop touches shared memory only, and all
+//     of the staging and flushing is done by a helper warp per compute warp
+//     (same scheduler: it issues in the compute warp's stall slots), the two
+//     meeting at a named barrier once per block.
+//   * The row above a warp (lane 31 of the warp before) arrives, inside a CTA,
+//     through a shared-memory ring of {value, column} words read a window of 16
+//     columns at a time (the consumer trails the producer by ~47 steps), and
+//     between CTAs through global
 //     memory as 16-byte {value, generation} words, one per column, stored with a
 //     single relaxed vector store and fetched 16 columns at a time one window
-//     ahead of use: no flags, fences, progress counters or shared rings. The
+//     ahead of use: no flags or fences. The
 //     generation (one per launch) tells a fresh value from the previous sweep's.
 //     A window that is not complete yet is polled when it is needed (start-up
 //     only: the consumer then trails the producer far enough).
@@ -38,8 +44,12 @@
 
 namespace gmg_dev {
 
-constexpr int kGsWarps = 4;     // warps (x 32 rows) per CTA: one per scheduler
+constexpr int kGsWarps = 4;     // compute warps (x 32 rows) per CTA: one per scheduler; as many helper warps
 constexpr int kGsWin = 16;      // edge values fetched per window
+constexpr int kGsERing = 128;   // intra-CTA edge ring (columns)
+#ifndef GMG_GS_RING
+#define GMG_GS_RING 0  // 1: hand-offs inside a CTA through a shared-memory ring (A/B variant)
+#endif
 constexpr int kGsBlk = 32;      // staged column block
 constexpr int kGsSlots = 3;     // staged blocks in flight
 constexpr int kGsCols = kGsBlk * kGsSlots;
@@ -65,6 +75,24 @@ __device__ __forceinline__ longlong2 edge_load(const longlong2* p) {
     return r;
 }
 
+// ring words {value, column}: the value is stored before its tag and the tag is read before
+// the value (volatile shared accesses of one thread stay in program order)
+// (predicated inside the asm: no branch in the step for the one lane that stores)
+__device__ __forceinline__ void ring_store(bool on, unsigned a, double z, int col) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %0, 0;\n\t"
+        "@p st.volatile.shared.f64 [%1], %2;\n\t"
+        "@p st.volatile.shared.s64 [%1+8], %3;\n\t}" ::"r"((int)on),
+        "r"(a), "d"(z), "l"((long long)col)
+        : "memory");
+}
+__device__ __forceinline__ void edge_store_if(bool on, longlong2* p, double z, long long gen) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %0, 0;\n\t"
+        "@p st.relaxed.gpu.global.v2.s64 [%1], {%2, %3};\n\t}" ::"r"((int)on),
+        "l"(p), "l"(__double_as_longlong(z)), "l"(gen)
+        : "memory");
+}
 __device__ __forceinline__ double lds64(unsigned a) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -103,7 +131,13 @@ struct GsPolicy {
     }
     __device__ __forceinline__ double finish(double acc, const GsOps& o, int i, int j) const {
         if constexpr (FIN == 1) return acc * A.inv_c;
-        else if constexpr (FIN == 2) return div_rcp(acc, A.c, A.rcp);
+        else if constexpr (FIN == 2) {
+            // branch-free quotient; the out-of-range dividend (never seen in a solve) recomputes
+            bool slow;
+            double q = div_rcp_fast(acc, A.c, A.rcp, slow);
+            if (__builtin_expect(slow, 0)) q = div_rcp(acc, A.c, A.rcp);
+            return q;
+        }
         else return div_loaded(A, acc, o.f, i, j);
     }
 };
@@ -136,10 +170,13 @@ struct IluBwdPolicy {
     __device__ __forceinline__ double finish(double acc, const GsOps& o, int, int) const { return acc / o.f; }
 };
 
+// named barrier of a compute warp and its helper (ids 1..kGsWarps; 0 is __syncthreads)
+__device__ __forceinline__ void pair_bar(int w) { asm volatile("bar.sync %0, 64;" ::"r"(w + 1) : "memory"); }
+
 // dynamic smem: kGsWarps * 2 * 32 * kGsStride doubles. gedge: [warps][epitch] edge words
 // (epitch >= nx), gstate: {generation, finished-CTA count}; both zero at allocation.
 template <class Pol>
-__global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, const double* __restrict__ d,
+__global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, const double* __restrict__ d,
                                                            const double* __restrict__ x, double* __restrict__ xo,
                                                            double damp, longlong2* __restrict__ gedge, int epitch,
                                                            long long* __restrict__ gstate) {
@@ -147,13 +184,20 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
     pdl_trigger();
     extern __shared__ __align__(16) double stg[];
     __shared__ long long s_gen;
+    // edge rings between the compute warps of this CTA: {value, column} words, 128 columns
+    // deep; cpos[w] = columns of ring[w-1] warp w has consumed (back-pressure for the producer)
+    __shared__ longlong2 ering[kGsWarps][kGsERing];
+    __shared__ volatile int cpos[kGsWarps];
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
-    const int W = blockIdx.x * kGsWarps + w;  // global warp index
+    const bool helper = (threadIdx.x >> 5) >= kGsWarps;  // warps kGsWarps.. stage and flush for warps 0..
+    const int w = (threadIdx.x >> 5) & (kGsWarps - 1);
+    const int W = blockIdx.x * kGsWarps + w;  // global (compute) warp index
     // This launch's generation = gstate[0] + 1, read once per CTA; the CTA that finishes its
     // warp 0 last (gstate[1] counts them) advances gstate[0] for the next launch. A device
     // counter, not a kernel argument: launches replayed from a CUDA graph get fresh tags too.
     if (threadIdx.x == 0) s_gen = *reinterpret_cast<volatile long long*>(gstate) + 1;
+    for (int q = threadIdx.x; q < kGsWarps * kGsERing; q += blockDim.x) (&ering[0][0])[q] = make_longlong2(0, -1);
+    if (threadIdx.x < kGsWarps) cpos[threadIdx.x] = 0;
     __syncthreads();
     const long long gen = s_gen;
     if (W * 32 >= g.ny) return;  // warp entirely below the grid (no block barriers from here on)
@@ -164,6 +208,14 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
     const unsigned full = 0xffffffffu;
     const bool has_up = W > 0;
     const bool has_down = (W + 1) * 32 < ny;
+    // the warp above / below is in this CTA (shared-memory ring) or in the previous / next one
+    // (global edge words)
+    // (GMG_GS_RING=1; measured slower than the global words for every hand-off: the two extra
+    // stores and the window polls lengthen the step from 92 to 148 cycles, and a consumer that
+    // must see a whole 16-column window trails its producer no closer than through global memory)
+    constexpr bool kRing = GMG_GS_RING != 0;
+    const bool up_ring = kRing && has_up && w > 0, up_glob = has_up && !up_ring;
+    const bool down_ring = kRing && has_down && w + 1 < kGsWarps, down_glob = has_down && !down_ring;
     double* sd = stg + (size_t)w * 2 * 32 * kGsStride;
     double* sr = Pol::UPDATE ? sd + 32 * kGsStride : sd;  // where results are kept until the flush
     const int rows = min(32, ny - W * 32);
@@ -228,11 +280,52 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
         }
     };
 
-    stage(0);
-    stage(1);
+    // the same window from the ring of the warp above in this CTA (tag = column)
+    auto ring_fetch = [&](int c0, double& v, bool& ok) {
+        ok = true;
+        v = 0.0;
+        if (lane < kGsWin && c0 + lane >= 0 && c0 + lane < nx) {
+            const int c = c0 + lane;
+            const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(&ering[w - 1][c & (kGsERing - 1)]));
+            long long vy;
+            asm volatile("ld.volatile.shared.s64 %0, [%1+8];" : "=l"(vy) : "r"(a) : "memory");
+            asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+            ok = vy == (long long)c;
+        }
+    };
+
+    const int steps = nx + shift + 31;
+    const int kb_max = (steps - 1) / kGsBlk;  // block boundaries the step loop passes
+    if (helper) {
+        // rows below the grid (last warp only) hold zeros, so their lanes run the recurrence
+        // on benign values
+        if (rows < 32) {
+            for (int q = rows * kGsStride + lane; q < 32 * kGsStride; q += 32) {
+                sd[q] = 0.0;
+                sd[32 * kGsStride + q] = 0.0;
+            }
+        }
+        stage(0);
+        stage(1);
+        cp_wait<0>();
+        pair_bar(w);  // blocks 0 and 1 are resident
+        for (int kb = 1; kb <= kb_max; ++kb) {
+            // the compute warp arrives when lane 0 enters block kb: block kb is resident (it
+            // was waited for before this warp arrived), every lane has left block kb - 2
+            pair_bar(w);
+            if (kb >= 2) flush(kb - 2);
+            __syncwarp();
+            stage(kb + 1);
+            cp_wait<0>();
+        }
+        pair_bar(w);  // the sweep is complete: the last blocks still in shared memory
+        for (int k = max(0, kb_max - 1); k < nblk; ++k) flush(k);
+        return;
+    }
+
     double up = 0.0, upn = 0.0;  // edge windows: current, next
     bool upn_ok = true;
-    if (has_up) {
+    if (up_glob) {
         bool ok;
         edge_fetch(-shift, up, ok);
         while (!__all_sync(full, ok)) {
@@ -240,8 +333,8 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
             edge_fetch(-shift, up, ok);
         }
     }
-    cp_wait<1>();
-    __syncwarp();
+    pair_bar(w);
+    const unsigned a_ring = static_cast<unsigned>(__cvta_generic_to_shared(&ering[w][0]));
 
     // The step loop is written to compile to straight-line predicated code (one warp per
     // scheduler pays the latency of every instruction and branch it issues): every lane
@@ -266,22 +359,26 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
     const unsigned a_d = static_cast<unsigned>(__cvta_generic_to_shared(sd + lane * kGsStride));
     const unsigned a_x = static_cast<unsigned>(__cvta_generic_to_shared(sd + (32 + lane) * kGsStride));
     const unsigned a_r = Pol::UPDATE ? a_x : a_d;
-    const bool down31 = has_down && lane == 31;
     const bool jpos = j > 0;
-    const int steps = nx + shift + 31;
+    const bool dg31 = down_glob && lane == 31, dr31 = down_ring && lane == 31;
     for (int t0 = 0; t0 < steps; t0 += kGsWin) {
-        if ((t0 & (kGsBlk - 1)) == 0 && t0 > 0) {
-            // lane 0 enters block t0/32: it must be resident; every lane has left block
-            // t0/32 - 2, whose results go out before its slots take block t0/32 + 1
-            const int kb = t0 / kGsBlk;
-            cp_wait<0>();
-            __syncwarp();
-            if (kb >= 2) flush(kb - 2);
-            __syncwarp();
-            stage(kb + 1);
-        }
+        // lane 0 enters block t0/32: the helper has it resident, and takes block t0/32 - 2
+        if ((t0 & (kGsBlk - 1)) == 0 && t0 > 0) pair_bar(w);
         const int c0 = t0 - shift;  // lane 0's logical column at step t0
-        if (has_up && c0 < nx) {
+        if (up_ring && c0 < nx) {
+            // this window straight from the ring (a shared-memory round trip per 16 steps)
+            bool ok;
+            ring_fetch(c0, up, ok);
+            while (!__all_sync(full, ok)) ring_fetch(c0, up, ok);
+            if (lane == 0) cpos[w] = c0;  // everything before c0 sits in registers
+        }
+        if (down_ring) {
+            // lane 31 writes columns c0-31 .. c0-16 in this window: their slots' previous
+            // columns must have been read
+            while (c0 - 16 - kGsERing >= cpos[w + 1]) {
+            }
+        }
+        if (up_glob && c0 < nx) {
             if (t0 > 0) {
                 // the window fetched one window ago; poll only if the producer was not there yet
                 while (!__all_sync(full, upn_ok)) {
@@ -297,7 +394,7 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
         // body. Rows without a left / upper neighbour skip that term as the reference does
         // (i > 0, j > 0): in the steady body only lane 0 of warp 0 has none, and it subtracts
         // a2 * (0 with a2's sign) = +0, the exact identity.
-        const bool steady = rows == 32 && c0 >= 32 && c0 + kGsWin <= nx;
+        const bool steady = c0 >= 32 && c0 + kGsWin <= nx;
         if (steady) {
 #pragma unroll
             for (int u = 0; u < kGsWin; ++u) {
@@ -313,8 +410,9 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
                 const double z = pol.finish(acc, cur, Pol::REV ? nx - 1 - i : i, pjc);
                 double res = z;
                 if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
-                sts64(a_r + off, res);
-                if (down31) edge_store(eout + i, z, gen);
+                if (row_ok) sts64(a_r + off, res);  // (rows below the grid stay zero)
+                edge_store_if(dg31, eout + i, z, gen);
+                ring_store(dr31, a_ring + ((i & (kGsERing - 1)) << 4), z, i);
                 if (Pol::REV) off = off == 0 ? 8 * (kGsCols - 1) : off - 8;
                 else off = off == 8 * (kGsCols - 1) ? 0 : off + 8;
                 zl = z;
@@ -339,7 +437,8 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
                 double res = z;
                 if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
                 if (act) sts64(a_r + off, res);
-                if (act && down31) edge_store(eout + i, z, gen);
+                edge_store_if(act && dg31, eout + i, z, gen);
+                ring_store(act && dr31, a_ring + ((i & (kGsERing - 1)) << 4), z, i);
                 if (Pol::REV) off = act ? (off == 0 ? 8 * (kGsCols - 1) : off - 8) : off;
                 else off = act ? (off == 8 * (kGsCols - 1) ? 0 : off + 8) : off;
                 zl = z;
@@ -349,13 +448,7 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
             }
         }
     }
-    cp_wait<0>();
-    __syncwarp();
-    // the last blocks still in shared memory
-    {
-        const int kb_max = (steps - 1) / kGsBlk;  // last block boundary the loop passed (it flushed up to kb_max - 2)
-        for (int k = max(0, kb_max - 1); k < nblk; ++k) flush(k);
-    }
+    pair_bar(w);  // the helper writes out the last blocks
     if (w == 0 && lane == 0) {
         __threadfence();
         if (atomicAdd(reinterpret_cast<unsigned long long*>(gstate) + 1, 1ull) == gridDim.x - 1) {
@@ -366,6 +459,7 @@ __global__ void __launch_bounds__(kGsWarps * 32) k_gs_wave(Grid g, Pol pol, cons
     }
 }
 
+constexpr int kGsThreads = 2 * kGsWarps * 32;
 constexpr size_t gs_smem() { return sizeof(double) * kGsWarps * 2 * 32 * kGsStride; }
 
 }  // namespace gmg_dev

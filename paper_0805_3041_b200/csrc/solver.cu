@@ -837,7 +837,7 @@ void launch_wave(gmg_problem* p, const Lev& L, const Pol& pol, const double* d, 
     if (blocks > 148) throw GmgError{GMG_ERR_UNSUPPORTED, "gs: more rows than one co-resident wavefront"};
     set_smem(k_gs_wave<Pol>, gs_smem());
     prof_tag("gs wavefront", L.l, (Pol::UPDATE ? 24.0 : 16.0) * (double)L.nx * L.ny);
-    launch_k(k_gs_wave<Pol>, blocks, kGsWarps * 32, gs_smem(), p->st, L.grid(), pol, d, x, xo, damp, p->gs_edge,
+    launch_k(k_gs_wave<Pol>, blocks, kGsThreads, gs_smem(), p->st, L.grid(), pol, d, x, xo, damp, p->gs_edge,
              p->gs_epitch, p->gs_state);
     KCHECK();
 }
