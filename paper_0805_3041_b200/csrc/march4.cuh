@@ -23,6 +23,17 @@
 namespace gmg_dev {
 
 constexpr int kS4W = 4;  // warps per CTA (independent strips)
+// CTAs per SM the register budgets are sized for. These kernels are latency-bound: occupancy
+// buys more than the instructions a tighter register budget costs (profiles/r02_summary.md).
+#ifndef GMG_S4_MINB
+#define GMG_S4_MINB 4
+#endif
+#ifndef GMG_R4_MINB
+#define GMG_R4_MINB 4
+#endif
+#ifndef GMG_O4_MINB
+#define GMG_O4_MINB 4
+#endif
 
 template <int SK>
 struct Smooth4Smem {
@@ -325,7 +336,7 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
 }
 
 template <int M, int SK, class Coef>
-__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? 4 : 3))
+__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? GMG_S4_MINB : 3))
     k_smooth4(Grid fg, Coef A, const double* __restrict__ u, Prolong P, OmegaSrc om, const double* __restrict__ g,
               double* __restrict__ out, double omega_damp, int seg) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
@@ -372,7 +383,7 @@ struct Resid4Smem {
 };
 
 template <bool SUM, class Coef>
-__global__ void __launch_bounds__(kS4W * 32, 4)
+__global__ void __launch_bounds__(kS4W * 32, GMG_R4_MINB)
     k_resid4(Grid fg, Coef A, const double* __restrict__ x, const double* __restrict__ e,
              const double* __restrict__ g, double* __restrict__ dout, double* __restrict__ x0out, Grid cg,
              RestrictW rw, double* __restrict__ gc, int seg) {
@@ -565,7 +576,7 @@ struct Omega4Smem {
 };
 
 template <class Coef>
-__global__ void __launch_bounds__(kS4W * 32, 4)
+__global__ void __launch_bounds__(kS4W * 32, GMG_O4_MINB)
     k_omega4(Grid fg, Coef A, Prolong P, const double* __restrict__ dd, double* __restrict__ T0,
              double* __restrict__ T1, int* __restrict__ nz, int seg) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete

@@ -1967,7 +1967,13 @@ void create_problem(const gmg_problem_desc* d, gmg_problem** out) {
         L.ny = ld.ny;
         L.w0 = 0;
         L.w1 = ld.ny;
-        L.pitch = ((ld.nx + 31) / 32) * 32;
+        // rows 256-B aligned; GMG_PITCH_PAD (multiples of 32 doubles) breaks power-of-two row
+        // strides (A/B knob: measured no gain, the HBM address hash already spreads them)
+        static const int pitch_pad = [] {
+            const char* e = getenv("GMG_PITCH_PAD");
+            return e ? (atoi(e) + 31) / 32 * 32 : 0;
+        }();
+        L.pitch = ((ld.nx + 31) / 32) * 32 + pitch_pad;
         L.off0 = (size_t)L.pitch + 32;
         L.elems = L.off0 + (size_t)(L.ny + 1) * L.pitch + 64;
         L.hx = h.x;
