@@ -154,6 +154,33 @@ def test_exact_dot_and_norm_on_device(problems, n):
         assert abs(gmg.dot(d, a, b, reduction="fast") - o.dot(a, b)) <= 1e-10 * (np.abs(a * b).sum() + 1e-300)
 
 
+def test_exact_sums_failed_speculation_and_literal_chunks(gpu):
+    """Inputs that defeat the walk's speculation (the approximate prefix lands in another
+    binade than the sequential sum) and chunks too dense in breaks to record: the chain must
+    fall back to literal re-sums and still return the left-to-right result bit for bit
+    (stencil.cpp:9-26). The engine counters prove the fallback paths ran."""
+    d = gmg.MultilevelProblem(11)
+    o = Oracle(3)
+    n = 1 << 20
+    rng = np.random.default_rng(5)
+    cancel = rng.uniform(-1, 1, n)
+    cancel[::4096] = 1e17
+    cancel[1::4096] = -1e17
+    spike = np.full(n, 2.0 ** -30)
+    spike[n // 3] = 2.0 ** 40
+    spike[2 * n // 3] = -2.0 ** 40
+    alternating = np.where(np.arange(n) % 2 == 0, 1.0, -1.0) * (1 + 2.0 ** -30 * rng.integers(0, 8, n))
+    ones = np.ones(n)
+    for name, a, want_dense in (("cancel", cancel, False), ("spike", spike, True), ("alternating", alternating, True)):
+        gmg.seqsum_stats(d, reset=True)
+        assert gmg.dot(d, a, ones) == o.dot(a, ones), name
+        assert gmg.norm_l2(d, a) == o.norm_l2(a), name
+        st = gmg.seqsum_stats(d)
+        assert st["rewalks"] > 0, (name, st)
+        if want_dense:
+            assert st["dense_chunks"] > 0, (name, st)
+
+
 def test_axpy(problems):
     d, _ = problems[0]
     x = Oracle.random_vector(1000, 1)
