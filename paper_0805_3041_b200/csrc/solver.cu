@@ -399,6 +399,20 @@ int seg_rows(int nx, int ny) {
         const char* e = getenv("GMG_SEG_MIN");
         return e ? atoi(e) : 8;
     }();
+    // GMG_SEG_FORCE="nx:seg,nx:seg": rows per segment for levels of that width (tuning sweeps)
+    static const std::map<int, int> forced = [] {
+        std::map<int, int> m;
+        if (const char* e = getenv("GMG_SEG_FORCE")) {
+            int a = 0, b = 0, nch = 0;
+            while (sscanf(e, "%d:%d%n", &a, &b, &nch) == 2) {
+                m[a] = std::max(2, b & ~1);
+                e += nch;
+                if (*e == ',') ++e;
+            }
+        }
+        return m;
+    }();
+    if (auto it = forced.find(nx); it != forced.end()) return it->second;
     const int strips = (nx + 123) / 124;
     // large levels (the warp-strip kernels): segments no shorter than seg_min_big rows, so the
     // 2M-row vertical halo of a fused smoothing launch stays a small share of the march
