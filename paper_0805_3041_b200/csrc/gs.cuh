@@ -14,8 +14,8 @@
 // scheduler the sweep is bound by the latency of everything a step issues, so
 // the step is kept to the recurrence itself:
 //   * Operands: the 32 rows of d and x of a warp pass through shared memory,
-//     32 columns at a time in coalesced 16-byte cp.async chunks, three blocks
-//     deep; results go back into the same slots and leave as 16-byte stores a
+//     16 columns at a time in coalesced 16-byte cp.async chunks, two blocks
+//     ahead; results go back into the same slots and leave as 16-byte stores a
 //     block at a time. The sequential loop touches shared memory only, and all
 //     of the staging and flushing is done by a helper warp per compute warp
 //     (same scheduler: it issues in the compute warp's stall slots), the two
@@ -30,6 +30,10 @@
 //     generation (one per launch) tells a fresh value from the previous sweep's.
 //     A window that is not complete yet is polled when it is needed (start-up
 //     only: the consumer then trails the producer far enough).
+//     Measured alternatives, both slower: a shared-memory ring for the hand-offs inside
+//     a CTA (GMG_GS_RING; the extra stores and polls lengthen the step from 92 to 148
+//     cycles), and per-column fetches 16 steps ahead with per-step validity checks
+//     (4x slower: the window-boundary register hand-over waits for the newest load).
 //   * Coefficients and the finishing operand of the next column are fetched one
 //     step ahead (table/field operators, ILU factors).
 //   * All CTAs are co-resident (grid <= 148 CTAs of kGsWarps warps), so the
@@ -50,8 +54,8 @@ constexpr int kGsERing = 128;   // intra-CTA edge ring (columns)
 #ifndef GMG_GS_RING
 #define GMG_GS_RING 0  // 1: hand-offs inside a CTA through a shared-memory ring (A/B variant)
 #endif
-constexpr int kGsBlk = 32;      // staged column block
-constexpr int kGsSlots = 3;     // staged blocks in flight
+constexpr int kGsBlk = 16;      // staged column block (= kGsWin: one helper rendezvous per window)
+constexpr int kGsSlots = 6;     // block groups: 3 the lanes span, 2 in flight, 1 being written back
 constexpr int kGsCols = kGsBlk * kGsSlots;
 constexpr int kGsStride = kGsCols + 2;  // even row stride: conflict-free diagonal reads, 16-B chunks
 
@@ -131,14 +135,16 @@ struct GsPolicy {
     }
     __device__ __forceinline__ double finish(double acc, const GsOps& o, int i, int j) const {
         if constexpr (FIN == 1) return acc * A.inv_c;
-        else if constexpr (FIN == 2) {
-            // branch-free quotient; the out-of-range dividend (never seen in a solve) recomputes
-            bool slow;
-            double q = div_rcp_fast(acc, A.c, A.rcp, slow);
-            if (__builtin_expect(slow, 0)) q = div_rcp(acc, A.c, A.rcp);
-            return q;
-        }
+        else if constexpr (FIN == 2) return div_rcp(acc, A.c, A.rcp);
         else return div_loaded(A, acc, o.f, i, j);
+    }
+    // The same quotient without a call on the path; `slow` (FIN 2: a dividend outside the
+    // range div_rcp's two FMAs are exact for, never seen in a solve) asks for finish().
+    static constexpr bool kMaySlow = FIN == 2;
+    __device__ __forceinline__ double finish_fast(double acc, const GsOps& o, int i, int j, bool& slow) const {
+        slow = false;
+        if constexpr (FIN == 2) return div_rcp_fast(acc, A.c, A.rcp, slow);
+        else return finish(acc, o, i, j);
     }
 };
 
@@ -152,6 +158,11 @@ struct IluFwdPolicy {
         o.f = 0.0;
     }
     __device__ __forceinline__ double finish(double acc, const GsOps&, int, int) const { return acc; }
+    static constexpr bool kMaySlow = false;
+    __device__ __forceinline__ double finish_fast(double acc, const GsOps&, int, int, bool& slow) const {
+        slow = false;
+        return acc;
+    }
 };
 
 template <class Coef>
@@ -168,6 +179,11 @@ struct IluBwdPolicy {
         o.f = __ldg(dp + (long long)j * pitch + i);
     }
     __device__ __forceinline__ double finish(double acc, const GsOps& o, int, int) const { return acc / o.f; }
+    static constexpr bool kMaySlow = false;
+    __device__ __forceinline__ double finish_fast(double acc, const GsOps& o, int, int, bool& slow) const {
+        slow = false;
+        return acc / o.f;
+    }
 };
 
 // named barrier of a compute warp and its helper (ids 1..kGsWarps; 0 is __syncthreads)
@@ -229,8 +245,11 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
     // The k-th block in sweep order covers physical columns [32 pb, 32 pb + 32), pb = k or
     // nblk-1-k (REV), kept in slot group pb % 3 at its physical position. This lane moves the
     // 16-byte chunks (row rr0 + 2m, column pair pp) of a block, m = 0..15.
-    const int pp = lane & 15, rr0 = lane >> 4;
-    auto chunk_row = [&](int rr) { return Pol::REV ? ny - 1 - (W * 32 + rr) : W * 32 + rr; };
+    // 16-byte chunks of a 16-column block: this lane moves (row rr0 + 4m, column pair pp), m = 0..7
+    const int pp = lane & 7, rr0 = lane >> 3;
+    const long long rstep = (Pol::REV ? -4 : 4) * g.pitch;  // global rows advance with the logical rows
+    const long long row0 = (long long)(Pol::REV ? ny - 1 - (W * 32 + rr0) : W * 32 + rr0) * g.pitch;
+    double* const srow = sd + rr0 * kGsStride;
     auto stage = [&](int k) {
         if (k < nblk) {
             const int pb = Pol::REV ? nblk - 1 - k : k;
@@ -238,14 +257,18 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
             const int bytes = col + 1 < nx ? 16 : (col < nx ? 8 : 0);
             const int slot = (pb % kGsSlots) * kGsBlk + 2 * pp;
             if (bytes) {
-#pragma unroll 4
-                for (int m = 0; m < 16; ++m) {
-                    const int rr = rr0 + 2 * m;
-                    if (rr < rows) {
-                        const long long kk = (long long)chunk_row(rr) * g.pitch + col;
-                        cp_async16z(sd + rr * kGsStride + slot, d + kk, bytes);
-                        if (Pol::UPDATE) cp_async16z(sd + (32 + rr) * kGsStride + slot, x + kk, bytes);
+                const double* pd = d + row0 + col;
+                const double* px = Pol::UPDATE ? x + row0 + col : nullptr;
+                double* ps = srow + slot;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    if (rr0 + 4 * m < rows) {
+                        cp_async16z(ps, pd, bytes);
+                        if (Pol::UPDATE) cp_async16z(ps + 32 * kGsStride, px, bytes);
                     }
+                    pd += rstep;
+                    if (Pol::UPDATE) px += rstep;
+                    ps += 4 * kGsStride;
                 }
             }
         }
@@ -257,15 +280,18 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
         const int col = pb * kGsBlk + 2 * pp;
         const int slot = (pb % kGsSlots) * kGsBlk + 2 * pp;
         if (col < nx) {
-#pragma unroll 4
-            for (int m = 0; m < 16; ++m) {
-                const int rr = rr0 + 2 * m;
-                if (rr < rows) {
-                    const double2 v = *reinterpret_cast<const double2*>(sr + rr * kGsStride + slot);
-                    double* o = xo + (long long)chunk_row(rr) * g.pitch + col;
-                    if (col + 1 < nx) *reinterpret_cast<double2*>(o) = v;
-                    else *o = v.x;
+            double* o = xo + row0 + col;
+            const double* ps = (Pol::UPDATE ? srow + 32 * kGsStride : srow) + slot;
+            double2 v[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v[m] = *reinterpret_cast<const double2*>(ps + 4 * m * kGsStride);
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                if (rr0 + 4 * m < rows) {
+                    if (col + 1 < nx) *reinterpret_cast<double2*>(o) = v[m];
+                    else *o = v[m].x;
                 }
+                o += rstep;
             }
         }
     };
@@ -307,19 +333,20 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
         }
         stage(0);
         stage(1);
-        cp_wait<0>();
-        pair_bar(w);  // blocks 0 and 1 are resident
+        stage(2);
+        cp_wait<1>();
+        pair_bar(w);  // blocks 0 and 1 are resident, block 2 is on its way
         for (int kb = 1; kb <= kb_max; ++kb) {
-            // the compute warp arrives when lane 0 enters block kb: block kb is resident (it
-            // was waited for before this warp arrived), every lane has left block kb - 2
+            // the compute warp arrives when lane 0 enters block kb (resident: it was waited
+            // for before this warp arrived at the previous rendezvous); the lanes span blocks
+            // kb-2 .. kb, so block kb-3 is complete and its group is the one after next to fill
             pair_bar(w);
-            if (kb >= 2) flush(kb - 2);
-            __syncwarp();
-            stage(kb + 1);
-            cp_wait<0>();
+            if (kb >= 3) flush(kb - 3);
+            stage(kb + 2);  // into the group block kb-4 left at the previous rendezvous
+            cp_wait<1>();   // block kb+1 has landed; kb+2 may still be in flight
         }
         pair_bar(w);  // the sweep is complete: the last blocks still in shared memory
-        for (int k = max(0, kb_max - 1); k < nblk; ++k) flush(k);
+        for (int k = max(0, kb_max - 2); k < nblk; ++k) flush(k);
         return;
     }
 
@@ -362,8 +389,8 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
     const bool jpos = j > 0;
     const bool dg31 = down_glob && lane == 31, dr31 = down_ring && lane == 31;
     for (int t0 = 0; t0 < steps; t0 += kGsWin) {
-        // lane 0 enters block t0/32: the helper has it resident, and takes block t0/32 - 2
-        if ((t0 & (kGsBlk - 1)) == 0 && t0 > 0) pair_bar(w);
+        // lane 0 enters block t0/16: the helper has it resident, and takes block t0/16 - 3
+        if (t0 > 0) pair_bar(w);
         const int c0 = t0 - shift;  // lane 0's logical column at step t0
         if (up_ring && c0 < nx) {
             // this window straight from the ring (a shared-memory round trip per 16 steps)
@@ -389,13 +416,17 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
             }
             if (c0 + kGsWin < nx) edge_fetch(c0 + kGsWin, upn, upn_ok);
         }
-        // Steady windows (every lane inside its row on a column > 0 for all 16 steps; almost all
-        // of the sweep): no activity selects at all. The first and last windows take the general
-        // body. Rows without a left / upper neighbour skip that term as the reference does
-        // (i > 0, j > 0): in the steady body only lane 0 of warp 0 has none, and it subtracts
-        // a2 * (0 with a2's sign) = +0, the exact identity.
-        const bool steady = c0 >= 32 && c0 + kGsWin <= nx;
-        if (steady) {
+        // The 16 steps of a window as straight-line code. Rows without a left / upper
+        // neighbour skip that term as the reference does (i > 0, j > 0): j = 0 is lane 0 of
+        // warp 0 only, which subtracts a2 * (0 with a2's sign) = +0, the exact identity; i = 0
+        // happens in the first two windows (START), which select on it — every warp's first
+        // 47 steps sit on the critical path of the whole sweep, so they run this body too.
+        // Lanes ahead of their row (i < 0) or past it (i >= nx) compute on benign values and
+        // store nothing. A dividend the fast quotient cannot take (kMaySlow) is voted on
+        // before anything of the step is released; the rest of the window then runs the exact
+        // rolled body below — the call it contains stays out of the hot loop.
+        auto fast_window = [&](auto tag) -> int {
+            constexpr bool START = decltype(tag)::value;
 #pragma unroll
             for (int u = 0; u < kGsWin; ++u) {
                 const double zs = __shfl_up_sync(full, zprev, 1);
@@ -406,46 +437,56 @@ __global__ void __launch_bounds__(2 * kGsWarps * 32) k_gs_wave(Grid g, Pol pol, 
                 const double dk = lds64(a_d + off);
                 const double t1 = cur.a1 * zl;
                 const double t2 = cur.a2 * zup;
-                const double acc = (dk - t1) - t2;
-                const double z = pol.finish(acc, cur, Pol::REV ? nx - 1 - i : i, pjc);
+                double acc = dk - t1;
+                if (START) acc = i > 0 ? acc : dk;
+                acc = acc - t2;
+                bool slow;
+                const double z = pol.finish_fast(acc, cur, Pol::REV ? nx - 1 - i : i, pjc, slow);
+                if (Pol::kMaySlow) {
+                    if (__any_sync(full, slow)) return u;  // nothing of step u has been released
+                }
+                const bool live = row_ok && (!START || i >= 0) && i < nx;
                 double res = z;
                 if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
-                if (row_ok) sts64(a_r + off, res);  // (rows below the grid stay zero)
-                edge_store_if(dg31, eout + i, z, gen);
-                ring_store(dr31, a_ring + ((i & (kGsERing - 1)) << 4), z, i);
-                if (Pol::REV) off = off == 0 ? 8 * (kGsCols - 1) : off - 8;
-                else off = off == 8 * (kGsCols - 1) ? 0 : off + 8;
+                if (live) sts64(a_r + off, res);  // (rows below the grid stay zero)
+                edge_store_if(live && dg31, eout + i, z, gen);
+                ring_store(live && dr31, a_ring + ((i & (kGsERing - 1)) << 4), z, i);
+                int offn;
+                if (Pol::REV) offn = off == 0 ? 8 * (kGsCols - 1) : off - 8;
+                else offn = off == 8 * (kGsCols - 1) ? 0 : off + 8;
+                off = (!START || i >= 0) ? offn : off;
                 zl = z;
                 zprev = z;
                 cur = nxt;
                 ++i;
             }
-        } else {
+            return kGsWin;
+        };
+        int u0 = c0 < 32 ? fast_window(std::true_type{}) : fast_window(std::false_type{});
 #pragma unroll 1
-            for (int u = 0; u < kGsWin; ++u) {
-                const double zs = __shfl_up_sync(full, zprev, 1);
-                const double e = __shfl_sync(full, up, u);  // (0 without a warp above: unused, j == 0)
-                const double zup = lane == 0 ? e : zs;
-                const bool act = row_ok && static_cast<unsigned>(i) < static_cast<unsigned>(nx);
-                load_ops(i + 1, nxt);
-                const double dk = lds64(a_d + off);
-                double acc = dk;
-                if (i > 0) acc = acc - cur.a1 * zl;
-                if (jpos) acc = acc - cur.a2 * zup;
-                double z = pol.finish(acc, cur, Pol::REV ? nx - 1 - i : i, pjc);
-                z = act ? z : 0.0;
-                double res = z;
-                if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
-                if (act) sts64(a_r + off, res);
-                edge_store_if(act && dg31, eout + i, z, gen);
-                ring_store(act && dr31, a_ring + ((i & (kGsERing - 1)) << 4), z, i);
-                if (Pol::REV) off = act ? (off == 0 ? 8 * (kGsCols - 1) : off - 8) : off;
-                else off = act ? (off == 8 * (kGsCols - 1) ? 0 : off + 8) : off;
-                zl = z;
-                zprev = z;
-                cur = nxt;
-                ++i;
-            }
+        for (int u = u0; u < kGsWin; ++u) {  // exact steps (after a vote only)
+            const double zs = __shfl_up_sync(full, zprev, 1);
+            const double e = __shfl_sync(full, up, u);  // (0 without a warp above: unused, j == 0)
+            const double zup = lane == 0 ? e : zs;
+            const bool act = row_ok && static_cast<unsigned>(i) < static_cast<unsigned>(nx);
+            load_ops(i + 1, nxt);
+            const double dk = lds64(a_d + off);
+            double acc = dk;
+            if (i > 0) acc = acc - cur.a1 * zl;
+            if (jpos) acc = acc - cur.a2 * zup;
+            double z = pol.finish(acc, cur, Pol::REV ? nx - 1 - i : i, pjc);
+            z = act ? z : 0.0;
+            double res = z;
+            if (Pol::UPDATE) res = lds64(a_x + off) - damp * z;
+            if (act) sts64(a_r + off, res);
+            edge_store_if(act && dg31, eout + i, z, gen);
+            ring_store(act && dr31, a_ring + ((i & (kGsERing - 1)) << 4), z, i);
+            if (Pol::REV) off = act ? (off == 0 ? 8 * (kGsCols - 1) : off - 8) : off;
+            else off = act ? (off == 8 * (kGsCols - 1) ? 0 : off + 8) : off;
+            zl = z;
+            zprev = z;
+            cur = nxt;
+            ++i;
         }
     }
     pair_bar(w);  // the helper writes out the last blocks
