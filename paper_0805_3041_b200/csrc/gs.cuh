@@ -31,7 +31,7 @@
 //     A window that is not complete yet is polled when it is needed (start-up
 //     only: the consumer then trails the producer far enough).
 //     Measured alternatives, both slower: a shared-memory ring for the hand-offs inside
-//     a CTA (the extra stores and polls lengthen the step from 92 to 148
+//     a CTA (GMG_GS_RING; the extra stores and polls lengthen the step from 92 to 148
 //     cycles), and per-column fetches 16 steps ahead with per-step validity checks
 //     (4x slower: the window-boundary register hand-over waits for the newest load).
 //   * Coefficients and the finishing operand of the next column are fetched one
