@@ -27,6 +27,12 @@ GEOMS = {
     "wide": dict(levels=3, coarse=(60, 1), coords="cartesian", alpha=0.5, beta=2.0, grading=(1.0, 1.02)),
     # 255 x 383: several wavefront CTAs, partial line blocks, lines longer than a chunk
     "tall": dict(levels=7, coarse=(1, 2), coords="cartesian", alpha=0.3, beta=1.0, grading=(1.0, 1.0)),
+    # wavefront edge cases: widths that are no multiple of the 16-column staging block (the reversed
+    # ILU wave shifts its clock), a last warp with a single row (33 rows), fewer columns than a window
+    "odd_39x15": dict(levels=4, coarse=(4, 1), coords="cartesian", alpha=0.7, beta=1.0, grading=(1.0, 1.0)),
+    "odd_47x39": dict(levels=3, coarse=(11, 9), coords="cartesian", alpha=1e-3, beta=1.0, grading=(1.0, 1.0)),
+    "odd_41x33": dict(levels=2, coarse=(20, 16), coords="cylindrical", alpha=1.0, beta=1.0, grading=(1.0, 1.0)),
+    "odd_9x65": dict(levels=2, coarse=(4, 32), coords="cartesian", alpha=1.0, beta=1.0, grading=(1.03, 1.0)),
 }
 
 
@@ -63,7 +69,8 @@ def test_smooth_step_all_kinds_every_level(problems, gi):
         n = d.n(l)
         x = Oracle.random_vector(n, 60 + l)
         b = Oracle.random_vector(n, 70 + l)
-        cases = [("richardson", 1.0), ("richardson", 1e-4), ("ilu0", 1.0), ("ilu0", 0.5)]
+        cases = [("richardson", 1.0), ("richardson", 1e-4), ("ilu0", 1.0), ("ilu0", 0.5),
+                 ("gauss_seidel", 1.0), ("sor", 1.3), ("sor", 0.4)]
         cases += [(k, w) for k in LINE_KINDS for w in (1.0, 0.6)]
         for kind, som in cases:
             for damp in (0.7, 1.0):
