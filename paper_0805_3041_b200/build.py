@@ -21,7 +21,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: no FMA contraction anywhere (bit-exact with the reference's
 # unfused x86-64 arithmetic); -ffp-contract=off for the host code likewise.
-NVFLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr", "-split-compile", "0",
+# No -split-compile: it cost 6% per C4 cycle (worse code for the streaming kernels) and made
+# builds of the same source differ by +-3% (kernel placement depends on its worker threads);
+# the library builds as parallel translation units instead (inst.h).
+# -static-global-template-stub=false: kernels instantiated in one translation unit (inst.cu) are
+# launched from another (solver.cu, extern template) through their host stubs.
+NVFLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-fmad=false", "--expt-relaxed-constexpr",
+           "-static-global-template-stub=false", "-diag-suppress", "20279,20281",
            "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-Xptxas", "-v"]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall"]
 
@@ -31,7 +37,7 @@ SOURCES_CPP = ["host_setup.cpp"]
 def _deps():
     """Every header the sources may include (all of csrc/ plus the C ABI)."""
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".hpp"))]
-    return hs + [os.path.join(ROOT, "include", "gmg_b200.h")]
+    return hs + [os.path.join(ROOT, "include", "gmg_b200.h"), os.path.abspath(__file__)]  # (flags live here)
 
 
 def _newer(target: str, sources) -> bool:
