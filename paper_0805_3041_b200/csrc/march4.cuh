@@ -25,6 +25,18 @@ namespace gmg_dev {
 constexpr int kS4W = 4;  // warps per CTA (independent strips)
 // CTAs per SM the register budgets are sized for. These kernels are latency-bound: occupancy
 // buys more than the instructions a tighter register budget costs (profiles/r02_summary.md).
+#ifndef GMG_S4_SPLIT_MINM
+#define GMG_S4_SPLIT_MINM 3  // fused step counts from which the march is split into interior / boundary paths
+#endif
+#ifndef GMG_S4_GSMEM_MINM
+#define GMG_S4_GSMEM_MINM 3   // fused step counts from which the right-hand side is re-read from a deeper ring
+#endif
+#ifndef GMG_S4_GRING_ALL
+#define GMG_S4_GRING_ALL 0  // 1: the 3-slot register ring for the right-hand side on the general path too
+#endif
+#ifndef GMG_S4_TYPRE
+#define GMG_S4_TYPRE 1  // 1: the row's prolongation weight fetched one row ahead
+#endif
 #ifndef GMG_S4_MINB
 #define GMG_S4_MINB 4
 #endif
@@ -35,10 +47,15 @@ constexpr int kS4W = 4;  // warps per CTA (independent strips)
 #define GMG_O4_MINB 4
 #endif
 
-template <int SK>
+template <int SK, int M>
 struct Smooth4Smem {
     static constexpr bool HAS_U = SK == K3_U || SK == K3_CORRECT;
     static constexpr bool HAS_C = SK == K3_PROLONG || SK == K3_CORRECT;
+    // GSMEM (M >= 3): the right-hand side of the M rows the fused steps work on is re-read
+    // from a deeper ring instead of riding in registers (a 4 x M doubles window): at their
+    // 168-register budget the 3- and 4-step kernels had spilled loop invariants and reloaded
+    // them every row (25% of the stall samples of C5's finest post-smoother; -1.6% per C5 cycle)
+    static constexpr bool GSMEM = M >= GMG_S4_GSMEM_MINM;
     // ring depth: rows in flight per warp = D-1 (a deeper ring, 8, for the sources with one
     // streamed array measured 25% slower in the cycle)
 #ifndef GMG_S4_DEEP
@@ -47,7 +64,8 @@ struct Smooth4Smem {
     static constexpr int D = HAS_U ? 4 : GMG_S4_DEEP;
     // [slot][half][lane]: lane's columns 4l..4l+1 in half 0, 4l+2..4l+3 in half 1
     // (16-B lane stride: conflict-free 128-bit accesses)
-    double2 g[D][2][32];
+    static constexpr int GD = GSMEM ? 8 : D;  // rows J-M .. J+D-1 live at once
+    double2 g[GD][2][32];
     double2 u[HAS_U ? D : 1][2][32];
     double c[HAS_C ? D : 1][68];  // coarse rows, slot = coarse row & (D-1)
 };
@@ -58,13 +76,13 @@ struct Smooth4Smem {
 // common case (all but the first/last strips and row segments). BND = true: the
 // general path with domain masks. Same arithmetic per point in both.
 template <int M, int SK, class Coef, bool BND>
-__device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg, const Coef& A,
+__device__ __forceinline__ void smooth4_march(Smooth4Smem<SK, M>& S, const Grid& fg, const Coef& A,
                                               const double* __restrict__ u, const Prolong& P, double omega,
                                               const double* __restrict__ g, double* __restrict__ out,
                                               double omega_damp, int i0, int j0, int j1) {
-    using SM = Smooth4Smem<SK>;
-    constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C;
-    constexpr int D = SM::D;
+    using SM = Smooth4Smem<SK, M>;
+    constexpr bool HAS_U = SM::HAS_U, HAS_C = SM::HAS_C, GSMEM = SM::GSMEM;
+    constexpr int D = SM::D, GD = SM::GD;
     constexpr int H = (M + 1) & ~1;  // halo columns, even: 16-B aligned strips
     constexpr int ML = M > 0 ? M : 1;
     // coarse columns are staged from the even column mS = m0 - COFF (16-B pairs)
@@ -104,18 +122,19 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
             if (COFF && lane == 1) cpa8(dst + 64, src + 64, 8);
         }
     };
+    auto gslot_of = [](int J) { return (J + 8) & (GD - 1); };
     auto stage = [&](int J) {
-        const int sl = slot_of(J);
+        const int sl = slot_of(J), gsl = gslot_of(J);
         const bool row_in = !BND || (J >= 0 && J < ny);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             if constexpr (BND) {
                 const int bytes = row_in ? (h ? cb1 : cb0) : 0;
                 const long long o = bytes ? soff + 2 * h : 0;
-                cpa16(&S.g[sl][h][lane], g + o, bytes);
+                cpa16(&S.g[gsl][h][lane], g + o, bytes);
                 if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], u + o, bytes);
             } else {
-                cpa16(&S.g[sl][h][lane], g + soff + 2 * h, 16);
+                cpa16(&S.g[gsl][h][lane], g + soff + 2 * h, 16);
                 if constexpr (HAS_U) cpa16(&S.u[sl][h][lane], u + soff + 2 * h, 16);
             }
         }
@@ -127,8 +146,19 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
         }
         cpa_commit();
     };
+#if GMG_S4_TYPRE
+    double ty_cur = (HAS_C && ((Jbeg + 1) & 1) && Jbeg >= 0 && Jbeg < ny) ? __ldg(P.ty + Jbeg) : 0.0;
+#endif
     // the source value of row J for this lane's 4 columns (zero outside the interior)
     auto source = [&](int J, int sl, double (&nv)[4]) {
+#if GMG_S4_TYPRE
+        double tyJ = 0.0;
+        if constexpr (HAS_C) {  // this row's weight was fetched an iteration ago; fetch the next row's
+            tyJ = ty_cur;
+            const int Jn = J + 1;
+            ty_cur = (((Jn + 1) & 1) && Jn >= 0 && Jn < ny) ? __ldg(P.ty + Jn) : 0.0;
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < 4; ++k) nv[k] = 0.0;
         if (BND && (J < 0 || J >= ny)) return;
@@ -146,7 +176,11 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
             const double* ca = &S.c[((even ? qf - 1 : qf) + 8) & (D - 1)][COFF + 2 * lane];
             const double* cb = &S.c[(qf + 8) & (D - 1)][COFF + 2 * lane];
             Pair2Raw r;
+#if GMG_S4_TYPRE
+            r.ty = tyJ;
+#else
             r.ty = ((J + 1) & 1) ? __ldg(P.ty + J) : 0.0;
+#endif
             r.a = ca[0];
             r.b = ca[1];
             r.c = cb[0];
@@ -199,6 +233,15 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
         }
     };
 
+    if constexpr (GSMEM) {
+        // rows before Jbeg are never staged: their slots read as zero right-hand sides
+#pragma unroll
+        for (int q = 0; q < GD; ++q) {
+            S.g[q][0][lane] = make_double2(0.0, 0.0);
+            S.g[q][1][lane] = make_double2(0.0, 0.0);
+        }
+        __syncwarp();
+    }
     if constexpr (HAS_C) {
         // coarse rows of fine rows Jbeg .. Jbeg+D-2 that stage() itself will not fetch
         // Jbeg even: floor(Jbeg/2)-1 (its pair partner comes with stage(Jbeg));
@@ -216,8 +259,8 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
     // (w) so the unrolled-by-3 row loop rotates them by renaming; gw is a 3-slot ring
     // as well when M <= 2, else a shifted window.
     double w[ML][3][4];
-    constexpr bool GRING = M <= 2 && !BND;
-    constexpr int GS = GRING ? 3 : ML + 1;
+    constexpr bool GRING = M <= 2 && (!BND || GMG_S4_GRING_ALL);
+    constexpr int GS = GSMEM ? 1 : (GRING ? 3 : ML + 1);
     double gw[GS][4];
 #pragma unroll
     for (int l = 0; l < ML; ++l)
@@ -242,15 +285,15 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
         } else {
             // g of row J into its slot (ring: slot PH; shifted window: slot 0 after the shift)
             constexpr int gJ = GRING ? PH : 0;
-            if constexpr (!GRING) {
+            if constexpr (!GSMEM) {  // (GSMEM: every step reads its row from the ring below)
+                if constexpr (!GRING) {
 #pragma unroll
-                for (int q = GS - 1; q > 0; --q)
+                    for (int q = GS - 1; q > 0; --q)
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) gw[q][k] = gw[q - 1][k];
-            }
-            {
-                const double2 a = S.g[sl][0][lane];
-                const double2 b = S.g[sl][1][lane];
+                        for (int k = 0; k < 4; ++k) gw[q][k] = gw[q - 1][k];
+                }
+                const double2 a = S.g[gslot_of(J)][0][lane];
+                const double2 b = S.g[gslot_of(J)][1][lane];
                 gw[gJ][0] = a.x;
                 gw[gJ][1] = a.y;
                 gw[gJ][2] = b.x;
@@ -265,6 +308,18 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
 #pragma unroll
                 for (int k = 0; k < 4; ++k) w[l][sn][k] = nv[k];
                 const int R = J - l - 1;
+                double gk[4];
+                if constexpr (GSMEM) {
+                    const double2 a = S.g[gslot_of(R)][0][lane];
+                    const double2 b = S.g[gslot_of(R)][1][lane];
+                    gk[0] = a.x;
+                    gk[1] = a.y;
+                    gk[2] = b.x;
+                    gk[3] = b.y;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) gk[k] = gw[gs][k];
+                }
                 const double xl = __shfl_up_sync(0xffffffffu, w[l][sc][3], 1);
                 const double xr = __shfl_down_sync(0xffffffffu, w[l][sc][0], 1);
                 double y[4];
@@ -274,7 +329,7 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
                     const double xw = k == 0 ? xl : w[l][sc][k - 1];
                     const double xe = k == 3 ? xr : w[l][sc][k + 1];
                     y[k] = jacobi_point_fast(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe, w[l][sd][k],
-                                             w[l][sn][k], gw[gs][k], omega_damp, slow[k]);
+                                             w[l][sn][k], gk[k], omega_damp, slow[k]);
                 }
                 if constexpr (Coef::kMaySlow) {
                     // one warp vote per fused step and row; the exact division only where asked
@@ -284,7 +339,7 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
                             const double xw = k == 0 ? xl : w[l][sc][k - 1];
                             const double xe = k == 3 ? xr : w[l][sc][k + 1];
                             y[k] = jacobi_point(A, cix(i + k, fg.nx), cix(R, fg.ny), w[l][sc][k], xw, xe,
-                                                w[l][sd][k], w[l][sn][k], gw[gs][k], omega_damp);
+                                                w[l][sd][k], w[l][sn][k], gk[k], omega_damp);
                         }
                     }
                 }
@@ -307,7 +362,7 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK>& S, const Grid& fg
         cpa_wait<D - 2>();  // row J+1 has landed (for this lane)
         __syncwarp();       // ... for every lane; slot of row J is free again
     };
-    if constexpr (BND && M >= 3) {
+    if constexpr (BND && M >= GMG_S4_SPLIT_MINM) {
         // the rare path (first/last strips and row segments) stays small in the instruction
         // cache: one row body, the windows shifted by moves (slot names of PH = 0)
 #pragma unroll 1
@@ -341,7 +396,7 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? GMG_S4_MINB : 3))
               double* __restrict__ out, double omega_damp, int seg) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
     pdl_trigger();
-    using SM = Smooth4Smem<SK>;
+    using SM = Smooth4Smem<SK, M>;
     constexpr int H = (M + 1) & ~1;  // halo columns, even: 16-B aligned strips
     constexpr int OW = 128 - 2 * H;  // columns each strip produces
     extern __shared__ __align__(16) unsigned char sm4raw[];
@@ -362,7 +417,7 @@ __global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? GMG_S4_MINB : 3))
     // The split pays for M >= 3 (C5's 3+3: -18% on the finest level; the one-path loop is
     // instruction-cache bound there). For M <= 2 the single general loop measured faster
     // (C4 finest post-smoother 0.336 vs 0.354 ms), so every strip takes it.
-    if (M >= 3 && interior)
+    if (M >= GMG_S4_SPLIT_MINM && interior)
         smooth4_march<M, SK, Coef, false>(S, fg, A, u, P, omega, g, out, omega_damp, i0, j0, j1);
     else
         smooth4_march<M, SK, Coef, true>(S, fg, A, u, P, omega, g, out, omega_damp, i0, j0, j1);
@@ -642,6 +697,7 @@ __global__ void __launch_bounds__(kS4W * 32, GMG_O4_MINB)
     cpa_wait<1>();
     __syncwarp();
 
+    double ty_cur = (((Jbeg + 1) & 1) && Jbeg >= 0 && Jbeg < ny) ? __ldg(P.ty + Jbeg) : 0.0;
     double cw[3][4];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
@@ -654,8 +710,13 @@ __global__ void __launch_bounds__(kS4W * 32, GMG_O4_MINB)
         constexpr int sJ = PH % 3, sJ1 = (PH + 2) % 3, sJ2 = (PH + 1) % 3;  // rows J, J-1, J-2
         stage(J + 2);
         const int sl1 = slot_of(J - 1);
-        // corr of row J
+        // corr of row J (its prolongation weight was fetched an iteration ago; fetch the next row's)
         {
+            const double tyJ = ty_cur;
+            {
+                const int Jn = J + 1;
+                ty_cur = (((Jn + 1) & 1) && Jn >= 0 && Jn < ny) ? __ldg(P.ty + Jn) : 0.0;
+            }
             double v[4] = {0.0, 0.0, 0.0, 0.0};
             if (J >= 0 && J < ny) {
                 const int qf = (J + 8) / 2 - 4;
@@ -663,7 +724,7 @@ __global__ void __launch_bounds__(kS4W * 32, GMG_O4_MINB)
                 const double* ca = &S.c[((even ? qf - 1 : qf) + 8) & (D - 1)][2 * lane];
                 const double* cb = &S.c[(qf + 8) & (D - 1)][2 * lane];
                 Pair2Raw r;
-                r.ty = ((J + 1) & 1) ? __ldg(P.ty + J) : 0.0;
+                r.ty = tyJ;
                 r.a = ca[0];
                 r.b = ca[1];
                 r.c = cb[0];
@@ -742,9 +803,9 @@ constexpr size_t resid4_smem() {
     return sizeof(Resid4Smem<SUM>) * kS4W;
 }
 
-template <int SK>
+template <int SK, int M>
 constexpr size_t smooth4_smem() {
-    return sizeof(Smooth4Smem<SK>) * kS4W;
+    return sizeof(Smooth4Smem<SK, M>) * kS4W;
 }
 
 }  // namespace gmg_dev

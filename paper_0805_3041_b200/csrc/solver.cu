@@ -423,6 +423,23 @@ int seg_rows(int nx, int ny) {
     const int smin = nx >= 255 ? seg_min_big : seg_min_small;
     int seg = 128;
     while (seg > smin && (long long)strips * ((ny + seg - 1) / seg) < target) seg /= 2;
+    // One resident wave: if longer segments make the whole grid fit the SMs at once (4 CTAs of
+    // 4 strips per SM) and nearly fill them, take them — no second-wave tail, and the 2M halo
+    // rows and the start-up latency of a segment are paid less often (4095^2: 16 -> 64 rows,
+    // -1.0% per C4 cycle, -0.3% per C5 cycle; no other level of the configs qualifies).
+    if (nx >= 255) {
+        static const long long resident = [] {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            return 4LL * sms;
+        }();
+        const long long ctax = (strips + 3) / 4;
+        for (int s2 = 128; s2 > seg; s2 /= 2) {
+            const long long n = ctax * ((ny + s2 - 1) / s2);
+            if (n <= resident && 10 * n >= 8 * resident) return s2;
+        }
+    }
     return seg;
 }
 
@@ -667,7 +684,7 @@ void launch_smooth4_t(gmg_problem* p, const Lev& L, const Coef& A, const double*
                       OmegaSrc om, const double* g, double* out, double wd) {
     constexpr int H = (M + 1) & ~1;
     constexpr int OW = 128 - 2 * H;
-    constexpr size_t smem = smooth4_smem<SK>();
+    constexpr size_t smem = smooth4_smem<SK, M>();
     set_smem(k_smooth4<M, SK, Coef>, smem);
     Prolong P{};
     if (SK == K3_PROLONG || SK == K3_CORRECT) P = prolong_from(p, L.l - 1, uc);
