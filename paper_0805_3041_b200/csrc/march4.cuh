@@ -37,6 +37,9 @@ constexpr int kS4W = 4;  // warps per CTA (independent strips)
 #ifndef GMG_S4_TYPRE
 #define GMG_S4_TYPRE 1  // 1: the row's prolongation weight fetched one row ahead
 #endif
+#ifndef GMG_S4_M3_MINB
+#define GMG_S4_M3_MINB 4  // CTAs per SM of the 3-/4-step kernels without a streamed iterate (their smem allows 4)
+#endif
 #ifndef GMG_S4_MINB
 #define GMG_S4_MINB 4
 #endif
@@ -391,7 +394,8 @@ __device__ __forceinline__ void smooth4_march(Smooth4Smem<SK, M>& S, const Grid&
 }
 
 template <int M, int SK, class Coef>
-__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? GMG_S4_MINB : 3))
+__global__ void __launch_bounds__(kS4W * 32, (M <= 2 ? GMG_S4_MINB
+                                                         : ((SK == K3_ZERO || SK == K3_PROLONG) ? GMG_S4_M3_MINB : 3)))
     k_smooth4(Grid fg, Coef A, const double* __restrict__ u, Prolong P, OmegaSrc om, const double* __restrict__ g,
               double* __restrict__ out, double omega_damp, int seg) {
     pdl_wait();  // programmatic dependent launch: inputs of the previous kernel are complete
