@@ -171,7 +171,8 @@ int gmg_dev_level_window(const gmg_problem* p, int level, int* w0, int* w1);
 
 /* ---- the hot path ---------------------------------------------------------- */
 /* gmg::solve: b read, x_inout carries the start vector in and the solution out.
- * Host pointers (nx*ny doubles, reference layout). */
+ * Host pointers (nx*ny doubles, reference layout); pinned, registered or pageable
+ * (large pageable vectors are staged through a pinned ring by a few host threads). */
 int gmg_dev_solve(gmg_problem* p, const gmg_cycle_desc* spec, const double* b, double* x_inout,
                   gmg_solve_report* report);
 /* Same, with b and x already resident on the device (reference layout, nx*ny

@@ -25,6 +25,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gmg_b200.h"
@@ -62,6 +63,19 @@ struct GmgError {
 // after a launch: the launch error, and with GMG_DEBUG_SYNC the kernel's own
 // completion status (debugging: pinpoints a faulting launch by line)
 static const bool g_debug_sync = getenv("GMG_DEBUG_SYNC") != nullptr;
+// GMG_NO_STAGE=1: pageable host vectors go through the runtime's own pageable copy (A/B knob)
+static const bool g_no_stage = getenv("GMG_NO_STAGE") != nullptr;
+// staged transfers of pageable host vectors (staged_rows)
+constexpr int kStageThreads = 8, kStageSlots = 2;
+// host threads that copy: GMG_STAGE_THREADS, default half the host's cores up to 8
+// (C4 round trip of 1.6 GB on a 16-core box: 2/4/6/8 threads = 92/64/51/46 ms; pinned buffers 29 ms)
+static const int g_stage_threads = [] {
+    const char* e = getenv("GMG_STAGE_THREADS");
+    const int n = e ? atoi(e) : (int)std::thread::hardware_concurrency() / 2;
+    return std::max(1, std::min(kStageThreads, n));
+}();
+constexpr size_t kStageBytes = 4u << 20;  // per slot
+constexpr size_t kStageMin = 32u << 20;   // smaller vectors take the plain copy
 inline void dbg_sync(int line) {
     const cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess)
@@ -262,6 +276,8 @@ struct gmg_problem {
     int* nz = nullptr;
     int* status = nullptr;
     double* hostbuf = nullptr;  // pinned: {norm^2, status}
+    char* stage = nullptr;      // pinned ring for pageable host vectors (staged_rows), allocated on first use
+    cudaEvent_t stage_ev[kStageThreads * kStageSlots] = {};
     std::map<std::string, std::array<cudaGraphExec_t, 2>> graphs;
     std::map<std::pair<int, unsigned long long>, SmSetup> smsetups;  // (kind, omega bits)
     double* linebuf = nullptr;  // k_gstri scratch: 2 x max(nx, ny)
@@ -1627,14 +1643,96 @@ void check_cycle(const gmg_problem* p, const gmg_cycle_desc& sp) {
     if (sp.cycle < 0 || sp.cycle > 2) throw std::invalid_argument("cycle: must be one of V, W, F");
 }
 
+// Transfers of pageable host vectors (the C++ shim passes std::vector storage, and
+// gmg::solve's b and x are such vectors): staged through a small pinned ring by a few
+// host threads, so the host copy of one chunk of rows overlaps the DMA of the previous
+// ones. The CUDA runtime's own pageable path runs at about a fifth of the link rate.
+// Pinned or registered buffers, and small ones, go straight to the copy engine.
+bool host_pageable(const void* h) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+void staged_rows(gmg_problem* p, const Lev& L, double* dev, double* host, bool to_device) {
+    if (!p->stage) {
+        CK(cudaHostAlloc(&p->stage, (size_t)kStageThreads * kStageSlots * kStageBytes, cudaHostAllocDefault));
+        for (auto& e : p->stage_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const size_t rowb = (size_t)L.nx * sizeof(double);
+    const int rows_per = (int)std::max<size_t>(1, kStageBytes / rowb);
+    if (rowb > kStageBytes) throw GmgError{GMG_ERR_LOGIC, "staged copy: row longer than a staging slot"};
+    const int nchunks = (L.ny + rows_per - 1) / rows_per;
+    const int T = std::min(g_stage_threads, nchunks);
+    std::exception_ptr err[kStageThreads];
+    auto work = [&](int t) {
+        try {
+            CK(cudaSetDevice(p->device));
+            auto slot = [&](int s) { return p->stage + ((size_t)t * kStageSlots + s) * kStageBytes; };
+            auto ev = [&](int s) { return p->stage_ev[t * kStageSlots + s]; };
+            auto rows0 = [&](int k) { return (t + k * T) * rows_per; };
+            auto nrows = [&](int k) { return std::min(rows_per, L.ny - rows0(k)); };
+            const int mine = (nchunks - t + T - 1) / T;
+            if (to_device) {
+                for (int k = 0; k < mine; ++k) {
+                    const int s = k % kStageSlots;
+                    CK(cudaEventSynchronize(ev(s)));  // the DMA that last read this slot (any earlier call too)
+                    std::memcpy(slot(s), host + (size_t)rows0(k) * L.nx, nrows(k) * rowb);
+                    CK(cudaMemcpy2DAsync(dev + (size_t)rows0(k) * L.pitch, L.pitch * sizeof(double), slot(s), rowb, rowb,
+                                         nrows(k), cudaMemcpyHostToDevice, p->st));
+                    CK(cudaEventRecord(ev(s), p->st));
+                }
+            } else {
+                auto issue = [&](int k) {
+                    const int s = k % kStageSlots;
+                    CK(cudaMemcpy2DAsync(slot(s), rowb, dev + (size_t)rows0(k) * L.pitch, L.pitch * sizeof(double), rowb,
+                                         nrows(k), cudaMemcpyDeviceToHost, p->st));
+                    CK(cudaEventRecord(ev(s), p->st));
+                };
+                for (int k = 0; k < std::min(mine, kStageSlots); ++k) issue(k);
+                for (int k = 0; k < mine; ++k) {
+                    const int s = k % kStageSlots;
+                    CK(cudaEventSynchronize(ev(s)));
+                    std::memcpy(host + (size_t)rows0(k) * L.nx, slot(s), nrows(k) * rowb);
+                    if (k + kStageSlots < mine) issue(k + kStageSlots);
+                }
+            }
+        } catch (...) {
+            err[t] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    for (int t = 0; t < T; ++t)
+        if (err[t]) std::rethrow_exception(err[t]);
+}
+
+bool stage_this(const Lev& L, const void* host, cudaMemcpyKind kind) {
+    return (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) && !g_no_stage &&
+           (size_t)L.nx * L.ny * sizeof(double) >= kStageMin && host_pageable(host);
+}
+
 void upload(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
-    CK(cudaMemcpy2DAsync(dst, L.pitch * sizeof(double), src, L.nx * sizeof(double), L.nx * sizeof(double),
-                         L.ny, kind, p->st));
+    if (stage_this(L, src, kind)) {
+        staged_rows(p, L, dst, const_cast<double*>(src), true);
+    } else {
+        CK(cudaMemcpy2DAsync(dst, L.pitch * sizeof(double), src, L.nx * sizeof(double), L.nx * sizeof(double),
+                             L.ny, kind, p->st));
+    }
     if (g_debug_sync) dbg_sync(__LINE__);
 }
 void download(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
-    CK(cudaMemcpy2DAsync(dst, L.nx * sizeof(double), src, L.pitch * sizeof(double), L.nx * sizeof(double),
-                         L.ny, kind, p->st));
+    if (stage_this(L, dst, kind)) {
+        staged_rows(p, L, const_cast<double*>(src), dst, false);
+    } else {
+        CK(cudaMemcpy2DAsync(dst, L.nx * sizeof(double), src, L.pitch * sizeof(double), L.nx * sizeof(double),
+                             L.ny, kind, p->st));
+    }
     if (g_debug_sync) dbg_sync(__LINE__);
 }
 
@@ -1944,6 +2042,9 @@ void free_problem(gmg_problem* p) {
     dfree(p->nz_slots);
     dfree(p->status);
     if (p->hostbuf) cudaFreeHost(p->hostbuf);
+    if (p->stage) cudaFreeHost(p->stage);
+    for (auto e : p->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->st && p->owns_stream) cudaStreamDestroy(p->st);

@@ -390,3 +390,30 @@ def test_jacobi_division_paths_edge_values(gpu, alpha):
         got = gmg.mg_cycle(d, levels, xo, bo, gmg.CycleSpec(**spec))
         want = o.mg_cycle(OSpec(**spec), levels, xo, bo)
         assert bits_equal(got, want), (steps, first_mismatch(got, want))
+
+
+def test_pageable_vectors_staged_like_pinned(gpu):
+    """gmg_dev_solve takes pageable host vectors (the shim's std::vector storage) through the
+    pinned staging ring (solver.cu staged_rows, vectors >= 32 MB) and pinned ones straight to
+    the copy engine: same history and the same x, bit for bit, on a rectangular grid whose
+    rows do not fill the last chunk; the random start vector travels in, so both directions
+    are covered."""
+    import torch
+    d = gmg.MultilevelProblem(8, 19, 13, (1.0, 1.0), "cartesian", 1.0, 0.3)
+    n = d.n(8)
+    assert n * 8 >= 32 << 20
+    b = gmg.random_vector(n, 5)
+    x0 = gmg.random_vector(n, 6)
+    spec = gmg.CycleSpec(tolerance=1e-6, max_cycles=3, smoother="jacobi", smoothing_omega=0.7,
+                         pre_steps=1, post_steps=1, cycle="F", adaptive_correction=True)
+    xs = x0.copy()
+    rs = gmg.solve(d, b, spec, xs)
+    pb = torch.from_numpy(b).pin_memory()
+    px = torch.from_numpy(x0.copy()).pin_memory()
+    rp = gmg.solve(d, pb.numpy(), spec, px.numpy())
+    assert bits_equal(rs.residual_history, rp.residual_history)
+    assert bits_equal(xs, px.numpy())
+    # zero cycles: x comes back exactly as it went in
+    xr = x0.copy()
+    gmg.solve(d, b, gmg.CycleSpec(tolerance=1e-6, max_cycles=0, smoother="jacobi", smoothing_omega=0.7), xr)
+    assert bits_equal(xr, x0)
