@@ -503,10 +503,11 @@ def run_ours(args):
     # the drop-in C++ shim passes pageable std::vector memory: the same call on pageable buffers
     e2e_pageable = None
     if rank == 0 and ws == 1:
-        xp = x0_host.copy()
-        t0 = time.perf_counter()
-        r = gmg.solve(prob, b_host, e2e_spec, xp)
-        e2e_pageable = n * r.iterations / (time.perf_counter() - t0)
+        for _ in range(2):  # the first call allocates the library's pinned staging ring: warm-up
+            xp = x0_host.copy()
+            t0 = time.perf_counter()
+            r = gmg.solve(prob, b_host, e2e_spec, xp)
+            e2e_pageable = n * r.iterations / (time.perf_counter() - t0)
     del pin_b, pin_x
 
     c5 = None
@@ -547,7 +548,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": n * 8 + 8 * 51, "cycles_per_step": e2e_cycles / e2e_steps,
                     "pageable_value": e2e_pageable,
                     "note": "gmg_dev_solve on pinned host buffers to the reference tolerance (pageable_value: the "
-                            "same call on pageable numpy buffers, as the C++ shim passes std::vector memory)"},
+                            "same call on pageable numpy buffers, as the C++ shim passes std::vector memory; staged "
+                            "through the library's pinned ring by host threads, second call)"},
             "gpu_launches": (per_cycle or 0) * args.steps + 9,
             "clocks": clk.summary(),
         }
