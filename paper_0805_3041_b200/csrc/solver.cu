@@ -277,6 +277,7 @@ struct gmg_problem {
     int* status = nullptr;
     double* hostbuf = nullptr;  // pinned: {norm^2, status}
     char* stage = nullptr;      // pinned ring for pageable host vectors (staged_rows), allocated on first use
+    bool stage_failed = false;  // the host refused to pin the ring: plain pageable copies
     cudaEvent_t stage_ev[kStageThreads * kStageSlots] = {};
     std::map<std::string, std::array<cudaGraphExec_t, 2>> graphs;
     std::map<std::pair<int, unsigned long long>, SmSetup> smsetups;  // (kind, omega bits)
@@ -1657,14 +1658,25 @@ bool host_pageable(const void* h) {
     return a.type == cudaMemoryTypeUnregistered;
 }
 
-void staged_rows(gmg_problem* p, const Lev& L, double* dev, double* host, bool to_device) {
-    if (!p->stage) {
-        CK(cudaHostAlloc(&p->stage, (size_t)kStageThreads * kStageSlots * kStageBytes, cudaHostAllocDefault));
-        for (auto& e : p->stage_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+// The ring, allocated on first use. A host that cannot pin 64 MB (locked-memory limits) keeps
+// the runtime's pageable copy: slower, never wrong.
+bool stage_ready(gmg_problem* p) {
+    if (p->stage) return true;
+    if (p->stage_failed) return false;
+    if (cudaHostAlloc(&p->stage, (size_t)kStageThreads * kStageSlots * kStageBytes, cudaHostAllocDefault) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        p->stage = nullptr;
+        p->stage_failed = true;
+        return false;
     }
+    for (auto& e : p->stage_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return true;
+}
+
+void staged_rows(gmg_problem* p, const Lev& L, double* dev, double* host, bool to_device) {
     const size_t rowb = (size_t)L.nx * sizeof(double);
     const int rows_per = (int)std::max<size_t>(1, kStageBytes / rowb);
-    if (rowb > kStageBytes) throw GmgError{GMG_ERR_LOGIC, "staged copy: row longer than a staging slot"};
     const int nchunks = (L.ny + rows_per - 1) / rows_per;
     const int T = std::min(g_stage_threads, nchunks);
     std::exception_ptr err[kStageThreads];
@@ -1712,13 +1724,14 @@ void staged_rows(gmg_problem* p, const Lev& L, double* dev, double* host, bool t
         if (err[t]) std::rethrow_exception(err[t]);
 }
 
-bool stage_this(const Lev& L, const void* host, cudaMemcpyKind kind) {
+bool stage_this(gmg_problem* p, const Lev& L, const void* host, cudaMemcpyKind kind) {
     return (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) && !g_no_stage &&
-           (size_t)L.nx * L.ny * sizeof(double) >= kStageMin && host_pageable(host);
+           (size_t)L.nx * L.ny * sizeof(double) >= kStageMin && (size_t)L.nx * sizeof(double) <= kStageBytes &&
+           host_pageable(host) && stage_ready(p);
 }
 
 void upload(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
-    if (stage_this(L, src, kind)) {
+    if (stage_this(p, L, src, kind)) {
         staged_rows(p, L, dst, const_cast<double*>(src), true);
     } else {
         CK(cudaMemcpy2DAsync(dst, L.pitch * sizeof(double), src, L.nx * sizeof(double), L.nx * sizeof(double),
@@ -1727,7 +1740,7 @@ void upload(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMe
     if (g_debug_sync) dbg_sync(__LINE__);
 }
 void download(gmg_problem* p, const Lev& L, double* dst, const double* src, cudaMemcpyKind kind) {
-    if (stage_this(L, dst, kind)) {
+    if (stage_this(p, L, dst, kind)) {
         staged_rows(p, L, const_cast<double*>(src), dst, false);
     } else {
         CK(cudaMemcpy2DAsync(dst, L.nx * sizeof(double), src, L.pitch * sizeof(double), L.nx * sizeof(double),
